@@ -1,0 +1,110 @@
+"""Pin the C oracle (oracle/fastsum_oracle.c) against the reference's goldens.
+
+CPU only.  The oracle is the checker for every GPU parity test, so it must
+reproduce the imported reference bit for bit first (coulomb/winding; the
+smooth kernel within a few ulp because exp() may differ in the last bit).
+"""
+
+import numpy as np
+import pytest
+
+from golden_data import TREE_KEYS, arrays, case_id, digest, meta, parse_sto
+from oracle import oracle as O
+import scenes
+
+KINDS = {"coulomb": 0, "winding_dipole": 1, "smooth_exp": 2}
+
+
+@pytest.mark.parametrize("case", meta()["small_trees"], ids=case_id)
+def test_oracle_small_trees_bitwise(case):
+    A = arrays()
+    pre = case["prefix"]
+    t = O.build_tree(A[pre + "in_positions"], A[pre + "in_masses"], A[pre + "in_weights"],
+                     case["d"], case["max_depth"])
+    for k in TREE_KEYS:
+        np.testing.assert_array_equal(t[k], A[pre + k], err_msg=k)
+        assert t[k].dtype == A[pre + k].dtype, k
+
+
+@pytest.mark.parametrize("case", meta()["large_trees"], ids=case_id)
+def test_oracle_large_trees_digest(case):
+    s = scenes.build_sources(case)
+    for k in ("positions", "masses", "weights"):
+        assert digest(getattr(s, k)) == case["inputs"][k], f"input regenerator drift: {k}"
+    t = O.build_tree(s.positions, s.masses, s.weights, case["d"], case["max_depth"])
+    for k in TREE_KEYS:
+        assert digest(t[k]) == case["arrays"][k], k
+
+
+def test_oracle_rng_keys_and_draws():
+    for e in meta()["rng"]["keys"]:
+        args = [int(a) for a in e["args"]]
+        key = O.stream_key(*args)
+        assert key == int(e["key"])
+        got = [O.uniform_draw(key, c) for c in range(8)] + [O.uniform_draw(key, 2 ** 64 - 1)]
+        assert got == e["draws"]
+
+
+def test_np_pairwise_sum_replica():
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        n = int(rng.integers(1, 600))
+        a = rng.normal(size=n) * np.exp(5 * rng.normal(size=n))
+        assert O.np_sum(a) == float(a.sum())
+
+
+def _core_inputs(entry):
+    A = arrays()
+    pre = entry["prefix"]
+    return (A[pre + "positions"], A[pre + "masses"], A[pre + "weights"], A[pre + "queries"],
+            KINDS[entry["kernel"]], entry.get("alpha", 200.0))
+
+
+def _assert_close(got, ref, kernel, what):
+    if kernel == "smooth_exp":
+        np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-300, err_msg=what)
+    else:
+        np.testing.assert_array_equal(got, ref, err_msg=what)
+
+
+@pytest.mark.parametrize("entry", meta()["cores"], ids=lambda e: e["prefix"])
+def test_oracle_cores_match_reference(entry):
+    A = arrays()
+    pre = entry["prefix"]
+    pos, ms, w, q, kid, alpha = _core_inputs(entry)
+    n = q.shape[0]
+    out = np.zeros(n)
+    O.brute_force_batch(kid, alpha, 1e-12, pos, ms, q, out)
+    _assert_close(out, A[pre + "brute"], entry["kernel"], "brute")
+    md = entry.get("max_depth", 32)
+    for d in (2, 4):
+        t = O.build_tree(pos, ms, w, d, md)
+        ca = O.core_arrays(t)
+        for run in entry["runs"]:
+            if not run.endswith(f"_d{d}") and f"_d{d}_" not in run:
+                continue
+            out = np.zeros(n)
+            vis = np.zeros(n, dtype=np.int64)
+            if run.startswith("bh_"):
+                beta = float(run.split("_b")[-1])
+                O.barnes_hut_batch(*ca, kid, alpha, 1e-12, q, beta, (md + 2) * d ** 3 + 8, out, vis)
+                _assert_close(out, A[pre + run], entry["kernel"], run)
+                np.testing.assert_array_equal(vis, A[pre + run + "_visited"])
+            elif run.startswith("tel_"):
+                O.telescoping_batch(*ca, kid, alpha, 1e-12, q, out, vis)
+                _assert_close(out, A[pre + run], entry["kernel"], run)
+                np.testing.assert_array_equal(vis, A[pre + run + "_visited"])
+            elif run.startswith("sto_"):
+                S, rr, seed, off = parse_sto(run)
+                st = np.zeros(n, dtype=np.int64)
+                pc = np.zeros(n, dtype=np.int64)
+                O.stochastic_batch(*ca, kid, alpha, 1e-12, q, S, rr, seed, off, out, vis, st, pc)
+                _assert_close(out, A[pre + run], entry["kernel"], run)
+                np.testing.assert_array_equal(vis, A[pre + run + "_visited"])
+                np.testing.assert_array_equal(st, A[pre + run + "_steps"])
+                np.testing.assert_array_equal(pc, A[pre + run + "_count"])
+            elif run.startswith("mom_"):
+                var = np.zeros(n)
+                O.stochastic_moments_batch(*ca, kid, alpha, 1e-12, q, 50, 0, 7, out, var)
+                _assert_close(out, A[pre + run + "_mean"], entry["kernel"], run)
+                _assert_close(var, A[pre + run + "_var"], entry["kernel"], run + " var")
