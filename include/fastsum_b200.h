@@ -1,0 +1,116 @@
+/*
+ * fastsum_b200.h -- C ABI of the B200 stochastic Barnes-Hut hot path.
+ *
+ * Every entry point replaces one call the reference package makes into its
+ * numba cores or tree builder (paths relative to
+ * /root/reference/pkg/src/fastsum/).  All array pointers are DEVICE pointers
+ * (cudaMalloc / torch CUDA tensors), C-contiguous, FP64 unless stated; outputs
+ * are caller-allocated and written in place, exactly like the reference cores.
+ * `stream` is a cudaStream_t (NULL = legacy default stream); work is
+ * stream-ordered and the call returns without synchronising unless noted.
+ *
+ * Return value: 0 = ok, 1 = invalid argument, 2 = CUDA error;
+ * fsb_last_error() returns a thread-local message for the last failure.
+ *
+ * Kernel ids follow kernels.py:34-38 (0 coulomb, 1 winding_dipole,
+ * 2 smooth_exp); rr modes follow _core.py:25-27 (0 paper_ratio,
+ * 1 fixed_half, 2 disabled); precision 0 = "f64" (bitwise parity mode),
+ * 1 = "f32" (FP32 terms, FP64 accumulation; outputs are float).
+ */
+#ifndef FASTSUM_B200_H
+#define FASTSUM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fsb_tree fsb_tree; /* opaque device-resident tree */
+
+int fsb_abi_version(void);
+const char *fsb_last_error(void);
+
+/* brute_force_batch(kid, alpha, dfloor, pts, ms, queries, out) -- _core.py:80-98.
+ * pts (m,3), ms (m,c), queries (n,3); out (n,) double (precision 0) or float (1). */
+int fsb_brute_force_batch(int kid, double alpha, double dfloor, int precision,
+                          const double *pts, const double *ms, int64_t m, int c,
+                          const double *queries, int64_t n, void *out, void *stream);
+
+/* Ground-truth helper for large problems: FP32 terms, FP64 accumulation, out double. */
+int fsb_brute_force_f32acc64(int kid, double alpha, double dfloor, const double *pts,
+                             const double *ms, int64_t m, int c, const double *queries,
+                             int64_t n, double *out, void *stream);
+
+/* build_tree(sources, branching_per_dim, max_depth) -- octree.py:118-239.
+ * positions (m,3), masses (m,c), weights (m,).  Synchronises `stream`. */
+int fsb_build_tree(const double *positions, const double *masses, const double *weights,
+                   int64_t m, int c, int branching_per_dim, int max_depth, fsb_tree **out,
+                   void *stream);
+
+/* A tree from the positional bundle of Octree.core_arrays() (octree.py:110-115),
+ * i.e. what a caller of _core.*_batch passes (bbox_min is unused by every core).
+ * int64 index arrays, as the reference's.  Synchronises `stream`. */
+int fsb_tree_from_core_arrays(const double *diameter, const double *aggregate_mass,
+                              const double *center_of_mass, const int64_t *child_start,
+                              const int64_t *child_count, const int64_t *child_index,
+                              const int64_t *begin, const int64_t *end, const double *points,
+                              const double *masses, int64_t num_nodes, int64_t num_points,
+                              int channels, fsb_tree **out, void *stream);
+
+/* info[0..7] = num_nodes, num_points, channels, branching, max_depth, depth_levels,
+ *              root child count, has_export (1 if built by fsb_build_tree). */
+int fsb_tree_info(const fsb_tree *tree, int64_t *info);
+
+/* Copy the 16 reference-layout arrays (octree.py:61-67 order, minus the two
+ * scalars) into caller buffers (device or pinned host: cudaMemcpyDefault):
+ * bbox_min, bbox_max, diameter, aggregate_mass, aggregate_weight,
+ * center_of_mass, child_start, child_count, child_index, begin, end, depth,
+ * permuted_indices, points, masses, weights.  Synchronises `stream`. */
+int fsb_tree_export(const fsb_tree *tree, void *const *dst, void *stream);
+
+int fsb_tree_free(fsb_tree *tree);
+
+/* barnes_hut_batch(*core, kid, alpha, dfloor, queries, beta, stack_cap, out, visited)
+ * -- _core.py:101-129.  qperm (optional, may be NULL): evaluation order of the
+ * queries (a permutation of 0..n-1); results land at the original indices.
+ * visited (optional) int64 (n,). */
+int fsb_barnes_hut_batch(fsb_tree *tree, int kid, double alpha, double dfloor, int precision,
+                         const double *queries, int64_t n, const int32_t *qperm, double beta,
+                         void *out, int64_t *visited, void *stream);
+
+/* stochastic_batch(*core, kid, alpha, dfloor, queries, n_samples, rr_mode, seed,
+ * query_offset, out, visited, path_steps, path_count) -- _core.py:215-267.
+ * RNG streams are keyed on (seed, query index + query_offset, subdomain, sample). */
+int fsb_stochastic_batch(fsb_tree *tree, int kid, double alpha, double dfloor, int precision,
+                         const double *queries, int64_t n, const int32_t *qperm,
+                         int64_t n_samples, int rr_mode, uint64_t seed, int64_t query_offset,
+                         void *out, int64_t *visited, int64_t *path_steps,
+                         int64_t *path_count, void *stream);
+
+/* stochastic_moments_batch(*core, kid, alpha, dfloor, queries, n_reps, rr_mode, seed,
+ * mean_out, var_out) -- _core.py:270-336.  FP64 only. */
+int fsb_stochastic_moments_batch(fsb_tree *tree, int kid, double alpha, double dfloor,
+                                 const double *queries, int64_t n, int64_t n_reps,
+                                 int rr_mode, uint64_t seed, double *mean_out, double *var_out,
+                                 void *stream);
+
+/* telescoping_batch(*core, kid, alpha, dfloor, queries, out, visited) -- _core.py:132-156. */
+int fsb_telescoping_batch(fsb_tree *tree, int kid, double alpha, double dfloor, int precision,
+                          const double *queries, int64_t n, void *out, int64_t *visited,
+                          void *stream);
+
+/* Spatially coherent evaluation order for queries (3-D Morton code over the
+ * query bounding box, stable): perm_out (n,) int32.  Result-invariant (F8). */
+int fsb_query_order(const double *queries, int64_t n, int32_t *perm_out, void *stream);
+
+/* post_transform (kernels.py:110-122) applied to raw sums: smooth != 0 gives
+ * -ln(raw)/alpha with (+inf, flagged) for raw <= 0; otherwise values = raw.
+ * raw is float (raw_is_f32 = 1) or double; raw64 (optional) receives raw as double. */
+int fsb_post_transform(const void *raw, int raw_is_f32, int64_t n, int smooth, double alpha,
+                       double *values, double *raw64, uint8_t *flagged, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTSUM_B200_H */

@@ -1,0 +1,733 @@
+// fs_eval.cu -- the evaluators: brute force, Barnes-Hut, stochastic, moments, telescoping.
+//
+// F64 = parity flavour (bitwise with the reference's numba cores for coulomb and
+// winding); F32 = FP32 inputs/terms with FP64 accumulation (the reference's
+// precision="f32" contract, estimators.py:270-298), MUFU fast math for terms.
+#include <algorithm>
+#include <type_traits>
+
+#include "fs_common.cuh"
+#include "fs_eval.h"
+#include "fs_internal.h"
+
+namespace fsb {
+
+template <bool F64>
+struct Prec;
+template <>
+struct Prec<true> {
+  using T = double;
+  using V4 = double4;
+  using Out = double;
+};
+template <>
+struct Prec<false> {
+  using T = float;
+  using V4 = float4;
+  using Out = float;
+};
+
+__device__ __forceinline__ void load_query(const double* __restrict__ q, int64_t qi, double& x,
+                                           double& y, double& z) {
+  x = q[3 * qi];
+  y = q[3 * qi + 1];
+  z = q[3 * qi + 2];
+}
+
+// term of one aggregate / point (contribution_rows)
+template <int KID, bool F64>
+__device__ __forceinline__ double term(const typename Prec<F64>::V4& g,
+                                       const typename Prec<F64>::V4& mm, double qx, double qy,
+                                       double qz, const KParams& kp) {
+  if constexpr (F64) {
+    return contrib_parity<KID>(mm.x, mm.y, mm.z, g.x, g.y, g.z, qx, qy, qz, kp);
+  } else {
+    return (double)contrib_fast<KID>(mm.x, mm.y, mm.z, g.x, g.y, g.z, (float)qx, (float)qy,
+                                     (float)qz, kp);
+  }
+}
+
+template <bool F64>
+__device__ __forceinline__ double dadd(double a, double b) {
+  return F64 ? __dadd_rn(a, b) : a + b;
+}
+
+// exact per-point sum of a multi-point leaf (_node_term, _core.py:59-64)
+template <int KID, bool F64>
+__device__ double leaf_points_sum(const typename Prec<F64>::V4* __restrict__ pa,
+                                  const typename Prec<F64>::V4* __restrict__ pb, int64_t b,
+                                  int64_t e, double qx, double qy, double qz, const KParams& kp) {
+  using V4 = typename Prec<F64>::V4;
+  double acc = 0.0;
+  for (int64_t j = b; j < e; ++j) {
+    V4 u = pa[j];
+    V4 mm;
+    mm.x = u.w;
+    if (KID == KID_WINDING) {
+      V4 v = pb[j];
+      mm.y = v.x;
+      mm.z = v.y;
+    } else {
+      mm.y = 0;
+      mm.z = 0;
+    }
+    acc = dadd<F64>(acc, term<KID, F64>(u, mm, qx, qy, qz, kp));
+  }
+  return acc;
+}
+
+template <bool F64>
+__device__ __forceinline__ double ffr(const typename Prec<F64>::V4& g, double qx, double qy,
+                                      double qz) {
+  if constexpr (F64)
+    return ffr_parity(g.x, g.y, g.z, g.w, qx, qy, qz);
+  else
+    return ffr_f32(g.x, g.y, g.z, g.w, (float)qx, (float)qy, (float)qz);
+}
+
+// ====================================================================== BH
+// barnes_hut_batch (_core.py:101-129).  The reference pops an explicit stack
+// with children pushed in reverse, i.e. it walks the accepted frontier in DFS
+// preorder.  Here each query walks preorder with skip links (open: i+1,
+// accept: skip[i]); a warp processes the union of its lanes' node sequences in
+// increasing preorder index, so every record load is one broadcast transaction
+// while each lane still sees exactly its own sequence (results unchanged).
+template <int KID, bool F64>
+__global__ void __launch_bounds__(256) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
+                                            const typename Prec<F64>::V4* __restrict__ pa,
+                                            const typename Prec<F64>::V4* __restrict__ pb,
+                                            uint32_t nn, const double* __restrict__ q, int64_t n,
+                                            const int32_t* __restrict__ qperm, double beta,
+                                            KParams kp, typename Prec<F64>::Out* __restrict__ out,
+                                            int64_t* __restrict__ visited) {
+  using V4 = typename Prec<F64>::V4;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool live = t < n;
+  int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
+  double qx = 0, qy = 0, qz = 0;
+  if (live) load_query(q, qi, qx, qy, qz);
+  uint32_t i = live ? 0u : nn;
+  double acc = 0.0;
+  int64_t seen = 0;
+  while (true) {
+    uint32_t cur = warp_min_u32(i);
+    if (cur >= nn) break;
+    if (i == cur) {
+      V4 g = rec[2 * (int64_t)cur];
+      V4 mm = rec[2 * (int64_t)cur + 1];
+      ++seen;
+      uint32_t skip;
+      if constexpr (F64)
+        skip = (uint32_t)__double_as_longlong(mm.w);
+      else
+        skip = (uint32_t)__float_as_int(mm.w);
+      bool leaf = skip == cur + 1;
+      if (leaf || ffr<F64>(g, qx, qy, qz) >= beta) {
+        double v;
+        if (g.w < 0) {  // multi-point leaf: exact per-point sum
+          int64_t b, e;
+          if constexpr (F64) {
+            b = __double_as_longlong(mm.x);
+            e = __double_as_longlong(mm.y);
+          } else {
+            b = __float_as_int(mm.x);
+            e = __float_as_int(mm.y);
+          }
+          v = leaf_points_sum<KID, F64>(pa, pb, b, e, qx, qy, qz, kp);
+        } else {
+          v = term<KID, F64>(g, mm, qx, qy, qz, kp);
+        }
+        acc = dadd<F64>(acc, v);
+        i = skip;
+      } else {
+        i = cur + 1;
+      }
+    }
+  }
+  if (live) {
+    out[qi] = (typename Prec<F64>::Out)acc;
+    if (visited) visited[qi] = seen;
+  }
+}
+
+// ============================================================== level order
+template <int KID, bool F64>
+struct LoTree {
+  using V4 = typename Prec<F64>::V4;
+  const V4* __restrict__ geo;
+  const V4* __restrict__ mass;
+  const int4* __restrict__ topo;
+  const V4* __restrict__ pa;
+  const V4* __restrict__ pb;
+
+  __device__ __forceinline__ double agg_term(int r, double qx, double qy, double qz,
+                                             const KParams& kp) const {
+    return term<KID, F64>(geo[r], mass[r], qx, qy, qz, kp);
+  }
+  // _node_term, _core.py:55-66
+  __device__ __forceinline__ double node_term(int r, double qx, double qy, double qz,
+                                              const KParams& kp) const {
+    int4 tp = topo[r];
+    if (tp.y == 0 && tp.w - tp.z > 1)
+      return leaf_points_sum<KID, F64>(pa, pb, tp.z, tp.w, qx, qy, qz, kp);
+    return agg_term(r, qx, qy, qz, kp);
+  }
+  // _children_term_sum, _core.py:69-77
+  __device__ __forceinline__ double children_sum(const int4& tp, double qx, double qy, double qz,
+                                                 const KParams& kp) const {
+    double acc = 0.0;
+    for (int t = 0; t < tp.y; ++t) acc = dadd<F64>(acc, node_term(tp.x + t, qx, qy, qz, kp));
+    return acc;
+  }
+  // the child whose point range holds j (children are contiguous and ordered)
+  __device__ __forceinline__ int child_of(const int4& tp, int64_t j) const {
+    int lo = 0, hi = tp.y;  // invariant: begin(child lo) <= j
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (topo[tp.x + mid].z <= j)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    return tp.x + lo;
+  }
+};
+
+// _sample_residual, _core.py:159-212 (one path from subdomain a)
+template <int KID, bool F64>
+__device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int a,
+                                                  const int4& tpa, double delta_a,
+                                                  uint64_t key_i, uint64_t key_r, int rr_mode,
+                                                  double qx, double qy, double qz,
+                                                  const KParams& kp, int64_t& steps,
+                                                  int64_t& seen) {
+  int64_t count_a = (int64_t)tpa.w - tpa.z;
+  double u0 = uniform_draw(key_i, 0);
+  int64_t j = tpa.z + (int64_t)__dmul_rn(u0, (double)count_a);
+  if (j >= tpa.w) j = tpa.w - 1;
+  int node = a;
+  int4 tp = tpa;
+  double prr = 1.0, resid = 0.0;
+  uint64_t rctr = 0;
+  while (tp.y > 0) {
+    int child = T.child_of(tp, j);
+    double delta;
+    if (node == a)
+      delta = delta_a;
+    else
+      delta = F64 ? __dsub_rn(T.children_sum(tp, qx, qy, qz, kp), T.agg_term(node, qx, qy, qz, kp))
+                  : T.children_sum(tp, qx, qy, qz, kp) - T.agg_term(node, qx, qy, qz, kp);
+    seen += tp.y;
+    double pagg = __ddiv_rn((double)(tp.w - tp.z), (double)count_a);
+    resid = __dadd_rn(resid, __ddiv_rn(delta, __dmul_rn(pagg, prr)));
+    double rp = ffr<F64>(T.geo[node], qx, qy, qz);
+    double rc = ffr<F64>(T.geo[child], qx, qy, qz);
+    double p = rr_probability(rp, rc, rr_mode);
+    double u = uniform_draw(key_r, rctr);
+    ++rctr;
+    ++seen;
+    if (u >= p) break;
+    prr = __dmul_rn(prr, p);
+    node = child;
+    tp = T.topo[node];
+    ++steps;
+  }
+  return resid;
+}
+
+// stochastic_batch, _core.py:215-267
+template <int KID, bool F64>
+__global__ void __launch_bounds__(128) k_stochastic(LoTree<KID, F64> T, int root_kids,
+                                                    const double* __restrict__ q, int64_t n,
+                                                    const int32_t* __restrict__ qperm, int S,
+                                                    int rr_mode, uint64_t seed, int64_t qoff,
+                                                    KParams kp,
+                                                    typename Prec<F64>::Out* __restrict__ out,
+                                                    int64_t* __restrict__ visited,
+                                                    int64_t* __restrict__ path_steps,
+                                                    int64_t* __restrict__ path_count) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int64_t qi = qperm ? (int64_t)qperm[t] : t;
+  double qx, qy, qz;
+  load_query(q, qi, qx, qy, qz);
+  int64_t seen = 0, steps = 0, paths = 0;
+  double acc = 0.0;
+  if (root_kids == 0) {
+    acc = T.node_term(0, qx, qy, qz, kp);
+    seen = 1;
+  } else {
+    uint64_t hq = key_fold(mix64(seed + kGamma), (uint64_t)(qi + qoff));
+    for (int a_ord = 0; a_ord < root_kids; ++a_ord) {
+      int a = 1 + a_ord;  // level order: the root's children follow the root
+      ++seen;
+      int4 tpa = T.topo[a];
+      if (tpa.y == 0) {
+        acc = dadd<F64>(acc, T.node_term(a, qx, qy, qz, kp));
+        continue;
+      }
+      double cv = T.agg_term(a, qx, qy, qz, kp);
+      double ks = T.children_sum(tpa, qx, qy, qz, kp);
+      double delta_a = F64 ? __dsub_rn(ks, cv) : ks - cv;
+      uint64_t ha = key_fold(hq, (uint64_t)a_ord);
+      double fa = 0.0;
+      for (int s = 0; s < S; ++s) {
+        uint64_t hs = key_fold(ha, (uint64_t)s);
+        uint64_t key_i = key_fold(hs, 0), key_r = key_fold(hs, 1);
+        double resid = sample_residual<KID, F64>(T, a, tpa, delta_a, key_i, key_r, rr_mode, qx,
+                                                 qy, qz, kp, steps, seen);
+        fa = __dadd_rn(fa, resid);
+        ++paths;
+      }
+      acc = __dadd_rn(acc, __dadd_rn(cv, __ddiv_rn(fa, (double)S)));
+    }
+  }
+  out[qi] = (typename Prec<F64>::Out)acc;
+  if (visited) visited[qi] = seen;
+  if (path_steps) path_steps[qi] = steps;
+  if (path_count) path_count[qi] = paths;
+}
+
+// stochastic_moments_batch, _core.py:270-336 (per-subdomain swaps cached in `work`)
+template <int KID, bool F64>
+__global__ void __launch_bounds__(128) k_moments(LoTree<KID, F64> T, int root_kids,
+                                                 const double* __restrict__ q, int64_t n,
+                                                 int64_t n_reps, int rr_mode, uint64_t seed,
+                                                 KParams kp, double* __restrict__ work,
+                                                 double* __restrict__ mean_out,
+                                                 double* __restrict__ var_out) {
+  int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (qi >= n) return;
+  double qx, qy, qz;
+  load_query(q, qi, qx, qy, qz);
+  if (root_kids == 0) {
+    mean_out[qi] = T.node_term(0, qx, qy, qz, kp);
+    var_out[qi] = 0.0;
+    return;
+  }
+  double* delta = work + qi * (int64_t)root_kids;
+  double base = 0.0;
+  for (int a_ord = 0; a_ord < root_kids; ++a_ord)
+    if (T.topo[1 + a_ord].y == 0) base = dadd<F64>(base, T.node_term(1 + a_ord, qx, qy, qz, kp));
+  for (int a_ord = 0; a_ord < root_kids; ++a_ord) {
+    int a = 1 + a_ord;
+    int4 tpa = T.topo[a];
+    if (tpa.y == 0) continue;
+    double cv = T.agg_term(a, qx, qy, qz, kp);
+    base = dadd<F64>(base, cv);
+    double ks = T.children_sum(tpa, qx, qy, qz, kp);
+    delta[a_ord] = F64 ? __dsub_rn(ks, cv) : ks - cv;
+  }
+  uint64_t hq = key_fold(mix64(seed + kGamma), (uint64_t)qi);
+  double acc = 0.0, acc2 = 0.0;
+  int64_t st = 0, se = 0;
+  for (int64_t r = 0; r < n_reps; ++r) {
+    double tsum = 0.0;
+    for (int a_ord = 0; a_ord < root_kids; ++a_ord) {
+      int a = 1 + a_ord;
+      int4 tpa = T.topo[a];
+      if (tpa.y == 0) continue;
+      uint64_t hs = key_fold(key_fold(hq, (uint64_t)a_ord), (uint64_t)r);
+      tsum = __dadd_rn(tsum, sample_residual<KID, F64>(T, a, tpa, delta[a_ord], key_fold(hs, 0),
+                                                       key_fold(hs, 1), rr_mode, qx, qy, qz, kp,
+                                                       st, se));
+    }
+    acc = __dadd_rn(acc, tsum);
+    acc2 = __dadd_rn(acc2, __dmul_rn(tsum, tsum));
+  }
+  double mr = __ddiv_rn(acc, (double)n_reps);
+  mean_out[qi] = __dadd_rn(base, mr);
+  double v = __dsub_rn(__ddiv_rn(acc2, (double)n_reps), __dmul_rn(mr, mr));
+  var_out[qi] = v > 0.0 ? v : 0.0;
+}
+
+// telescoping_batch, _core.py:132-156 (preorder sweep over every internal node)
+template <int KID, bool F64>
+__global__ void __launch_bounds__(128) k_telescoping(LoTree<KID, F64> T,
+                                                     const int32_t* __restrict__ pre2lo,
+                                                     int64_t nn, const double* __restrict__ q,
+                                                     int64_t n, KParams kp,
+                                                     typename Prec<F64>::Out* __restrict__ out,
+                                                     int64_t* __restrict__ visited) {
+  int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (qi >= n) return;
+  double qx, qy, qz;
+  load_query(q, qi, qx, qy, qz);
+  double acc = T.node_term(0, qx, qy, qz, kp);
+  int64_t seen = 1;
+  for (int64_t a = 0; a < nn; ++a) {
+    int r = pre2lo[a];
+    int4 tp = T.topo[r];
+    if (tp.y > 0) {
+      double kids = T.children_sum(tp, qx, qy, qz, kp);
+      double parent = T.agg_term(r, qx, qy, qz, kp);
+      acc = F64 ? __dadd_rn(acc, __dsub_rn(kids, parent)) : acc + (kids - parent);
+      seen += 1 + tp.y;
+    }
+  }
+  out[qi] = (typename Prec<F64>::Out)acc;
+  if (visited) visited[qi] = seen;
+}
+
+// ============================================================== brute force
+// brute_force_batch (_core.py:80-98).  Parity flavour: one query per thread,
+// sources streamed through shared memory in the reference's order with the
+// same Kahan recurrence.
+constexpr int kBruteTile64 = 512;
+template <int KID>
+__global__ void __launch_bounds__(256) k_brute64(const double* __restrict__ pts,
+                                                 const double* __restrict__ ms, int64_t m, int c,
+                                                 const double* __restrict__ q, int64_t n,
+                                                 KParams kp, double* __restrict__ out) {
+  __shared__ double4 sa[kBruteTile64];
+  __shared__ double2 sb[KID == KID_WINDING ? kBruteTile64 : 1];
+  int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool live = qi < n;
+  double qx = 0, qy = 0, qz = 0;
+  if (live) load_query(q, qi, qx, qy, qz);
+  double acc = 0.0, comp = 0.0;
+  for (int64_t base = 0; base < m; base += kBruteTile64) {
+    int cnt = (int)(m - base < kBruteTile64 ? m - base : kBruteTile64);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+      int64_t j = base + k;
+      sa[k] = make_double4(pts[3 * j], pts[3 * j + 1], pts[3 * j + 2], ms[(int64_t)c * j]);
+      if (KID == KID_WINDING) sb[k] = make_double2(ms[(int64_t)c * j + 1], ms[(int64_t)c * j + 2]);
+    }
+    __syncthreads();
+    if (live) {
+      for (int k = 0; k < cnt; ++k) {
+        double4 s = sa[k];
+        double m1 = 0, m2 = 0;
+        if (KID == KID_WINDING) {
+          m1 = sb[k].x;
+          m2 = sb[k].y;
+        }
+        double v = contrib_parity<KID>(s.w, m1, m2, s.x, s.y, s.z, qx, qy, qz, kp);
+        double y = __dsub_rn(v, comp);
+        double tt = __dadd_rn(acc, y);
+        comp = __dsub_rn(__dsub_rn(tt, acc), y);
+        acc = tt;
+      }
+    }
+  }
+  if (live) out[qi] = acc;
+}
+
+// Fast flavour: FP32 terms, each thread owns QPT queries (register tiling over
+// one broadcast LDS.128 per source), FP32 partials folded into FP64 every
+// kFold sources; sources split across blockIdx.y when the query count alone
+// cannot fill 148 SMs (deterministic: partials reduced in chunk order).
+constexpr int kBruteTile32 = 1024;
+constexpr int kFold = 256;
+template <int KID, int QPT>
+__global__ void __launch_bounds__(256) k_brute32(const float4* __restrict__ sa_g,
+                                                 const float4* __restrict__ sb_g, int64_t m,
+                                                 int64_t chunk, const double* __restrict__ q,
+                                                 int64_t n, KParams kp,
+                                                 double* __restrict__ partial) {
+  __shared__ float4 sa[kBruteTile32];
+  __shared__ float2 sb[KID == KID_WINDING ? kBruteTile32 : 1];
+  int64_t q0 = blockIdx.x * (int64_t)blockDim.x * QPT + threadIdx.x;
+  float qx[QPT], qy[QPT], qz[QPT];
+  double accd[QPT];
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) {
+    int64_t qi = q0 + (int64_t)k * blockDim.x;
+    qx[k] = qy[k] = qz[k] = 0.f;
+    if (qi < n) {
+      qx[k] = (float)q[3 * qi];
+      qy[k] = (float)q[3 * qi + 1];
+      qz[k] = (float)q[3 * qi + 2];
+    }
+    accd[k] = 0.0;
+  }
+  int64_t s0 = blockIdx.y * chunk, s1 = min(m, s0 + chunk);
+  for (int64_t base = s0; base < s1; base += kBruteTile32) {
+    int cnt = (int)(s1 - base < kBruteTile32 ? s1 - base : kBruteTile32);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+      sa[k] = sa_g[base + k];
+      if (KID == KID_WINDING) {
+        float4 v = sb_g[base + k];
+        sb[k] = make_float2(v.x, v.y);
+      }
+    }
+    __syncthreads();
+    for (int f0 = 0; f0 < cnt; f0 += kFold) {
+      int f1 = min(cnt, f0 + kFold);
+      float accf[QPT];
+#pragma unroll
+      for (int k = 0; k < QPT; ++k) accf[k] = 0.f;
+#pragma unroll 4
+      for (int j = f0; j < f1; ++j) {
+        float4 s = sa[j];
+        float m1 = 0.f, m2 = 0.f;
+        if (KID == KID_WINDING) {
+          float2 v = sb[j];
+          m1 = v.x;
+          m2 = v.y;
+        }
+#pragma unroll
+        for (int k = 0; k < QPT; ++k)
+          accf[k] += contrib_fast<KID>(s.w, m1, m2, s.x, s.y, s.z, qx[k], qy[k], qz[k], kp);
+      }
+#pragma unroll
+      for (int k = 0; k < QPT; ++k) accd[k] += (double)accf[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) {
+    int64_t qi = q0 + (int64_t)k * blockDim.x;
+    if (qi < n) partial[blockIdx.y * n + qi] = accd[k];
+  }
+}
+
+__global__ void k_reduce_chunks(const double* __restrict__ partial, int chunks, int64_t n,
+                                double* __restrict__ out64, float* __restrict__ out32) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int y = 0; y < chunks; ++y) acc += partial[y * n + i];
+  if (out64) out64[i] = acc;
+  if (out32) out32[i] = (float)acc;
+}
+
+__global__ void k_pack_src32(const double* __restrict__ pts, const double* __restrict__ ms,
+                             int64_t m, int c, float4* __restrict__ a, float4* __restrict__ b) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  a[j] = make_float4((float)pts[3 * j], (float)pts[3 * j + 1], (float)pts[3 * j + 2],
+                     (float)ms[(int64_t)c * j]);
+  if (b) b[j] = make_float4(c >= 3 ? (float)ms[(int64_t)c * j + 1] : 0.f,
+                            c >= 3 ? (float)ms[(int64_t)c * j + 2] : 0.f, 0.f, 0.f);
+}
+
+// post_transform (kernels.py:110-122) over the raw sums, plus the FP64 raw copy
+// FieldResult exposes (estimators.py:313-323)
+__global__ void k_post_transform(const void* __restrict__ raw, int raw_f32, int64_t n, int smooth,
+                                 double alpha, double* __restrict__ values,
+                                 double* __restrict__ raw64, uint8_t* __restrict__ flagged) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double r = raw_f32 ? (double)static_cast<const float*>(raw)[i] : static_cast<const double*>(raw)[i];
+  if (raw64) raw64[i] = r;
+  double v = r;
+  uint8_t f = 0;
+  if (smooth) {
+    if (r <= 0.0) {
+      v = INFINITY;
+      f = 1;
+    } else {
+      v = __ddiv_rn(-log(r), alpha);
+    }
+  }
+  values[i] = v;
+  flagged[i] = f;
+}
+
+int post_transform(const void* raw, int raw_f32, int64_t n, int smooth, double alpha,
+                   double* values, double* raw64, uint8_t* flagged, cudaStream_t s) {
+  if (n <= 0) return 0;
+  k_post_transform<<<grid_for(n, 256), 256, 0, s>>>(raw, raw_f32, n, smooth, alpha, values, raw64,
+                                                    flagged);
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+// ================================================================ dispatch
+static KParams make_kp(double alpha, double dfloor) {
+  KParams kp;
+  kp.alpha = alpha;
+  kp.dfloor = dfloor;
+  kp.alpha_log2e_neg = (float)(-alpha * 1.4426950408889634);
+  kp.dfloor_f = (float)dfloor;
+  kp.inv_dfloor_f = (float)(1.0 / dfloor);
+  return kp;
+}
+
+// calls f(integral_constant<KID>, bool_constant<F64>) for the runtime pair
+template <class F>
+static int with_kid(int kid, bool f64, F&& f) {
+  using std::bool_constant;
+  using std::integral_constant;
+  switch (kid * 2 + (f64 ? 1 : 0)) {
+    case 0: f(integral_constant<int, 0>{}, bool_constant<false>{}); break;
+    case 1: f(integral_constant<int, 0>{}, bool_constant<true>{}); break;
+    case 2: f(integral_constant<int, 1>{}, bool_constant<false>{}); break;
+    case 3: f(integral_constant<int, 1>{}, bool_constant<true>{}); break;
+    case 4: f(integral_constant<int, 2>{}, bool_constant<false>{}); break;
+    case 5: f(integral_constant<int, 2>{}, bool_constant<true>{}); break;
+    default: set_error("unknown kernel id %d", kid); return 1;
+  }
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+static int sm_count() {
+  static int cnt = 0;
+  if (!cnt) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cnt, cudaDevAttrMultiProcessorCount, dev);
+    if (cnt <= 0) cnt = 148;
+  }
+  return cnt;
+}
+
+template <int KID>
+static int brute32_launch(const float4* sa, const float4* sb, int64_t m, const double* q, int64_t n,
+                          const KParams& kp, double* out64, float* out32, cudaStream_t s) {
+  constexpr int QPT = 4, B = 256;
+  int64_t per_block = (int64_t)B * QPT;
+  int64_t gx = (n + per_block - 1) / per_block;
+  int64_t want = 4LL * sm_count();  // ~4 resident blocks per SM
+  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(want / std::max<int64_t>(gx, 1),
+                                                          (m + kBruteTile32 - 1) / kBruteTile32));
+  chunks = std::min<int64_t>(chunks, 65535);
+  int64_t chunk = (m + chunks - 1) / chunks;
+  chunk = ((chunk + kBruteTile32 - 1) / kBruteTile32) * kBruteTile32;
+  chunks = (m + chunk - 1) / chunk;
+  Scratch part;
+  FS_TRY(part.alloc(sizeof(double) * chunks * n, s));
+  dim3 grid((unsigned)gx, (unsigned)chunks);
+  k_brute32<KID, QPT><<<grid, B, 0, s>>>(sa, sb, m, chunk, q, n, kp, part.as<double>());
+  k_reduce_chunks<<<grid_for(n, 256), 256, 0, s>>>(part.as<double>(), (int)chunks, n, out64, out32);
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+int brute_force(int kid, double alpha, double dfloor, bool f64, const double* pts,
+                const double* ms, int64_t m, int c, const double* q, int64_t n, void* out,
+                cudaStream_t s) {
+  if (n <= 0) return 0;
+  KParams kp = make_kp(alpha, dfloor);
+  if (f64) {
+    return with_kid(kid, true, [&](auto K, auto) {
+      k_brute64<decltype(K)::value><<<grid_for(n, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp,
+                                                                     (double*)out);
+    });
+  }
+  Scratch sa, sb;
+  FS_TRY(sa.alloc(sizeof(float4) * m, s));
+  FS_TRY(sb.alloc(sizeof(float4) * (kid == KID_WINDING ? m : 1), s));
+  k_pack_src32<<<grid_for(m, 256), 256, 0, s>>>(pts, ms, m, c, sa.as<float4>(),
+                                                kid == KID_WINDING ? sb.as<float4>() : nullptr);
+  switch (kid) {
+    case 0: return brute32_launch<0>(sa.as<float4>(), sb.as<float4>(), m, q, n, kp, nullptr, (float*)out, s);
+    case 1: return brute32_launch<1>(sa.as<float4>(), sb.as<float4>(), m, q, n, kp, nullptr, (float*)out, s);
+    case 2: return brute32_launch<2>(sa.as<float4>(), sb.as<float4>(), m, q, n, kp, nullptr, (float*)out, s);
+  }
+  set_error("unknown kernel id %d", kid);
+  return 1;
+}
+
+int brute_force_f32_acc64(int kid, double alpha, double dfloor, const double* pts,
+                          const double* ms, int64_t m, int c, const double* q, int64_t n,
+                          double* out, cudaStream_t s) {
+  KParams kp = make_kp(alpha, dfloor);
+  Scratch sa, sb;
+  FS_TRY(sa.alloc(sizeof(float4) * m, s));
+  FS_TRY(sb.alloc(sizeof(float4) * (kid == KID_WINDING ? m : 1), s));
+  k_pack_src32<<<grid_for(m, 256), 256, 0, s>>>(pts, ms, m, c, sa.as<float4>(),
+                                                kid == KID_WINDING ? sb.as<float4>() : nullptr);
+  switch (kid) {
+    case 0: return brute32_launch<0>(sa.as<float4>(), sb.as<float4>(), m, q, n, kp, out, nullptr, s);
+    case 1: return brute32_launch<1>(sa.as<float4>(), sb.as<float4>(), m, q, n, kp, out, nullptr, s);
+    case 2: return brute32_launch<2>(sa.as<float4>(), sb.as<float4>(), m, q, n, kp, out, nullptr, s);
+  }
+  set_error("unknown kernel id %d", kid);
+  return 1;
+}
+
+template <int KID, bool F64>
+static LoTree<KID, F64> lo_view(const FsTree* t) {
+  LoTree<KID, F64> T;
+  if constexpr (F64) {
+    T.geo = t->lo_geo64;
+    T.mass = t->lo_mass64;
+    T.pa = t->pts64a;
+    T.pb = t->pts64b;
+  } else {
+    T.geo = t->lo_geo32;
+    T.mass = t->lo_mass32;
+    T.pa = t->pts32a;
+    T.pb = t->pts32b;
+  }
+  T.topo = t->lo_topo;
+  return T;
+}
+
+int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
+               int64_t n, const int32_t* qperm, double beta, void* out, int64_t* visited,
+               cudaStream_t s) {
+  if (n <= 0) return 0;
+  FS_TRY(ensure_bh(t, f64, s));
+  FS_TRY(ensure_lo(t, f64, s));  // packed points for multi-point leaves
+  KParams kp = make_kp(alpha, dfloor);
+  return with_kid(kid, f64, [&](auto K, auto P) {
+    constexpr int KID = decltype(K)::value;
+    constexpr bool F64 = decltype(P)::value;
+    using V4 = typename Prec<F64>::V4;
+    const V4 *rec, *pa, *pb;
+    if constexpr (F64) {
+      rec = reinterpret_cast<const V4*>(t->bh64);
+      pa = t->pts64a;
+      pb = t->pts64b;
+    } else {
+      rec = reinterpret_cast<const V4*>(t->bh32);
+      pa = t->pts32a;
+      pb = t->pts32b;
+    }
+    k_bh<KID, F64><<<grid_for(n, 256), 256, 0, s>>>(rec, pa, pb, (uint32_t)t->n, q, n, qperm,
+                                                    beta, kp, (typename Prec<F64>::Out*)out,
+                                                    visited);
+  });
+}
+
+int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
+               int64_t n, const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
+               int64_t query_offset, void* out, int64_t* visited, int64_t* path_steps,
+               int64_t* path_count, cudaStream_t s) {
+  if (n <= 0) return 0;
+  FS_TRY(ensure_lo(t, f64, s));
+  KParams kp = make_kp(alpha, dfloor);
+  return with_kid(kid, f64, [&](auto K, auto P) {
+    constexpr int KID = decltype(K)::value;
+    constexpr bool F64 = decltype(P)::value;
+    k_stochastic<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(
+        lo_view<KID, F64>(t), t->root_kids, q, n, qperm, n_samples, rr_mode, seed, query_offset,
+        kp, (typename Prec<F64>::Out*)out, visited, path_steps, path_count);
+  });
+}
+
+int stochastic_moments(FsTree* t, int kid, double alpha, double dfloor, const double* q,
+                       int64_t n, int64_t n_reps, int rr_mode, uint64_t seed, double* mean_out,
+                       double* var_out, cudaStream_t s) {
+  if (n <= 0) return 0;
+  FS_TRY(ensure_lo(t, true, s));
+  KParams kp = make_kp(alpha, dfloor);
+  Scratch work;
+  FS_TRY(work.alloc(sizeof(double) * n * std::max(1, t->root_kids), s));
+  return with_kid(kid, true, [&](auto K, auto) {
+    constexpr int KID = decltype(K)::value;
+    k_moments<KID, true><<<grid_for(n, 128), 128, 0, s>>>(lo_view<KID, true>(t), t->root_kids, q,
+                                                          n, n_reps, rr_mode, seed, kp,
+                                                          work.as<double>(), mean_out, var_out);
+  });
+}
+
+int telescoping(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
+                int64_t n, void* out, int64_t* visited, cudaStream_t s) {
+  if (n <= 0) return 0;
+  FS_TRY(ensure_lo(t, f64, s));
+  KParams kp = make_kp(alpha, dfloor);
+  return with_kid(kid, f64, [&](auto K, auto P) {
+    constexpr int KID = decltype(K)::value;
+    constexpr bool F64 = decltype(P)::value;
+    k_telescoping<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(
+        lo_view<KID, F64>(t), t->pre2lo, t->n, q, n, kp, (typename Prec<F64>::Out*)out, visited);
+  });
+}
+
+}  // namespace fsb

@@ -1,0 +1,262 @@
+// fs_pack.cu -- packed node records for the evaluators, and device trees
+// assembled from reference-layout arrays (Octree.core_arrays(), octree.py:110-115).
+#include <algorithm>
+
+#include "fs_common.cuh"
+#include "fs_internal.h"
+
+namespace fsb {
+
+template <class T>
+static int dalloc(T** p, int64_t count) {
+  FS_CK(cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<int64_t>(count, 1)));
+  return 0;
+}
+
+void free_tree(FsTree* t) {
+  if (!t) return;
+  void* ptrs[] = {t->bbox_min, t->bbox_max, t->diameter, t->agg_mass, t->agg_weight, t->com,
+                  t->child_start, t->child_count, t->child_index, t->begin, t->end, t->depth,
+                  t->perm, t->points, t->masses, t->weights, t->lo2pre, t->pre2lo, t->skip,
+                  t->fc_lo, t->bh32, t->bh64, t->lo_geo32, t->lo_mass32, t->lo_geo64,
+                  t->lo_mass64, t->lo_topo, t->pts32a, t->pts32b, t->pts64a, t->pts64b};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete t;
+}
+
+// ------------------------------------------------------------ from arrays
+__global__ void k_parent(const int64_t* __restrict__ cs, const int64_t* __restrict__ cc,
+                         const int64_t* __restrict__ ci, int64_t n, int32_t* __restrict__ parent) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == 0) parent[0] = 0;
+  int64_t s = cs[i], k = cc[i];
+  for (int64_t t = 0; t < k; ++t) parent[ci[s + t]] = (int32_t)i;
+}
+
+__global__ void k_jump(const int32_t* __restrict__ anc, const int32_t* __restrict__ dist, int64_t n,
+                       int32_t* __restrict__ anc2, int32_t* __restrict__ dist2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t a = anc[i];
+  dist2[i] = dist[i] + dist[a];
+  anc2[i] = anc[a];
+}
+
+__global__ void k_init_dist(int64_t n, int32_t* __restrict__ dist) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dist[i] = i == 0 ? 0 : 1;
+}
+
+__global__ void k_begin32(const int64_t* __restrict__ b, int64_t n, int32_t* __restrict__ nb,
+                          int32_t* __restrict__ first_at) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  nb[i] = (int32_t)b[i];
+  if (i == 0 || b[i - 1] != b[i]) first_at[b[i]] = (int32_t)i;
+}
+
+__global__ void k_fc_skip(const int64_t* __restrict__ cs, const int64_t* __restrict__ cc,
+                          const int64_t* __restrict__ ci, const int64_t* __restrict__ end,
+                          const int32_t* __restrict__ pre2lo, const int32_t* __restrict__ first_at,
+                          int64_t n, int64_t m, int32_t* __restrict__ fc, int32_t* __restrict__ skip) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  fc[i] = cc[i] > 0 ? pre2lo[ci[cs[i]]] : 0;
+  int64_t e = end[i];
+  skip[i] = e < m ? first_at[e] : (int32_t)n;
+}
+
+int tree_from_arrays(FsTree** out, const double* diameter, const double* agg_mass,
+                     const double* com, const int64_t* child_start, const int64_t* child_count,
+                     const int64_t* child_index, const int64_t* begin, const int64_t* end,
+                     const double* points, const double* masses, int64_t n, int64_t m, int c,
+                     cudaStream_t s) {
+  *out = nullptr;
+  if (n < 1 || m < 1 || c < 1 || n >= (int64_t(1) << 31) - 2) {
+    set_error("tree_from_arrays: bad sizes");
+    return 1;
+  }
+  FsTree* t = new FsTree();
+  t->n = n;
+  t->m = m;
+  t->c = c;
+  int rc = 0;
+  auto cp = [&](auto** dst, const auto* src, int64_t count) -> int {
+    using T = std::remove_pointer_t<std::remove_reference_t<decltype(*dst)>>;
+    FS_TRY(dalloc(dst, count));
+    if (count > 0)
+      FS_CK(cudaMemcpyAsync(*dst, src, sizeof(T) * count, cudaMemcpyDeviceToDevice, s));
+    return 0;
+  };
+  if ((rc = cp(&t->diameter, diameter, n)) || (rc = cp(&t->agg_mass, agg_mass, n * c)) ||
+      (rc = cp(&t->com, com, 3 * n)) || (rc = cp(&t->child_start, child_start, n)) ||
+      (rc = cp(&t->child_count, child_count, n)) ||
+      (rc = cp(&t->child_index, child_index, n - 1)) || (rc = cp(&t->begin, begin, n)) ||
+      (rc = cp(&t->end, end, n)) || (rc = cp(&t->points, points, 3 * m)) ||
+      (rc = cp(&t->masses, masses, m * c)) || (rc = dalloc(&t->lo2pre, n)) ||
+      (rc = dalloc(&t->pre2lo, n)) || (rc = dalloc(&t->skip, n)) || (rc = dalloc(&t->fc_lo, n))) {
+    free_tree(t);
+    return rc;
+  }
+  const int B = 256;
+  Scratch anc, dist, anc2, dist2, nb, first_at;
+  if ((rc = anc.alloc(4 * n, s)) || (rc = dist.alloc(4 * n, s)) || (rc = anc2.alloc(4 * n, s)) ||
+      (rc = dist2.alloc(4 * n, s)) || (rc = nb.alloc(4 * n, s)) || (rc = first_at.alloc(4 * m, s))) {
+    free_tree(t);
+    return rc;
+  }
+  k_parent<<<grid_for(n, B), B, 0, s>>>(t->child_start, t->child_count, t->child_index, n,
+                                        anc.as<int32_t>());
+  k_init_dist<<<grid_for(n, B), B, 0, s>>>(n, dist.as<int32_t>());
+  int32_t *a = anc.as<int32_t>(), *d = dist.as<int32_t>(), *a2 = anc2.as<int32_t>(),
+          *d2 = dist2.as<int32_t>();
+  for (int round = 0; round < 12; ++round) {  // depths < 4096
+    k_jump<<<grid_for(n, B), B, 0, s>>>(a, d, n, a2, d2);
+    std::swap(a, a2);
+    std::swap(d, d2);
+  }
+  k_begin32<<<grid_for(n, B), B, 0, s>>>(t->begin, n, nb.as<int32_t>(), first_at.as<int32_t>());
+  int64_t* lstart = nullptr;
+  if ((rc = level_order(t, nb.as<int32_t>(), d, 4095, &lstart, s))) {
+    free_tree(t);
+    return rc;
+  }
+  cudaFree(lstart);
+  k_fc_skip<<<grid_for(n, B), B, 0, s>>>(t->child_start, t->child_count, t->child_index, t->end,
+                                         t->pre2lo, first_at.as<int32_t>(), n, m, t->fc_lo,
+                                         t->skip);
+  int64_t rk = 0;
+  FS_CK(cudaMemcpyAsync(&rk, t->child_count, 8, cudaMemcpyDeviceToHost, s));
+  FS_CK(cudaStreamSynchronize(s));
+  FS_CK(cudaGetLastError());
+  t->root_kids = (int)rk;
+  *out = t;
+  return 0;
+}
+
+// ------------------------------------------------------------ BH records
+template <class T>
+__device__ __forceinline__ T int_bits(int64_t v);
+template <>
+__device__ __forceinline__ float int_bits<float>(int64_t v) { return __int_as_float((int)v); }
+template <>
+__device__ __forceinline__ double int_bits<double>(int64_t v) { return __longlong_as_double(v); }
+
+template <class T, class V4>
+__global__ void k_pack_bh(const double* __restrict__ com, const double* __restrict__ diam,
+                          const double* __restrict__ am, const int64_t* __restrict__ cc,
+                          const int64_t* __restrict__ b, const int64_t* __restrict__ e,
+                          const int32_t* __restrict__ skip, int64_t n, int c, V4* __restrict__ g,
+                          V4* __restrict__ mrec) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool multi = cc[i] == 0 && e[i] - b[i] > 1;
+  V4 gg, mm;
+  gg.x = (T)com[3 * i];
+  gg.y = (T)com[3 * i + 1];
+  gg.z = (T)com[3 * i + 2];
+  gg.w = multi ? (T)-1 : (T)diam[i];
+  mm.x = (T)am[(int64_t)c * i];
+  mm.y = c >= 3 ? (T)am[(int64_t)c * i + 1] : (T)0;
+  mm.z = c >= 3 ? (T)am[(int64_t)c * i + 2] : (T)0;
+  mm.w = int_bits<T>(skip[i]);
+  if (multi) {
+    mm.x = int_bits<T>(b[i]);
+    mm.y = int_bits<T>(e[i]);
+  }
+  g[2 * i] = gg;  // interleaved: record i = {g, m}
+  g[2 * i + 1] = mm;
+  (void)mrec;
+}
+
+int ensure_bh(FsTree* t, bool f64, cudaStream_t s) {
+  const int B = 256;
+  if (f64 && !t->bh64) {
+    FS_TRY(dalloc(&t->bh64, t->n));
+    k_pack_bh<double, double4><<<grid_for(t->n, B), B, 0, s>>>(
+        t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->skip, t->n, t->c,
+        reinterpret_cast<double4*>(t->bh64), nullptr);
+  } else if (!f64 && !t->bh32) {
+    FS_TRY(dalloc(&t->bh32, t->n));
+    k_pack_bh<float, float4><<<grid_for(t->n, B), B, 0, s>>>(
+        t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->skip, t->n, t->c,
+        reinterpret_cast<float4*>(t->bh32), nullptr);
+  }
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+// ------------------------------------------------------- level-order records
+template <class T, class V4>
+__global__ void k_pack_lo(const int32_t* __restrict__ lo2pre, const double* __restrict__ com,
+                          const double* __restrict__ diam, const double* __restrict__ am,
+                          const int64_t* __restrict__ cc, const int64_t* __restrict__ b,
+                          const int64_t* __restrict__ e, const int32_t* __restrict__ fc, int64_t n,
+                          int c, V4* __restrict__ geo, V4* __restrict__ mass,
+                          int4* __restrict__ topo) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t i = lo2pre[r];
+  V4 g, mm;
+  g.x = (T)com[3 * i];
+  g.y = (T)com[3 * i + 1];
+  g.z = (T)com[3 * i + 2];
+  g.w = (T)diam[i];
+  mm.x = (T)am[(int64_t)c * i];
+  mm.y = c >= 3 ? (T)am[(int64_t)c * i + 1] : (T)0;
+  mm.z = c >= 3 ? (T)am[(int64_t)c * i + 2] : (T)0;
+  mm.w = (T)0;
+  geo[r] = g;
+  mass[r] = mm;
+  if (topo) topo[r] = make_int4(fc[i], (int)cc[i], (int)b[i], (int)e[i]);
+}
+
+template <class T, class V4>
+__global__ void k_pack_pts(const double* __restrict__ pts, const double* __restrict__ ms, int64_t m,
+                           int c, V4* __restrict__ a, V4* __restrict__ bq) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  V4 u, v;
+  u.x = (T)pts[3 * j];
+  u.y = (T)pts[3 * j + 1];
+  u.z = (T)pts[3 * j + 2];
+  u.w = (T)ms[(int64_t)c * j];
+  v.x = c >= 3 ? (T)ms[(int64_t)c * j + 1] : (T)0;
+  v.y = c >= 3 ? (T)ms[(int64_t)c * j + 2] : (T)0;
+  v.z = (T)0;
+  v.w = (T)0;
+  a[j] = u;
+  bq[j] = v;
+}
+
+int ensure_lo(FsTree* t, bool f64, cudaStream_t s) {
+  const int B = 256;
+  if (!t->lo_topo) FS_TRY(dalloc(&t->lo_topo, t->n));
+  if (f64 && !t->lo_geo64) {
+    FS_TRY(dalloc(&t->lo_geo64, t->n));
+    FS_TRY(dalloc(&t->lo_mass64, t->n));
+    FS_TRY(dalloc(&t->pts64a, t->m));
+    FS_TRY(dalloc(&t->pts64b, t->m));
+    k_pack_lo<double, double4><<<grid_for(t->n, B), B, 0, s>>>(
+        t->lo2pre, t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->fc_lo,
+        t->n, t->c, t->lo_geo64, t->lo_mass64, t->lo_topo);
+    k_pack_pts<double, double4><<<grid_for(t->m, B), B, 0, s>>>(t->points, t->masses, t->m, t->c,
+                                                                t->pts64a, t->pts64b);
+  } else if (!f64 && !t->lo_geo32) {
+    FS_TRY(dalloc(&t->lo_geo32, t->n));
+    FS_TRY(dalloc(&t->lo_mass32, t->n));
+    FS_TRY(dalloc(&t->pts32a, t->m));
+    FS_TRY(dalloc(&t->pts32b, t->m));
+    k_pack_lo<float, float4><<<grid_for(t->n, B), B, 0, s>>>(
+        t->lo2pre, t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->fc_lo,
+        t->n, t->c, t->lo_geo32, t->lo_mass32, t->lo_topo);
+    k_pack_pts<float, float4><<<grid_for(t->m, B), B, 0, s>>>(t->points, t->masses, t->m, t->c,
+                                                              t->pts32a, t->pts32b);
+  }
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace fsb

@@ -1,0 +1,51 @@
+// fs_tree.cuh -- device-resident tree handle and packed node records.
+//
+// Reference layout (octree.py:61-67, DFS preorder) is kept on the device for
+// export and for the parity paths; the evaluators read packed records:
+//   * BH (preorder, skip links):      32 B FP32 / 64 B FP64 per node
+//   * level order (children contiguous): geo + mass + topo (int4) per node
+#pragma once
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+namespace fsb {
+
+struct BhRec32 {
+  float4 g;  // cx, cy, cz, diam  (diam = -1 marks a multi-point leaf)
+  float4 m;  // m0, m1, m2, skip (int bits); multi-point leaf: m0/m1 = begin/end bits
+};
+struct BhRec64 {
+  double4 g;
+  double4 m;  // m.w = skip (int64 bits); multi-point leaf: m.x/m.y = begin/end bits
+};
+
+struct FsTree {
+  int64_t n = 0, m = 0;
+  int c = 1, d = 2, max_depth = 32, d_eff = 0, num_levels = 0;
+  std::vector<int64_t> level_off;  // host copy, num_levels + 1 entries (level order)
+  bool owns_export = false;        // reference-layout arrays present
+
+  // reference layout (preorder), device
+  double *bbox_min = nullptr, *bbox_max = nullptr, *diameter = nullptr, *agg_mass = nullptr,
+         *agg_weight = nullptr, *com = nullptr;
+  int64_t *child_start = nullptr, *child_count = nullptr, *child_index = nullptr,
+          *begin = nullptr, *end = nullptr, *depth = nullptr, *perm = nullptr;
+  double *points = nullptr, *masses = nullptr, *weights = nullptr;
+
+  // derived, device
+  int32_t *lo2pre = nullptr, *pre2lo = nullptr, *skip = nullptr;
+  int32_t* fc_lo = nullptr;  // level-order index of the first child (internal nodes)
+
+  // packed records (built on first use)
+  BhRec32* bh32 = nullptr;
+  BhRec64* bh64 = nullptr;
+  float4 *lo_geo32 = nullptr, *lo_mass32 = nullptr;
+  double4 *lo_geo64 = nullptr, *lo_mass64 = nullptr;
+  int4* lo_topo = nullptr;
+  float4 *pts32a = nullptr, *pts32b = nullptr;  // permuted points {x,y,z,m0}, {m1,m2,0,0}
+  double4 *pts64a = nullptr, *pts64b = nullptr;
+  int root_kids = 0;  // child_count[0]
+};
+
+}  // namespace fsb

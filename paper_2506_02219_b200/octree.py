@@ -1,0 +1,285 @@
+"""The uniform-cell subdivision tree, built on the GPU.
+
+``build_tree`` (reference: octree.py:118-239) runs the data-parallel builder
+in csrc/fs_build.cu and keeps the tree device-resident; the 16
+reference-layout arrays (octree.py:61-67) are materialised on the host only
+when an attribute is read.  ``Octree(**arrays)`` also accepts host arrays
+(the reference's constructor); such a tree is uploaded on first evaluation.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as dev
+from . import _lib
+from .types import SourceSet
+
+__all__ = ["TreeNode", "Octree", "build_tree", "far_field_ratio", "validate_tree",
+           "dump_outline"]
+
+_DIAM_FLOOR = 1e-12
+_ARRAY_SLOTS = ("bbox_min", "bbox_max", "diameter", "aggregate_mass", "aggregate_weight",
+                "center_of_mass", "child_start", "child_count", "child_index", "begin", "end",
+                "depth", "permuted_indices", "points", "masses", "weights")
+
+
+@dataclass(frozen=True)
+class TreeNode:
+    """Read-only view of one node (octree.py:29-50)."""
+
+    index: int
+    bbox_min: np.ndarray
+    bbox_max: np.ndarray
+    diameter: float
+    aggregate_mass: np.ndarray
+    aggregate_weight: float
+    center_of_mass: np.ndarray
+    children: tuple
+    point_range: tuple
+    depth: int
+
+    @property
+    def is_leaf(self) -> bool:
+        return len(self.children) == 0
+
+    @property
+    def count(self) -> int:
+        return self.point_range[1] - self.point_range[0]
+
+
+class _DeviceTree:
+    """Owner of one fsb_tree handle (freed with the Python object)."""
+
+    def __init__(self, handle: int, keepalive=None):
+        self.handle = handle
+        self._keep = keepalive
+        info = (C.c_int64 * 8)()
+        _lib.check(_lib.load().fsb_tree_info(C.c_void_p(handle), info))
+        (self.num_nodes, self.num_points, self.channels, self.branching, self.max_depth,
+         self.levels, self.root_kids, self.has_export) = [int(v) for v in info]
+        self._fin = weakref.finalize(self, _free_handle, handle)
+
+
+def _free_handle(handle):
+    try:
+        _lib.load().fsb_tree_free(C.c_void_p(handle))
+    except Exception:
+        pass
+
+
+class Octree:
+    """Immutable flat-array tree; same slots and constructor as the reference."""
+
+    __slots__ = ("branching_per_dim", "max_depth") + _ARRAY_SLOTS + ("_dev", "__weakref__")
+
+    def __init__(self, **arrays):
+        for k in ("branching_per_dim", "max_depth") + _ARRAY_SLOTS:
+            v = arrays[k]
+            if isinstance(v, np.ndarray):
+                v.setflags(write=False)
+            object.__setattr__(self, k, v)
+        object.__setattr__(self, "_dev", None)
+
+    @classmethod
+    def _from_device(cls, devtree: _DeviceTree, branching: int, max_depth: int) -> "Octree":
+        self = object.__new__(cls)
+        object.__setattr__(self, "branching_per_dim", int(branching))
+        object.__setattr__(self, "max_depth", int(max_depth))
+        object.__setattr__(self, "_dev", devtree)
+        return self
+
+    def __getattr__(self, name):
+        # array slots of a GPU-built tree are exported lazily, all at once
+        if name in _ARRAY_SLOTS:
+            self._export()
+            return object.__getattribute__(self, name)
+        raise AttributeError(name)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("Octree is immutable")
+
+    def _export(self):
+        d = object.__getattribute__(self, "_dev")
+        n, m, c = d.num_nodes, d.num_points, d.channels
+        shapes = [((n, 3), np.float64), ((n, 3), np.float64), ((n,), np.float64),
+                  ((n, c), np.float64), ((n,), np.float64), ((n, 3), np.float64),
+                  ((n,), np.int64), ((n,), np.int64), ((n - 1,), np.int64), ((n,), np.int64),
+                  ((n,), np.int64), ((n,), np.int64), ((m,), np.int64), ((m, 3), np.float64),
+                  ((m, c), np.float64), ((m,), np.float64)]
+        torch = dev.torch()
+        bufs = [torch.empty(s, dtype=torch.from_numpy(np.zeros(0, dt)).dtype, pin_memory=True)
+                for s, dt in shapes]
+        ptrs = (C.c_void_p * 16)(*[b.data_ptr() if b.numel() else None for b in bufs])
+        _lib.check(_lib.lib().fsb_tree_export(C.c_void_p(d.handle), ptrs,
+                                              C.c_void_p(dev.stream_ptr())))
+        for k, b in zip(_ARRAY_SLOTS, bufs):
+            a = b.numpy().copy()
+            a.setflags(write=False)
+            object.__setattr__(self, k, a)
+
+    def _device_tree(self) -> _DeviceTree:
+        """The device handle; host-constructed trees are uploaded once."""
+        d = object.__getattribute__(self, "_dev")
+        if d is None:
+            d = _upload_core_arrays(self.core_arrays())
+            object.__setattr__(self, "_dev", d)
+        return d
+
+    @property
+    def num_nodes(self) -> int:
+        d = object.__getattribute__(self, "_dev")
+        if d is not None:
+            return d.num_nodes
+        return self.begin.shape[0]
+
+    @property
+    def num_points(self) -> int:
+        d = object.__getattribute__(self, "_dev")
+        if d is not None:
+            return d.num_points
+        return self.permuted_indices.shape[0]
+
+    @property
+    def root(self) -> TreeNode:
+        return self.node(0)
+
+    def node(self, i: int) -> TreeNode:
+        s, c = int(self.child_start[i]), int(self.child_count[i])
+        return TreeNode(index=i, bbox_min=self.bbox_min[i], bbox_max=self.bbox_max[i],
+                        diameter=float(self.diameter[i]), aggregate_mass=self.aggregate_mass[i],
+                        aggregate_weight=float(self.aggregate_weight[i]),
+                        center_of_mass=self.center_of_mass[i],
+                        children=tuple(int(j) for j in self.child_index[s:s + c]),
+                        point_range=(int(self.begin[i]), int(self.end[i])),
+                        depth=int(self.depth[i]))
+
+    def nodes(self):
+        for i in range(self.num_nodes):
+            yield self.node(i)
+
+    def core_arrays(self):
+        """octree.py:110-115 positional bundle (host arrays)."""
+        return (self.bbox_min, self.diameter, self.aggregate_mass, self.center_of_mass,
+                self.child_start, self.child_count, self.child_index, self.begin, self.end,
+                self.points, self.masses)
+
+
+def _upload_core_arrays(core11) -> _DeviceTree:
+    (_bmin, diam, am, com, cs, cc, ci, b, e, pts, ms) = core11
+    f = lambda a: dev.to_device(np.asarray(a, dtype=np.float64))  # noqa: E731
+    i = lambda a: dev.to_device(np.asarray(a, dtype=np.int64))  # noqa: E731
+    am = np.asarray(am)
+    c = am.shape[1] if am.ndim == 2 else 1
+    bufs = [f(diam), f(am), f(com), i(cs), i(cc), i(ci), i(b), i(e), f(pts), f(ms)]
+    n, m = int(np.shape(b)[0]), int(np.shape(pts)[0])
+    h = C.c_void_p()
+    _lib.check(_lib.lib().fsb_tree_from_core_arrays(
+        *[C.c_void_p(dev.ptr(x)) for x in bufs], n, m, c, C.byref(h),
+        C.c_void_p(dev.stream_ptr())))
+    return _DeviceTree(h.value)
+
+
+def build_tree(sources: SourceSet, branching_per_dim: int = 2, max_depth: int = 32) -> Octree:
+    """GPU build of the reference tree (octree.py:118-239); topology bit-exact."""
+    if branching_per_dim < 2:
+        raise ValueError("branching_per_dim must be >= 2")
+    if max_depth < 1:
+        raise ValueError("max_depth must be positive")
+    L = _lib.lib()
+    pos = dev.to_device(sources.positions)
+    ms = dev.to_device(sources.masses)
+    w = dev.to_device(sources.weights)
+    h = C.c_void_p()
+    _lib.check(L.fsb_build_tree(C.c_void_p(dev.ptr(pos)), C.c_void_p(dev.ptr(ms)),
+                                C.c_void_p(dev.ptr(w)), len(sources), sources.channel_count,
+                                int(branching_per_dim), int(max_depth), C.byref(h),
+                                C.c_void_p(dev.stream_ptr())))
+    return Octree._from_device(_DeviceTree(h.value), branching_per_dim, max_depth)
+
+
+def far_field_ratio(node: TreeNode, q) -> float:
+    """octree.py:242-247: ||q - com|| / max(diameter, 1e-12)."""
+    q = np.asarray(q, dtype=np.float64)
+    dv = q - node.center_of_mass
+    return math.sqrt(float(dv @ dv)) / max(node.diameter, _DIAM_FLOOR)
+
+
+def validate_tree(tree: Octree, sources: SourceSet) -> list:
+    """Structural invariants (octree.py:250-313); host checker over exported arrays."""
+    report = []
+    m_total = len(sources)
+    perm = tree.permuted_indices
+    if sorted(perm.tolist()) != list(range(m_total)):
+        return ["permuted_indices is not a permutation of 0..M-1"]
+    if not (tree.begin[0] == 0 and tree.end[0] == m_total):
+        report.append("root point_range does not cover all points")
+    d = tree.branching_per_dim
+    for i in range(tree.num_nodes):
+        b, e = int(tree.begin[i]), int(tree.end[i])
+        sel = perm[b:e]
+        mass_ref = sources.masses[sel].sum(axis=0)
+        l1 = np.abs(sources.masses[sel]).sum()
+        if np.any(np.abs(tree.aggregate_mass[i] - mass_ref) > 1e-12 * (1.0 + l1)):
+            report.append(f"node {i}: aggregate_mass != sum of contained masses")
+        w = sources.weights[sel]
+        wsum = w.sum()
+        if abs(tree.aggregate_weight[i] - wsum) > 1e-12 * (1.0 + wsum):
+            report.append(f"node {i}: aggregate_weight != sum of contained weights")
+        com_ref = (w[:, None] * sources.positions[sel]).sum(axis=0) / wsum
+        scale = max(1.0, float(np.abs(sources.positions[sel]).max()))
+        if np.any(np.abs(tree.center_of_mass[i] - com_ref) > 1e-9 * scale):
+            report.append(f"node {i}: center_of_mass != weighted mean of positions")
+        tol = 1e-9 * max(1.0, float(tree.diameter[i]))
+        if (np.any(tree.center_of_mass[i] < tree.bbox_min[i] - tol)
+                or np.any(tree.center_of_mass[i] > tree.bbox_max[i] + tol)):
+            report.append(f"node {i}: center_of_mass outside bbox")
+        cs, cc = int(tree.child_start[i]), int(tree.child_count[i])
+        kids = tree.child_index[cs:cs + cc]
+        if cc == 0:
+            if e - b != 1 and tree.depth[i] != tree.max_depth:
+                report.append(f"node {i}: multi-point leaf below the depth cap")
+            continue
+        if not 1 <= cc <= d ** 3:
+            report.append(f"node {i}: child count {cc} outside [1, d^3]")
+        cursor = b
+        contiguous = True
+        for k in kids:
+            if int(tree.begin[k]) != cursor:
+                report.append(f"node {i}: children ranges not contiguous")
+                contiguous = False
+                break
+            cursor = int(tree.end[k])
+        if contiguous and cursor != e:
+            report.append(f"node {i}: children ranges do not cover parent")
+        for k in kids:
+            if tree.diameter[k] > tree.diameter[i] / d + 1e-12:
+                report.append(f"node {i}: child {k} diameter exceeds parent/d")
+        w_kids = tree.aggregate_weight[kids].sum()
+        m_kids = tree.aggregate_mass[kids].sum(axis=0)
+        l1k = np.abs(tree.aggregate_mass[kids]).sum()
+        if abs(tree.aggregate_weight[i] - w_kids) > 1e-12 * (1.0 + w_kids):
+            report.append(f"node {i}: aggregate_weight inconsistent with children")
+        if np.any(np.abs(tree.aggregate_mass[i] - m_kids) > 1e-12 * (1.0 + l1k)):
+            report.append(f"node {i}: aggregate_mass inconsistent with children")
+        com_kids = (tree.aggregate_weight[kids, None] * tree.center_of_mass[kids]).sum(axis=0) / w_kids
+        if np.any(np.abs(tree.center_of_mass[i] - com_kids) > 1e-9 * scale):
+            report.append(f"node {i}: center_of_mass inconsistent with children")
+    return report
+
+
+def dump_outline(tree: Octree) -> str:
+    """One line per node (octree.py:316-327)."""
+    lines = []
+    for i in range(tree.num_nodes):
+        nd = tree.node(i)
+        mass = np.array2string(nd.aggregate_mass, precision=6)
+        lines.append(f"{'  ' * nd.depth}node {i} depth={nd.depth} "
+                     f"range=[{nd.point_range[0]},{nd.point_range[1]}) "
+                     f"children={len(nd.children)} weight={nd.aggregate_weight:.6g} mass={mass}")
+    return "\n".join(lines)
