@@ -1,0 +1,437 @@
+"""Benchmark of the B200 stochastic Barnes-Hut hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3]): electrical (Coulomb)
+potential of 2^22 area-uniform samples of one compact tilted torus
+(torus(0.25, 0.06) rotated 0.7 rad about x, shifted (0.1, 0.05, -0.1); masses
+1/M, seed 7) on a 1000 x 1000 slice plane at z = 0.03.  A step is one
+stochastic S=1 evaluation of all 10^6 queries (FP32 terms / FP64
+accumulation, tree prebuilt and resident).  Reported beside it:
+
+* median relative error of S=1 vs brute force (GPU brute force, FP64 accum.)
+* the GPU deterministic BH (same API, f32) beta sweep, log-log interpolated
+  to S=1's median error -> matched BH time and the speed-up
+* e2e: the same step through the public API (``evaluate_field``) from pinned
+  host queries to host results, copies inside the timed region
+* roofline of the stochastic kernel, cpu_baseline (the C oracle port on the
+  host cores, bounded sample), clocks sampled during the timed region.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+C oracle port, all host threads) on the same workload, bounded sample/step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+N_SIDE = 1000
+M_SOURCES = 2 ** 22
+METRIC = "queries/s at matched median rel. error vs brute force; speedup over det. BH"
+BETAS = (1.0, 1.5, 2.0, 3.0, 4.0, 6.0, 8.0, 10.0, 12.0, 16.0)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def workload(m=M_SOURCES, side=N_SIDE):
+    from paper_2506_02219_b200 import scenes as S
+    from paper_2506_02219_b200.types import KernelSpec
+    v, f = S.torus(0.25, 0.06)
+    v = S.rotate_x(v, 0.7) + np.array([0.1, 0.05, -0.1])
+    src = S.sample_mesh_surface(v, f, m, seed=7, kernel_kind="coulomb")
+    qs = S.make_queries(S.GridSpec("slice_plane", resolution=(side, side), origin=(0.0, 0.0, 0.03)))
+    return src, qs, KernelSpec("coulomb")
+
+
+def config_block():
+    return {"workload": "C4: coulomb, 2^22 tilted-torus surface samples, 1000^2 slice plane z=0.03",
+            "sources": M_SOURCES, "queries": N_SIDE * N_SIDE, "method": "stochastic S=1 paper_ratio",
+            "branching": {"stochastic": 4, "barnes_hut": 2}, "precision": "f32 terms, f64 accumulation",
+            "l2": "no flush; inputs larger than L2 (tree records ~0.3 GB, queries 24 MB)",
+            "parallelism": "query slabs (replica tree per rank)"}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+                 "utilization.gpu", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons, util = [], 0, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                u = float(parts[7])
+            except (ValueError, IndexError):
+                continue
+            mx = max(mx, m)
+            util.append(u)
+            if u > 0:
+                sm.append(s)
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(getattr(self, "lines", []))}
+
+
+def median_rel(est, ref):
+    return float(np.median(np.abs(est - ref) / np.abs(ref)))
+
+
+def loglog_interp(points, target):
+    """(err, ms) points; time at `target` error by log-log linear interpolation."""
+    pts = sorted(points)  # ascending error
+    for (e0, t0), (e1, t1) in zip(pts, pts[1:]):
+        if e0 <= target <= e1 and e0 > 0 and e1 > e0:
+            w = (math.log(target) - math.log(e0)) / (math.log(e1) - math.log(e0))
+            return math.exp(math.log(t0) + w * (math.log(t1) - math.log(t0)))
+    return None
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args):
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2506_02219_b200 as fs
+    from paper_2506_02219_b200 import _device as dev
+    from paper_2506_02219_b200 import _lib
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+
+    L = _lib.lib()
+    src, qs, kern = workload()
+    n = len(qs)
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- tree builds (setup, timed separately)
+    t0 = time.perf_counter()
+    tree4 = fs.build_tree(src, 4)
+    torch.cuda.synchronize()
+    build4_ms = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    tree2 = fs.build_tree(src, 2)
+    torch.cuda.synchronize()
+    build2_ms = (time.perf_counter() - t0) * 1e3
+    # warm builds (first call includes lazy module load / allocator growth)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fs.build_tree(src, 4)
+    e1.record()
+    torch.cuda.synchronize()
+    build4_warm_ms = e0.elapsed_time(e1)
+
+    q_dev = dev.to_device(qs.positions)
+    qoff = rank * n  # slab `rank` of a world*n query set: distinct RNG streams per rank
+    cfg_s1 = fs.EstimatorConfig("stochastic", samples_per_subdomain=1, seed=1, precision="f32")
+
+    def step():
+        return evaluate_field_device(cfg_s1, src, kern, q_dev, tree4, query_offset=qoff)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- launch count of one step (CUPTI via torch.profiler; outside the timed region)
+    launches_per_step = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        launches_per_step = sum(1 for e in prof.events()
+                                if e.device_type == torch.autograd.DeviceType.CUDA
+                                and "memcpy" not in e.name.lower() and "memset" not in e.name.lower())
+    except Exception as exc:  # pragma: no cover
+        log("profiler unavailable:", exc)
+
+    # ---- timed region: K steps, barrier + sync both sides, max over ranks
+    with Clocks(local) as clk:
+        barrier()
+        ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev_a.record()
+        for _ in range(args.steps):
+            res = step()
+        ev_b.record()
+        barrier()
+    step_ms = ev_a.elapsed_time(ev_b) / args.steps
+    if world > 1:
+        tt = torch.tensor([step_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms = float(tt.item())
+    value = world * n / (step_ms * 1e-3)
+
+    # ---- the stochastic kernel alone (events on the launching stream), for the roofline
+    perm = dev.empty(n, torch.int32)
+    _lib.check(L.fsb_query_order(C.c_void_p(dev.ptr(q_dev)), n, C.c_void_p(dev.ptr(perm)), sp))
+    raw = dev.empty(n, torch.float32)
+    vis = dev.empty(n, torch.int64)
+    h = C.c_void_p(tree4._device_tree().handle)
+
+    def kernel_only():
+        _lib.check(L.fsb_stochastic_batch(h, 0, kern.alpha, kern.distance_floor, 1,
+                                          C.c_void_p(dev.ptr(q_dev)), n,
+                                          C.c_void_p(dev.ptr(perm)), 1, 0, 1, qoff,
+                                          C.c_void_p(dev.ptr(raw)), C.c_void_p(dev.ptr(vis)),
+                                          None, None, sp))
+    kernel_only()
+    torch.cuda.synchronize()
+    reps = max(3, args.steps)
+    ev_a.record()
+    for _ in range(reps):
+        kernel_only()
+    ev_b.record()
+    torch.cuda.synchronize()
+    kern_ms = ev_a.elapsed_time(ev_b) / reps
+    visited_mean = float(vis.double().mean().item())
+
+    out = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (reference mesh generators, fixed seeds)", "config": config_block(),
+           "clocks": clk.summary()}
+    if launches_per_step is not None:
+        out["gpu_launches"] = launches_per_step * args.steps
+
+    # ---- accuracy and the matched-error BH comparison (rank 0 only)
+    if rank == 0:
+        truth = dev.empty(n, torch.float64)
+        pts_d, ms_d = dev.to_device(src.positions), dev.to_device(src.masses)
+        t0 = time.perf_counter()
+        _lib.check(L.fsb_brute_force_f32acc64(0, kern.alpha, kern.distance_floor,
+                                               C.c_void_p(dev.ptr(pts_d)), C.c_void_p(dev.ptr(ms_d)),
+                                               len(src), 1, C.c_void_p(dev.ptr(q_dev)), n,
+                                               C.c_void_p(dev.ptr(truth)), sp))
+        torch.cuda.synchronize()
+        brute_ms = (time.perf_counter() - t0) * 1e3
+        truth_h = truth.cpu().numpy()
+        s1 = res.values.cpu().numpy()
+        err_s1 = median_rel(s1, truth_h)
+        sweep = []
+        for beta in BETAS:
+            cfg = fs.EstimatorConfig("barnes_hut", beta=beta, precision="f32")
+            r = evaluate_field_device(cfg, src, kern, q_dev, tree2)
+            torch.cuda.synchronize()
+            ev_a.record()
+            r = evaluate_field_device(cfg, src, kern, q_dev, tree2)
+            ev_b.record()
+            torch.cuda.synchronize()
+            ms = ev_a.elapsed_time(ev_b)
+            err = median_rel(r.values.cpu().numpy(), truth_h)
+            sweep.append({"beta": beta, "ms": ms, "median_rel_err": err,
+                          "visited_mean": float(r.visited.double().mean().item())})
+            log(f"BH beta={beta}: {ms:.2f} ms, median rel err {err:.3e}")
+            if err < 0.5 * err_s1 or ms > 2000:
+                break
+        matched_ms = loglog_interp([(p["median_rel_err"], p["ms"]) for p in sweep], err_s1)
+        out["accuracy"] = {"s1_median_rel_err": err_s1, "s1_visited_mean": visited_mean,
+                           "truth": "GPU brute force (FP32 terms, FP64 accumulation)",
+                           "truth_ms": brute_ms}
+        out["barnes_hut_sweep"] = sweep
+        out["matched_bh_ms"] = matched_ms
+        out["speedup_vs_bh_at_matched_error"] = (matched_ms / step_ms) if matched_ms else None
+        out["tree_build_ms"] = {"d4_first_call": build4_ms, "d2_first_call": build2_ms,
+                                "d4_warm": build4_warm_ms}
+
+        # ---- roofline of the stochastic kernel: FP32+MUFU bound
+        pk = peaks()
+        f_mhz = float(pk.get("sm_max_mhz", 1965.0))
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        # dense control-variate part: N1 + N2 interactions per query (level-1 + level-2)
+        info = (C.c_int64 * 8)()
+        L.fsb_tree_info(h, info)
+        n_dense = _dense_interactions(tree4)
+        inter = n_dense * n
+        ach = inter / (kern_ms * 1e-3)
+        limit = min(128 * sms * f_mhz * 1e6 / 8, 16 * sms * f_mhz * 1e6 / 1)  # coulomb I=8, U=1
+        out["roofline"] = {"bound": "fp32+mufu", "achieved": ach * 10 / 1e12, "peak": limit * 10 / 1e12,
+                           "unit": "TFLOP/s", "frac": ach / limit, "traffic": None,
+                           "kernel": "k_stochastic<coulomb,f32>", "kernel_ms": kern_ms,
+                           "work": f"{n_dense} dense interactions/query x 10 flops (SURVEY 8d)",
+                           "peak_source": f"pipe rates x {sms} SMs x sm_max_mhz {f_mhz} (MEASURED_PEAKS.json)"}
+        # ---- e2e through the public API from pinned host memory
+        out["e2e"] = _e2e(args, fs, src, kern, qs, tree4, cfg_s1, world)
+        if args.cpu_baseline:
+            out["cpu_baseline"] = _cpu_baseline(tree4, src, qs, kern, args)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def _dense_interactions(tree) -> int:
+    """N1 + N2 for the d=4 tree: level-1 nodes plus children of internal level-1 nodes."""
+    cc = tree.child_count
+    cs = tree.child_start
+    ci = tree.child_index
+    lvl1 = ci[cs[0]:cs[0] + cc[0]]
+    return int(len(lvl1) + sum(int(cc[a]) for a in lvl1))
+
+
+def _e2e(args, fs, src, kern, qs, tree, cfg, world):
+    import torch
+    host = torch.empty((len(qs), 3), dtype=torch.float64, pin_memory=True)
+    host.numpy()[:] = qs.positions
+    qset = fs.QuerySet.__new__(fs.QuerySet)
+    object.__setattr__(qset, "positions", host.numpy())
+    for _ in range(max(1, args.warmup)):
+        fs.evaluate_field(cfg, src, kern, qset, tree=tree)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = fs.evaluate_field(cfg, src, kern, qset, tree=tree)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.steps
+    n = len(qs)
+    out_bytes = sum(a.nbytes for a in (r.values, r.raw, r.flagged, r.visited_nodes, r.path_steps,
+                                       r.path_count))
+    return {"value": n / dt, "unit": "queries/s", "h2d_bytes_per_step": int(host.numel() * 8),
+            "d2h_bytes_per_step": int(out_bytes), "ms_per_step": dt * 1e3,
+            "api": "paper_2506_02219_b200.evaluate_field (host numpy in/out)", "n_gpus": 1}
+
+
+def _cpu_baseline(tree, src, qs, kern, args):
+    """The C oracle port (reference algorithm) on the host cores, bounded sample."""
+    from oracle import oracle as O
+    n_sample = args.cpu_sample
+    idx = np.unique(np.linspace(0, len(qs) - 1, n_sample).astype(np.int64))
+    n_sample = len(idx)
+    q = np.ascontiguousarray(qs.positions[idx])
+    ca = tuple(np.ascontiguousarray(a) for a in tree.core_arrays())
+    out = np.zeros(n_sample)
+    z = [np.zeros(n_sample, dtype=np.int64) for _ in range(3)]
+    O.stochastic_batch(*ca, 0, kern.alpha, kern.distance_floor, q[:64], 1, 0, 1, 0, out[:64],
+                       z[0][:64], z[1][:64], z[2][:64])
+    t0 = time.perf_counter()
+    O.stochastic_batch(*ca, 0, kern.alpha, kern.distance_floor, q, 1, 0, 1, 0, out, *z)
+    dt = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": n_sample / dt, "unit": "queries/s", "cores": cores, "kind": "port",
+            "sample": f"{n_sample} queries of the C4 plane, stochastic S=1 f64 "
+                      f"(oracle/fastsum_oracle.c, OpenMP), tree from the GPU build"}
+
+
+# ----------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    src, qs, kern = workload()
+    t0 = time.perf_counter()
+    t = O.build_tree(src.positions, src.masses, src.weights, 4, 32)
+    build_s = time.perf_counter() - t0
+    ca = O.core_arrays(t)
+    n_sample = args.cpu_sample
+    rng = np.random.default_rng(0)
+    z = [np.zeros(n_sample, dtype=np.int64) for _ in range(3)]
+    out = np.zeros(n_sample)
+
+    def step(k):
+        idx = rng.integers(0, len(qs), n_sample)
+        q = np.ascontiguousarray(qs.positions[idx])
+        O.stochastic_batch(*ca, 0, kern.alpha, kern.distance_floor, q, 1, 0, 1, 0, out, *z)
+
+    for k in range(args.warmup):
+        step(k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        step(k)
+    dt = (time.perf_counter() - t0) / args.steps
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    v = n_sample / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference mesh generators, fixed seeds)", "config": config_block(),
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
+                             "sample": f"{n_sample} random queries of the C4 plane per step, "
+                                       f"stochastic S=1 f64, oracle/fastsum_oracle.c (OpenMP)"},
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "tree_build_s": build_s}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--cpu-sample", type=int, default=N_SIDE * N_SIDE)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -163,7 +163,10 @@ void or_barnes_hut_batch(const double *diam, const double *agg_mass, const doubl
     tree_t t = mk_tree(diam, agg_mass, com, cs, cc, ci, b, e, pts, ms, num_nodes, c);
 #pragma omp parallel
     {
-        int64_t *stack = (int64_t *)malloc(sizeof(int64_t) * (size_t)stack_cap);
+        /* the DFS stack never holds more than num_nodes entries; callers may pass a
+         * smaller (or zero) stack_cap, as the reference's signature allows */
+        int64_t cap = stack_cap > num_nodes + 8 ? stack_cap : num_nodes + 8;
+        int64_t *stack = (int64_t *)malloc(sizeof(int64_t) * (size_t)cap);
 #pragma omp for schedule(dynamic, 16)
         for (int64_t qi = 0; qi < n; ++qi) {
             double qx = q[3 * qi], qy = q[3 * qi + 1], qz = q[3 * qi + 2];

@@ -1,6 +1,7 @@
 // fs_abi.cu -- extern "C" boundary (include/fastsum_b200.h) over the device code.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -26,10 +27,11 @@ void set_error(const char* fmt, ...) {
 }
 
 // ---------------------------------------------------------- query ordering
-__global__ void k_qbbox(const double* __restrict__ q, int64_t n, float* __restrict__ out) {
+__global__ void k_qbbox(const double* __restrict__ q, int64_t n, float* __restrict__ part) {
   __shared__ float sm[6][256];
   float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
     for (int k = 0; k < 3; ++k) {
       float v = (float)q[3 * i + k];
       lo[k] = fminf(lo[k], v);
@@ -48,7 +50,15 @@ __global__ void k_qbbox(const double* __restrict__ q, int64_t n, float* __restri
       }
     __syncthreads();
   }
-  if (threadIdx.x < 6) out[threadIdx.x] = sm[threadIdx.x][0];
+  if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sm[threadIdx.x][0];
+}
+
+__global__ void k_qbbox_final(float* __restrict__ part, int nb) {
+  if (threadIdx.x >= 6) return;
+  int k = threadIdx.x;
+  float v = part[k];
+  for (int b = 1; b < nb; ++b) v = k < 3 ? fminf(v, part[b * 6 + k]) : fmaxf(v, part[b * 6 + k]);
+  part[k] = v;
 }
 
 __device__ __forceinline__ uint32_t spread10(uint32_t v) {
@@ -77,11 +87,13 @@ __global__ void k_qmorton(const double* __restrict__ q, int64_t n, const float* 
 static int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s) {
   if (n <= 0) return 0;
   Scratch bb, code, code2, idx;
-  FS_TRY(bb.alloc(6 * sizeof(float), s));
+  const int nb = (int)std::min<int64_t>(296, (n + 255) / 256);
+  FS_TRY(bb.alloc(6 * sizeof(float) * nb, s));
   FS_TRY(code.alloc(4 * n, s));
   FS_TRY(code2.alloc(4 * n, s));
   FS_TRY(idx.alloc(4 * n, s));
-  k_qbbox<<<1, 256, 0, s>>>(q, n, bb.as<float>());
+  k_qbbox<<<nb, 256, 0, s>>>(q, n, bb.as<float>());
+  k_qbbox_final<<<1, 32, 0, s>>>(bb.as<float>(), nb);
   k_qmorton<<<grid_for(n, 256), 256, 0, s>>>(q, n, bb.as<float>(), code.as<uint32_t>(),
                                              idx.as<int32_t>());
   size_t tb = 0;

@@ -4,6 +4,7 @@
 // winding); F32 = FP32 inputs/terms with FP64 accumulation (the reference's
 // precision="f32" contract, estimators.py:270-298), MUFU fast math for terms.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "fs_common.cuh"
@@ -93,7 +94,7 @@ __device__ __forceinline__ double ffr(const typename Prec<F64>::V4& g, double qx
 // increasing preorder index, so every record load is one broadcast transaction
 // while each lane still sees exactly its own sequence (results unchanged).
 template <int KID, bool F64>
-__global__ void __launch_bounds__(256) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
+__global__ void __launch_bounds__(64) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
                                             const typename Prec<F64>::V4* __restrict__ pa,
                                             const typename Prec<F64>::V4* __restrict__ pb,
                                             uint32_t nn, const double* __restrict__ q, int64_t n,
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(256) k_bh(const typename Prec<F64>::V4* __rest
   uint32_t i = live ? 0u : nn;
   double acc = 0.0;
   int64_t seen = 0;
+  const float beta_f = (float)beta;
   while (true) {
     uint32_t cur = warp_min_u32(i);
     if (cur >= nn) break;
@@ -122,7 +124,17 @@ __global__ void __launch_bounds__(256) k_bh(const typename Prec<F64>::V4* __rest
       else
         skip = (uint32_t)__float_as_int(mm.w);
       bool leaf = skip == cur + 1;
-      if (leaf || ffr<F64>(g, qx, qy, qz) >= beta) {
+      bool far;
+      if constexpr (F64) {
+        far = ffr<F64>(g, qx, qy, qz) >= beta;  // exact _ffr (_core.py:44-52)
+      } else {
+        // FP32 mode: ||q - c||^2 >= (beta * max(diam, 1e-12))^2, no sqrt / division
+        float dx = (float)qx - g.x, dy = (float)qy - g.y, dz = (float)qz - g.z;
+        float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        float thr = beta_f * fmaxf(g.w, 1e-12f);
+        far = d2 >= thr * thr;
+      }
+      if (leaf || far) {
         double v;
         if (g.w < 0) {  // multi-point leaf: exact per-point sum
           int64_t b, e;
@@ -416,10 +428,10 @@ __global__ void __launch_bounds__(256) k_brute64(const double* __restrict__ pts,
 
 // Fast flavour: FP32 terms, each thread owns QPT queries (register tiling over
 // one broadcast LDS.128 per source), FP32 partials folded into FP64 every
-// kFold sources; sources split across blockIdx.y when the query count alone
+// kFold = 32 sources (bounds FP32 cancellation error in signed-mass sums); sources split across blockIdx.y when the query count alone
 // cannot fill 148 SMs (deterministic: partials reduced in chunk order).
 constexpr int kBruteTile32 = 1024;
-constexpr int kFold = 256;
+constexpr int kFold = 32;
 template <int KID, int QPT>
 __global__ void __launch_bounds__(256) k_brute32(const float4* __restrict__ sa_g,
                                                  const float4* __restrict__ sb_g, int64_t m,
@@ -679,7 +691,9 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
       pa = t->pts32a;
       pb = t->pts32b;
     }
-    k_bh<KID, F64><<<grid_for(n, 256), 256, 0, s>>>(rec, pa, pb, (uint32_t)t->n, q, n, qperm,
+    // small blocks: per-warp work varies widely, and a block holds its slot until
+    // its slowest warp finishes
+    k_bh<KID, F64><<<grid_for(n, 64), 64, 0, s>>>(rec, pa, pb, (uint32_t)t->n, q, n, qperm,
                                                     beta, kp, (typename Prec<F64>::Out*)out,
                                                     visited);
   });
@@ -690,6 +704,12 @@ int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
                int64_t query_offset, void* out, int64_t* visited, int64_t* path_steps,
                int64_t* path_count, cudaStream_t s) {
   if (n <= 0) return 0;
+  if (!f64 && !std::getenv("FSB_DISABLE_FAST")) {
+    bool used = false;
+    FS_TRY(stochastic_fast(t, kid, alpha, dfloor, q, n, qperm, n_samples, rr_mode, seed,
+                           query_offset, (float*)out, visited, path_steps, path_count, s, &used));
+    if (used) return 0;
+  }
   FS_TRY(ensure_lo(t, f64, s));
   KParams kp = make_kp(alpha, dfloor);
   return with_kid(kid, f64, [&](auto K, auto P) {

@@ -1,6 +1,7 @@
 // fs_pack.cu -- packed node records for the evaluators, and device trees
 // assembled from reference-layout arrays (Octree.core_arrays(), octree.py:110-115).
 #include <algorithm>
+#include <vector>
 
 #include "fs_common.cuh"
 #include "fs_internal.h"
@@ -19,7 +20,8 @@ void free_tree(FsTree* t) {
                   t->child_start, t->child_count, t->child_index, t->begin, t->end, t->depth,
                   t->perm, t->points, t->masses, t->weights, t->lo2pre, t->pre2lo, t->skip,
                   t->fc_lo, t->bh32, t->bh64, t->lo_geo32, t->lo_mass32, t->lo_geo64,
-                  t->lo_mass64, t->lo_topo, t->pts32a, t->pts32b, t->pts64a, t->pts64b};
+                  t->lo_mass64, t->lo_topo, t->pts32a, t->pts32b, t->pts64a, t->pts64b,
+                  t->lo_cm32, t->lo_m12_32, t->lo_begin};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;
@@ -255,6 +257,72 @@ int ensure_lo(FsTree* t, bool f64, cudaStream_t s) {
     k_pack_pts<float, float4><<<grid_for(t->m, B), B, 0, s>>>(t->points, t->masses, t->m, t->c,
                                                               t->pts32a, t->pts32b);
   }
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+// ------------------------------------------------------------ fast records
+__global__ void k_pack_fast(const int32_t* __restrict__ lo2pre, const double* __restrict__ com,
+                            const double* __restrict__ am, const int64_t* __restrict__ b, int64_t n,
+                            int c, float4* __restrict__ cm, float2* __restrict__ m12,
+                            int32_t* __restrict__ lb) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t i = lo2pre[r];
+  cm[r] = make_float4((float)com[3 * i], (float)com[3 * i + 1], (float)com[3 * i + 2],
+                      (float)am[(int64_t)c * i]);
+  if (m12) m12[r] = make_float2((float)am[(int64_t)c * i + 1], (float)am[(int64_t)c * i + 2]);
+  lb[r] = (int32_t)b[i];
+}
+
+// per level: is the cell diameter uniform, and does the level hold a multi-point leaf?
+__global__ void k_level_check(int64_t r0, int64_t r1, int level, const int32_t* __restrict__ lo2pre,
+                              const double* __restrict__ diam, const int64_t* __restrict__ cc,
+                              const int64_t* __restrict__ b, const int64_t* __restrict__ e,
+                              int* __restrict__ flags) {
+  int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  int64_t i = lo2pre[r];
+  if (diam[i] != diam[lo2pre[r0]]) flags[0] = 1;
+  if (cc[i] == 0 && e[i] - b[i] > 1) atomicMin(&flags[1], level);
+}
+
+int ensure_fast(FsTree* t, cudaStream_t s) {
+  if (t->fast_ready) return 0;
+  const int B = 256;
+  FS_TRY(dalloc(&t->lo_cm32, t->n));
+  FS_TRY(dalloc(&t->lo_begin, t->n));
+  if (t->c >= 3) FS_TRY(dalloc(&t->lo_m12_32, t->n));
+  k_pack_fast<<<grid_for(t->n, B), B, 0, s>>>(t->lo2pre, t->com, t->agg_mass, t->begin, t->n, t->c,
+                                              t->lo_cm32, t->c >= 3 ? t->lo_m12_32 : nullptr,
+                                              t->lo_begin);
+  Scratch fl;
+  FS_TRY(fl.alloc(2 * sizeof(int), s));
+  int init[2] = {0, 1 << 30};
+  FS_CK(cudaMemcpyAsync(fl.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  for (int l = 0; l < t->num_levels; ++l) {
+    int64_t r0 = t->level_off[l], r1 = t->level_off[l + 1];
+    if (r1 > r0)
+      k_level_check<<<grid_for(r1 - r0, B), B, 0, s>>>(r0, r1, l, t->lo2pre, t->diameter,
+                                                       t->child_count, t->begin, t->end,
+                                                       fl.as<int>());
+  }
+  int res[2];
+  FS_CK(cudaMemcpyAsync(res, fl.p, sizeof(res), cudaMemcpyDeviceToHost, s));
+  std::vector<int64_t> firsts(t->num_levels);
+  for (int l = 0; l < t->num_levels && l < FsTree::kMaxLevels; ++l) {
+    double dd = 0;
+    int32_t pre = 0;
+    FS_CK(cudaMemcpyAsync(&pre, t->lo2pre + t->level_off[l], 4, cudaMemcpyDeviceToHost, s));
+    FS_CK(cudaStreamSynchronize(s));
+    FS_CK(cudaMemcpyAsync(&dd, t->diameter + pre, 8, cudaMemcpyDeviceToHost, s));
+    FS_CK(cudaStreamSynchronize(s));
+    t->level_diam[l] = (float)dd;
+  }
+  FS_CK(cudaStreamSynchronize(s));
+  t->uniform_diam = res[0] == 0 && t->num_levels <= FsTree::kMaxLevels;
+  t->first_multi_level = res[1];
+  t->fast_ready = true;
   FS_CK(cudaGetLastError());
   return 0;
 }

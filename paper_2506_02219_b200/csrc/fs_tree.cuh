@@ -46,6 +46,16 @@ struct FsTree {
   float4 *pts32a = nullptr, *pts32b = nullptr;  // permuted points {x,y,z,m0}, {m1,m2,0,0}
   double4 *pts64a = nullptr, *pts64b = nullptr;
   int root_kids = 0;  // child_count[0]
+
+  // fast FP32 stochastic / BH path (built by ensure_fast)
+  static constexpr int kMaxLevels = 256;
+  bool fast_ready = false;
+  bool uniform_diam = false;     // every level has one cell diameter (uniform splits)
+  int first_multi_level = 1 << 30;  // shallowest level holding a multi-point leaf
+  float level_diam[kMaxLevels];
+  float4* lo_cm32 = nullptr;     // {cx, cy, cz, m0} per level-order node
+  float2* lo_m12_32 = nullptr;   // {m1, m2} (winding)
+  int32_t* lo_begin = nullptr;   // point-range begin per level-order node
 };
 
 }  // namespace fsb

@@ -101,10 +101,16 @@ class DeviceField:
 
     def to_host(self) -> FieldResult:
         torch = dev.torch()
-        host = [x.cpu() for x in (self.values, self.raw, self.flagged, self.visited,
-                                  self.path_steps, self.path_count)]
+        # pinned (cached) host buffers, async copies, one synchronisation
+        host = []
+        for x in (self.values, self.raw, self.flagged, self.visited, self.path_steps,
+                  self.path_count):
+            h = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+            h.copy_(x, non_blocking=True)
+            host.append(h)
+        torch.cuda.current_stream().synchronize()
         return FieldResult(values=host[0].numpy(), raw=host[1].numpy(),
-                           flagged=host[2].numpy().astype(bool), visited_nodes=host[3].numpy(),
+                           flagged=host[2].numpy().view(bool), visited_nodes=host[3].numpy(),
                            path_steps=host[4].numpy(), path_count=host[5].numpy(),
                            method=self.method)
 

@@ -1,0 +1,151 @@
+"""Larger-scale GPU checks: bitwise vs the pinned oracle at 2^16-2^18 sources, and
+size-independent properties at the C4 scale (2^22 sources).  Needs a GPU."""
+
+import numpy as np
+import pytest
+
+import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fs():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_02219_b200 as fs
+    return fs
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    return oracle
+
+
+KEYS = ("bbox_min", "bbox_max", "diameter", "aggregate_mass", "aggregate_weight",
+        "center_of_mass", "child_start", "child_count", "child_index", "begin", "end", "depth",
+        "permuted_indices", "points", "masses", "weights")
+
+
+@pytest.mark.parametrize("d", [2, 4])
+def test_tree_2e18_bitwise_vs_oracle(fs, O, d):
+    s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 18, seed=11))
+    t = fs.build_tree(s, d)
+    ref = O.build_tree(s.positions, s.masses, s.weights, d, 32)
+    for k in KEYS:
+        np.testing.assert_array_equal(getattr(t, k), ref[k], err_msg=k)
+
+
+def _structure_ok(t, m):
+    n = t.num_nodes
+    perm = t.permuted_indices
+    assert np.array_equal(np.sort(perm), np.arange(m))
+    assert t.begin[0] == 0 and t.end[0] == m
+    cc, cs, ci = t.child_count, t.child_start, t.child_index
+    assert cs[-1] + cc[-1] == n - 1 and len(ci) == n - 1
+    # every non-root node appears exactly once as a child
+    assert np.array_equal(np.sort(ci), np.arange(1, n))
+    internal = np.nonzero(cc)[0]
+    first = ci[cs[internal]]
+    assert np.array_equal(first, internal + 1)  # preorder: first child follows its parent
+    # children ranges tile the parent: begin(first) = begin(parent), ends chain
+    assert np.array_equal(t.begin[first], t.begin[internal])
+    # leaves are single points except at the depth cap
+    multi = (cc == 0) & (t.end - t.begin > 1)
+    assert np.all(t.depth[multi] == t.max_depth)
+    # sibling ranges chain: end(child k) == begin(child k+1) inside each parent
+    slot_parent = np.repeat(np.arange(n), cc)
+    nxt = np.ones(n - 1, dtype=bool)
+    nxt[(cs[internal] + cc[internal] - 1)] = False
+    idx = np.nonzero(nxt)[0]
+    assert np.array_equal(t.end[ci[idx]], t.begin[ci[idx + 1]])
+    last = ci[cs[internal] + cc[internal] - 1]
+    assert np.array_equal(t.end[last], t.end[internal])
+    return slot_parent
+
+
+def test_c4_scale_tree_properties(fs):
+    s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 22, seed=7))
+    for d in (4, 2):
+        t = fs.build_tree(s, d)
+        m = len(s)
+        _structure_ok(t, m)
+        # aggregates: root mass = total charge, weights positive, com inside cells
+        np.testing.assert_allclose(t.aggregate_mass[0, 0], s.masses.sum(), rtol=1e-12)
+        assert np.all(t.aggregate_weight > 0)
+        tol = 1e-9
+        assert np.all(t.center_of_mass >= t.bbox_min - tol)
+        assert np.all(t.center_of_mass <= t.bbox_max + tol)
+        # child cell diameter is exactly parent/d up to rounding (octree.py:225)
+        cc, cs, ci = t.child_count, t.child_start, t.child_index
+        parent = np.repeat(np.arange(t.num_nodes), cc)
+        child = ci[np.repeat(cs, cc) + np.concatenate([np.arange(k) for k in cc])]
+        np.testing.assert_allclose(t.diameter[child], t.diameter[parent] / d, rtol=1e-12)
+        assert np.all(t.depth[child] == t.depth[parent] + 1)
+
+
+def test_stochastic_and_bh_f64_bitwise_vs_oracle_2e16(fs, O):
+    s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 16, seed=13))
+    rng = np.random.default_rng(5)
+    q = rng.uniform(-0.6, 0.6, (2048, 3))
+    kern = fs.KernelSpec("coulomb")
+    for d, method, extra in ((4, "stochastic", dict(seed=9, samples_per_subdomain=2)),
+                             (2, "barnes_hut", dict(beta=3.0)),
+                             (4, "barnes_hut", dict(beta=1.5, branching_per_dim=4))):
+        cfg = fs.EstimatorConfig(method, **extra)
+        t = fs.build_tree(s, d)
+        r = fs.evaluate_field(cfg, s, kern, fs.QuerySet(q), tree=t)
+        ref = O.build_tree(s.positions, s.masses, s.weights, d, 32)
+        ca = O.core_arrays(ref)
+        out = np.zeros(len(q))
+        vis = np.zeros(len(q), dtype=np.int64)
+        if method == "barnes_hut":
+            O.barnes_hut_batch(*ca, 0, 200.0, 1e-12, q, extra["beta"], 0, out, vis)
+        else:
+            st = np.zeros(len(q), dtype=np.int64)
+            pc = np.zeros(len(q), dtype=np.int64)
+            O.stochastic_batch(*ca, 0, 200.0, 1e-12, q, 2, 0, 9, 0, out, vis, st, pc)
+            np.testing.assert_array_equal(r.path_steps, st)
+        np.testing.assert_array_equal(r.values, out)
+        np.testing.assert_array_equal(r.visited_nodes, vis)
+
+
+def test_statistical_unbiasedness_moments(fs):
+    """Acceptance criterion 3 (test_acceptance.py:195-214) on the GPU moments kernel."""
+    from paper_2506_02219_b200 import _core
+    s = scenes.make_sources(256, seed=31)
+    tree = fs.build_tree(s, 4)
+    q = scenes.make_query_points(64, seed=32)
+    bf = fs.evaluate_field(fs.EstimatorConfig("brute_force"), s, fs.KernelSpec("coulomb"),
+                           fs.QuerySet(q))
+    n_reps = 100_000
+    mean = np.zeros(64)
+    var = np.zeros(64)
+    _core.stochastic_moments_batch(*tree.core_arrays(), 0, 200.0, 1e-12, q, n_reps, 0,
+                                   np.uint64(7), mean, var)
+    se = np.sqrt(var * (n_reps / (n_reps - 1)) / n_reps)
+    within = np.abs(mean - bf.values) <= 4.0 * se
+    assert within.mean() >= 0.95
+
+
+def test_query_order_and_offset_invariance(fs):
+    """Results depend only on (seed, global query index): reordering or slicing the
+    query set with the matching query_offset leaves every value unchanged (F8)."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 15, seed=17))
+    rng = np.random.default_rng(3)
+    q = rng.uniform(-0.7, 0.7, (4000, 3))
+    t = fs.build_tree(s, 4)
+    kern = fs.KernelSpec("coulomb")
+    for prec in ("f64", "f32"):
+        cfg = fs.EstimatorConfig("stochastic", seed=21, precision=prec)
+        full = evaluate_field_device(cfg, s, kern, fs.QuerySet(q), t).to_host().values
+        unordered = evaluate_field_device(cfg, s, kern, fs.QuerySet(q), t,
+                                          query_order=False).to_host().values
+        np.testing.assert_array_equal(full, unordered)
+        parts = [evaluate_field_device(cfg, s, kern, fs.QuerySet(q[a:b]), t,
+                                       query_offset=a).to_host().values
+                 for a, b in ((0, 1500), (1500, 2600), (2600, 4000))]
+        np.testing.assert_array_equal(np.concatenate(parts), full)
