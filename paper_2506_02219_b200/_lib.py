@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfastsum_b200.so")
+LIB_PATH = os.environ.get("FSB_LIB") or os.path.join(_HERE, "libfastsum_b200.so")
 
 _lib = None
 _lock = threading.Lock()

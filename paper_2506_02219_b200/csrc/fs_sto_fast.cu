@@ -14,13 +14,15 @@
 //    from shared memory: binary search of the sampled point index over the
 //    children's begins, far-field ratios from per-level cell diameters (cells
 //    are uniform splits, so one diameter per level, octree.py:225).
-//  * Deeper steps (mean ~0.35 levels per sample, so only a few lanes of a
-//    warp walk on) are served cooperatively: pending walks are handed four at
-//    a time to 8-lane groups, which sum a node's contiguous children with
-//    coalesced loads, find the child holding the sampled point by counting
-//    children begins <= j, and carry the chosen child's term and far-field
-//    ratio to the next level.  The reduction tree is fixed, so every query's
-//    result is independent of which warp or lane served it.
+//  * Deeper steps (only ~1/3 of samples descend below level 1, and fewer
+//    further) would leave most lanes idle if walked in place.  Instead each
+//    descending sample is pushed onto a block-wide shared-memory queue and the
+//    block serves the queue in rounds: every thread takes one walk and
+//    advances it by exactly one level (sum the node's contiguous children,
+//    pick the child holding the sampled point, roulette), pushing it back if it
+//    continues.  Finished walks store their residual in the owner's creation-
+//    ordered slot, and owners fold their slots in that order, so a query's
+//    result does not depend on which thread served its walks or when.
 //  * FP32 terms and residuals, FP64 accumulation across subdomains.
 #include <algorithm>
 
@@ -74,7 +76,7 @@ __device__ __forceinline__ float fdist(float4 c, float qx, float qy, float qz) {
 __device__ __forceinline__ float rr_fast(float rp, float rc, int mode) {
   if (mode == 1) return 0.5f;
   if (mode == 2) return 1.0f;
-  return fminf(__fdividef(fmaxf(rp, 1.0f), fmaxf(rc, 1e-12f)), 1.0f);
+  return fminf(fmaxf(rp, 1.0f) * rcp_ftz(fmaxf(rc, 1e-12f)), 1.0f);
 }
 
 // roulette uniform from the top 24 bits of the same splitmix draw
@@ -83,95 +85,52 @@ __device__ __forceinline__ float draw24(uint64_t key, uint64_t ctr) {
   return (float)(uint32_t)(x >> 40) * (1.0f / 16777216.0f);
 }
 
-// One deep walk (levels >= 2) of a sample that survived the level-1 roulette.
-// Children of a node are contiguous in level order; one pass over them sums
-// their terms and finds the child holding the sampled point (the last child
-// whose begin <= j), capturing that child's term and centre for the next level.
-template <int KID>
-__device__ __forceinline__ float deep_walk(const FastView& V, const KParams& kp, float qx,
-                                           float qy, float qz, int node, int j, float prr,
-                                           float rp, float cvn, uint64_t kr, float inv_count,
-                                           int rr_mode, int& dseen, int& dsteps) {
-  const float2 w0 = make_float2(0.f, 0.f);
-  int lvl = 2;
-  uint64_t rctr = 1;
-  float resid = 0.f;
-  int4 tp = V.topo[node];
-  while (tp.y > 0) {
-    const bool cmulti = lvl + 1 >= V.first_multi;
-    float ks = 0.f, tch = 0.f;
-    float4 cch = make_float4(0.f, 0.f, 0.f, 0.f);
-    int cidx = tp.x;
-#pragma unroll 4
-    for (int c = 0; c < tp.y; ++c) {
-      const int r = tp.x + c;
-      const float4 cr = V.cm[r];
-      const float2 wr = KID == KID_WINDING ? V.m12[r] : w0;
-      const int b = V.lb[r];
-      float v;
-      if (cmulti) {
-        int4 tc = V.topo[r];
-        v = (tc.y == 0 && tc.w - tc.z > 1) ? leaf_exact<KID>(V, tc.z, tc.w, qx, qy, qz, kp)
-                                           : fterm<KID>(cr, wr, qx, qy, qz, kp);
-      } else {
-        v = fterm<KID>(cr, wr, qx, qy, qz, kp);
-      }
-      ks += v;
-      if (b <= j) {
-        tch = v;
-        cch = cr;
-        cidx = r;
-      }
-    }
-    dseen += tp.y + 1;
-    const float pagg = (float)(tp.w - tp.z) * inv_count;
-    resid += __fdividef(ks - cvn, pagg * prr);
-    ++lvl;
-    const float rc = fdist(cch, qx, qy, qz) * V.inv_diam[min(lvl, kFastMaxLevels - 1)];
-    const float p = rr_fast(rp, rc, rr_mode);
-    if (draw24(kr, rctr++) >= p) break;
-    prr *= p;
-    ++dsteps;
-    tp = V.topo[cidx];
-    cvn = tch;
-    rp = rc;
-  }
-  return resid;
-}
+constexpr int kBlock = 256;  // threads (= queries) per tile
+#ifndef FSB_STO_MINB
+#define FSB_STO_MINB 4  // resident blocks per SM the register budget is sized for
+#endif
 
-constexpr int kBlock = 256;   // threads (= queries) per tile
-constexpr int kTaskCap = 768; // deferred deep walks held in shared memory
-constexpr int kSlots = 12;    // per-query result slots between flushes
+// Walks below level 1, held per block in global memory (structure of arrays,
+// L2-resident); two queues ping-pong between service rounds.  Field offsets
+// (per queue of capacity cap): kr u64 | meta | seq | node | j | prr | rp | cvn | resid.
+enum QField { QF_META = 0, QF_SEQ, QF_NODE, QF_J, QF_PRR, QF_RP, QF_CVN, QF_RESID };
+constexpr int kQueueBytesPerTask = 40;
 
 template <int KID>
-__global__ void __launch_bounds__(kBlock) k_sto_fast(FastView V, const double* __restrict__ q,
-                                                     int64_t n, const int32_t* __restrict__ qperm,
-                                                     int S, int rr_mode, uint64_t seed,
-                                                     int64_t qoff, KParams kp,
-                                                     float* __restrict__ out,
-                                                     int64_t* __restrict__ visited,
-                                                     int64_t* __restrict__ path_steps,
-                                                     int64_t* __restrict__ path_count) {
+__global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, const double* __restrict__ q,
+                                                        int64_t n,
+                                                        const int32_t* __restrict__ qperm, int S,
+                                                        int rr_mode, uint64_t seed, int64_t qoff,
+                                                        KParams kp, float* __restrict__ res_g,
+                                                        int res_stride,
+                                                        unsigned char* __restrict__ queues,
+                                                        int qcap, float* __restrict__ out,
+                                                        int64_t* __restrict__ visited,
+                                                        int64_t* __restrict__ path_steps,
+                                                        int64_t* __restrict__ path_count) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n1 = V.n1, n2 = V.n2;
-  // deferred-walk queue (SoA), per-query result slots, query coordinates
-  uint2* t_kr = reinterpret_cast<uint2*>(smem);
-  int* t_meta = reinterpret_cast<int*>(t_kr + kTaskCap);
-  int* t_node = t_meta + kTaskCap;
-  int* t_j = t_node + kTaskCap;
-  float* t_prr = reinterpret_cast<float*>(t_j + kTaskCap);
-  float* t_rp = t_prr + kTaskCap;
-  float* t_cvn = t_rp + kTaskCap;
-  float* r_val = t_cvn + kTaskCap;                             // [kSlots][kBlock]
-  int* r_cnt = reinterpret_cast<int*>(r_val + kSlots * kBlock);  // seen | steps << 16
-  float4* s_q = reinterpret_cast<float4*>(r_cnt + kSlots * kBlock);
-  int* s_count = reinterpret_cast<int*>(s_q + kBlock);
+  float4* s_q = reinterpret_cast<float4*>(smem);
+  int* s_seen = reinterpret_cast<int*>(s_q + kBlock);  // nodes read below level 1, per query
+  int* s_steps = s_seen + kBlock;                        // descents below level 1, per query
+  int* s_count = s_steps + kBlock;                       // [0]: queue A, [1]: queue B
   float4* s_cm1 = reinterpret_cast<float4*>(s_count + 4);
   int4* s_tp1 = reinterpret_cast<int4*>(s_cm1 + n1);
   float4* s_cm2 = reinterpret_cast<float4*>(s_tp1 + n1);
   float2* s_w1 = reinterpret_cast<float2*>(s_cm2 + n2);
   float2* s_w2 = s_w1 + (KID == KID_WINDING ? n1 : 0);
   int* s_b2 = reinterpret_cast<int*>(s_w2 + (KID == KID_WINDING ? n2 : 0));
+
+  unsigned char* const qbase = queues + (size_t)blockIdx.x * 2 * qcap * kQueueBytesPerTask;
+  // queue `w` (0/1), field f
+  auto QI = [&](int w, int f) -> int* {
+    return reinterpret_cast<int*>(qbase + (size_t)w * qcap * kQueueBytesPerTask +
+                                  (size_t)qcap * (8 + 4 * f));
+  };
+  auto QF = [&](int w, int f) -> float* { return reinterpret_cast<float*>(QI(w, f)); };
+  auto QK = [&](int w) -> uint2* {
+    return reinterpret_cast<uint2*>(qbase + (size_t)w * qcap * kQueueBytesPerTask);
+  };
 
   // ---- stage level 1 (root's children, level order 1..n1) and level 2
   for (int i = threadIdx.x; i < n1; i += blockDim.x) {
@@ -190,13 +149,102 @@ __global__ void __launch_bounds__(kBlock) k_sto_fast(FastView V, const double* _
     }
     s_b2[i] = b;
   }
-  if (threadIdx.x == 0) s_count[0] = 0;
+  if (threadIdx.x == 0) {
+    s_count[0] = 0;
+    s_count[1] = 0;
+  }
+  s_seen[threadIdx.x] = 0;
+  s_steps[threadIdx.x] = 0;
   __syncthreads();
 
   const int tid = threadIdx.x;
   const uint64_t hseed = mix64(seed + kGamma);
   const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
   const float2 w0 = make_float2(0.f, 0.f);
+  float* my_res = res_g + ((int64_t)blockIdx.x * kBlock) * res_stride;
+
+  // Serve all queued walks: each service round advances every queued walk by
+  // one level (sum the node's contiguous children, pick the child holding the
+  // sampled point, roulette); survivors go to the other queue, finished walks
+  // store their residual in the owner's creation-ordered slot.
+  auto drain = [&]() {
+    int src = 0;  // walks are always produced into queue 0 by the level-1 step
+    int cnt = s_count[0];
+    while (cnt > 0) {
+      const int dst = src ^ 1;
+      for (int i = tid; i < cnt; i += kBlock) {
+        const int meta = QI(src, QF_META)[i];
+        const int owner = meta & 0xff, lvl = (meta >> 8) & 0xff, a_ord = meta >> 16;
+        const int node = QI(src, QF_NODE)[i], jj = QI(src, QF_J)[i];
+        const float prr = QF(src, QF_PRR)[i], rp = QF(src, QF_RP)[i], cvn = QF(src, QF_CVN)[i];
+        float resid = QF(src, QF_RESID)[i];
+        const float4 qq = s_q[owner];
+        const int4 tp = V.topo[node];
+        bool cont = false;
+        if (tp.y > 0) {
+          const bool cmulti = lvl + 1 >= V.first_multi;
+          float ks = 0.f, tch = 0.f;
+          float4 cch = make_float4(0.f, 0.f, 0.f, 0.f);
+          int cidx = tp.x;
+#pragma unroll 4
+          for (int c = 0; c < tp.y; ++c) {
+            const int r = tp.x + c;
+            const float4 cr = V.cm[r];
+            const float2 wr = KID == KID_WINDING ? V.m12[r] : w0;
+            const int b = V.lb[r];
+            float v;
+            if (cmulti) {
+              int4 tc = V.topo[r];
+              v = (tc.y == 0 && tc.w - tc.z > 1)
+                      ? leaf_exact<KID>(V, tc.z, tc.w, qq.x, qq.y, qq.z, kp)
+                      : fterm<KID>(cr, wr, qq.x, qq.y, qq.z, kp);
+            } else {
+              v = fterm<KID>(cr, wr, qq.x, qq.y, qq.z, kp);
+            }
+            ks += v;
+            if (b <= jj) {  // children are ordered by begin: the last such holds j
+              tch = v;
+              cch = cr;
+              cidx = r;
+            }
+          }
+          atomicAdd(&s_seen[owner], tp.y + 1);
+          const int4 tpa = s_tp1[a_ord];
+          const float pagg = (float)(tp.w - tp.z) / (float)(tpa.w - tpa.z);
+          resid += (ks - cvn) * rcp_ftz(pagg * prr);
+          const float rc =
+              fdist(cch, qq.x, qq.y, qq.z) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
+          const float p = rr_fast(rp, rc, rr_mode);
+          const uint2 k2 = QK(src)[i];
+          const uint64_t kr = ((uint64_t)k2.y << 32) | k2.x;
+          if (draw24(kr, (uint64_t)(lvl - 1)) < p) {  // roulette counter = levels descended
+            cont = true;
+            atomicAdd(&s_steps[owner], 1);
+            const int pos = atomicAdd(&s_count[dst], 1);
+            QI(dst, QF_META)[pos] = owner | ((lvl + 1) << 8) | (a_ord << 16);
+            QI(dst, QF_SEQ)[pos] = QI(src, QF_SEQ)[i];
+            QI(dst, QF_NODE)[pos] = cidx;
+            QI(dst, QF_J)[pos] = jj;
+            QF(dst, QF_PRR)[pos] = prr * p;
+            QF(dst, QF_RP)[pos] = rc;
+            QF(dst, QF_CVN)[pos] = tch;
+            QF(dst, QF_RESID)[pos] = resid;
+            QK(dst)[pos] = k2;
+          }
+        }
+        if (!cont) my_res[(int64_t)owner * res_stride + QI(src, QF_SEQ)[i]] = resid;
+      }
+      __syncthreads();
+      cnt = s_count[dst];
+      __syncthreads();
+      if (tid == 0) s_count[src] = 0;
+      src = dst;
+      __syncthreads();
+    }
+    if (src == 1) {  // survivors ended in queue 1 (now empty): keep queue 0 as the producer
+      __syncthreads();
+    }
+  };
 
   for (int64_t base = (int64_t)blockIdx.x * kBlock; base < n; base += (int64_t)gridDim.x * kBlock) {
     const int64_t t = base + tid;
@@ -210,40 +258,10 @@ __global__ void __launch_bounds__(kBlock) k_sto_fast(FastView V, const double* _
     }
     s_q[tid] = make_float4(qx, qy, qz, 0.f);
     const uint64_t hq = key_fold(hseed, (uint64_t)(qi + qoff));
-    double acc = 0.0;       // control variates + level-1 residuals, (a, s) order
-    double acc_deep = 0.0;  // deeper residual increments, creation order
-    int64_t seen = 0, steps = 0, paths = 0;
-    int nslot = 0;
-
-    // deferred deep walks: every thread serves queued walks, owners fold
-    // their results in slot (= creation) order, so the sum is order-free
-    auto flush = [&]() {
-      const int cnt = s_count[0];
-      for (int i = tid; i < cnt; i += kBlock) {
-        const int meta = t_meta[i];
-        const int owner = meta & 0xff, slot = (meta >> 8) & 0xff, a_ord = meta >> 16;
-        const int4 tpa = s_tp1[a_ord];
-        const float4 qq = s_q[owner];
-        int dseen = 0, dsteps = 0;
-        const uint2 k2 = t_kr[i];
-        const float res = deep_walk<KID>(V, kp, qq.x, qq.y, qq.z, t_node[i], t_j[i], t_prr[i],
-                                         t_rp[i], t_cvn[i], ((uint64_t)k2.y << 32) | k2.x,
-                                         1.0f / (float)(tpa.w - tpa.z), rr_mode, dseen, dsteps);
-        r_val[slot * kBlock + owner] = res;
-        r_cnt[slot * kBlock + owner] = dseen | (dsteps << 16);
-      }
-      __syncthreads();
-      for (int k = 0; k < nslot; ++k) {
-        acc_deep += (double)r_val[k * kBlock + tid];
-        const int c = r_cnt[k * kBlock + tid];
-        seen += c & 0xffff;
-        steps += c >> 16;
-      }
-      nslot = 0;
-      __syncthreads();
-      if (tid == 0) s_count[0] = 0;
-      __syncthreads();
-    };
+    double acc = 0.0;  // control variates + level-1 residuals, (a, s) order
+    int seen = 0, steps = 0, paths = 0;
+    int nseq = 0;      // walks that went below level 1
+    int qbound = 0;    // upper bound of queue 0's length (block-uniform)
 
     for (int a_ord = 0; a_ord < n1; ++a_ord) {  // block-uniform
       ++seen;
@@ -313,25 +331,44 @@ __global__ void __launch_bounds__(kBlock) k_sto_fast(FastView V, const double* _
         const float4 c2 = s_cm2[lo];
         const float rc = fdist(c2, qx, qy, qz) * id2;
         const float p = rr_fast(rp_a, rc, rr_mode);
-        if (live && draw24(kr, 0) < p) {  // descends: defer the deeper steps
+        if (live && draw24(kr, 0) < p) {  // descends: queue the deeper steps
           ++steps;
-          const int pos = atomicAdd(s_count, 1);
-          t_meta[pos] = tid | (nslot << 8) | (a_ord << 16);
-          t_node[pos] = V.base2 + lo;
-          t_j[pos] = j;
-          t_prr[pos] = p;
-          t_rp[pos] = rc;
-          t_cvn[pos] = fterm<KID>(c2, KID == KID_WINDING ? s_w2[lo] : w0, qx, qy, qz, kp);
-          t_kr[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
-          ++nslot;
+          const int pos = atomicAdd(&s_count[0], 1);
+          QI(0, QF_META)[pos] = tid | (2 << 8) | (a_ord << 16);
+          QI(0, QF_SEQ)[pos] = nseq++;
+          QI(0, QF_NODE)[pos] = V.base2 + lo;
+          QI(0, QF_J)[pos] = j;
+          QF(0, QF_PRR)[pos] = p;
+          QF(0, QF_RP)[pos] = rc;
+          QF(0, QF_CVN)[pos] = fterm<KID>(c2, KID == KID_WINDING ? s_w2[lo] : w0, qx, qy, qz, kp);
+          QF(0, QF_RESID)[pos] = 0.f;
+          QK(0)[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
         }
-        if (__syncthreads_or(s_count[0] > kTaskCap - kBlock || nslot >= kSlots)) flush();
+        // an iteration queues at most kBlock walks: track a block-uniform upper
+        // bound of the queue length and look at the real length only near capacity
+        qbound += kBlock;
+        if (qbound + kBlock > qcap) {
+          __syncthreads();
+          qbound = s_count[0];
+          __syncthreads();
+          if (qbound + kBlock > qcap) {
+            drain();
+            qbound = 0;
+          }
+        }
       }
-      // every sample's level-1 residual is delta_a: cv + (S * delta_a) / S; the deeper
-      // increments are folded into acc_deep
+      // every sample's level-1 residual is delta_a: cv + (S * delta_a) / S
       acc += (double)cv + (double)delta_a;
     }
-    flush();
+    __syncthreads();
+    drain();
+    // owners fold their deeper residuals in creation order (query-intrinsic)
+    double acc_deep = 0.0;
+    for (int k2 = 0; k2 < nseq; ++k2) acc_deep += (double)my_res[(int64_t)tid * res_stride + k2];
+    seen += s_seen[tid];
+    steps += s_steps[tid];
+    s_seen[tid] = 0;
+    s_steps[tid] = 0;
     const double total = acc + acc_deep / (double)S;
     if (live) {
       out[qi] = (float)total;
@@ -339,6 +376,7 @@ __global__ void __launch_bounds__(kBlock) k_sto_fast(FastView V, const double* _
       if (path_steps) path_steps[qi] = steps;
       if (path_count) path_count[qi] = paths;
     }
+    __syncthreads();
   }
 }
 
@@ -368,7 +406,8 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     V.inv_diam[l] = 1.0f / std::max(d, 1e-12f);
   }
   bool wind = kid == KID_WINDING;
-  size_t smem = (size_t)kTaskCap * 32 + (size_t)kSlots * kBlock * 8 + kBlock * sizeof(float4) + 16 +
+  if ((int64_t)V.n1 * n_samples > (1 << 20)) return 0;
+  size_t smem = kBlock * (sizeof(float4) + 2 * sizeof(int)) + 16 +
                 (size_t)V.n1 * (sizeof(float4) + sizeof(int4)) + (size_t)V.n2 * sizeof(float4) +
                 (wind ? (size_t)(V.n1 + V.n2) * sizeof(float2) : 0) + (size_t)V.n2 * sizeof(int);
   if (smem > 200 * 1024) return 0;
@@ -388,8 +427,15 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     FS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B, smem));
     int64_t tiles = (n + B - 1) / B;
     int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
-    kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, rr_mode, seed, qoff, kp, out,
-                                         visited, path_steps, path_count);
+    const int stride = V.n1 * n_samples;  // result slots per query (walks below level 1)
+    // per-block walk queues: room for one tile's worth of level-2 walks, capped
+    const int qcap = (int)std::min<int64_t>((int64_t)B * stride + B, 16384) + 2 * B;
+    Scratch res, queues;
+    FS_TRY(res.alloc(sizeof(float) * (size_t)grid * B * stride, s));
+    FS_TRY(queues.alloc((size_t)grid * 2 * qcap * kQueueBytesPerTask, s));
+    kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, rr_mode, seed, qoff, kp,
+                                         res.as<float>(), stride, queues.as<unsigned char>(), qcap,
+                                         out, visited, path_steps, path_count);
     FS_CK(cudaGetLastError());
     return 0;
   };
