@@ -203,9 +203,10 @@ def run_ours(args):
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             step()
             torch.cuda.synchronize()
+        # our kernels: everything compiled into libfastsum_b200.so (fsb:: and its CUB sorts)
         launches_per_step = sum(1 for e in prof.events()
                                 if e.device_type == torch.autograd.DeviceType.CUDA
-                                and "memcpy" not in e.name.lower() and "memset" not in e.name.lower())
+                                and ("fsb" in e.name or "cub" in e.name.lower()))
     except Exception as exc:  # pragma: no cover
         log("profiler unavailable:", exc)
 
@@ -309,7 +310,8 @@ def run_ours(args):
         ach = inter / (kern_ms * 1e-3)
         limit = min(128 * sms * f_mhz * 1e6 / 8, 16 * sms * f_mhz * 1e6 / 1)  # coulomb I=8, U=1
         out["roofline"] = {"bound": "fp32+mufu", "achieved": ach * 10 / 1e12, "peak": limit * 10 / 1e12,
-                           "unit": "TFLOP/s", "frac": ach / limit, "traffic": None,
+                           "unit": "TFLOP/s", "frac": ach / limit,
+                           "traffic": _profiled_traffic("k_sto_fast<0>"),
                            "kernel": "k_stochastic<coulomb,f32>", "kernel_ms": kern_ms,
                            "work": f"{n_dense} dense interactions/query x 10 flops (SURVEY 8d)",
                            "peak_source": f"pipe rates x {sms} SMs x sm_max_mhz {f_mhz} (MEASURED_PEAKS.json)"}
@@ -322,6 +324,21 @@ def run_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def _profiled_traffic(kernel_key: str):
+    """DRAM bytes per launch of the kernel from the newest committed ncu summary."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.json")), reverse=True):
+        try:
+            with open(path) as f:
+                side = json.load(f)
+        except (OSError, ValueError):
+            continue
+        for name, k in side.items():
+            if kernel_key in name and "dram_bytes" in k:
+                return {"bytes_per_launch": k["dram_bytes"], "source": os.path.relpath(path, ROOT)}
+    return None
 
 
 def _dense_interactions(tree) -> int:

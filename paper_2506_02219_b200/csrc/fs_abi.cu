@@ -26,6 +26,18 @@ void set_error(const char* fmt, ...) {
   g_last_error = buf;
 }
 
+void retain_pool_memory() {
+  static thread_local int done_mask = 0;  // one bit per device (first 32 devices)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32 || (done_mask >> dev) & 1) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_mask |= 1 << dev;
+}
+
 // ---------------------------------------------------------- query ordering
 __global__ void k_qbbox(const double* __restrict__ q, int64_t n, float* __restrict__ part) {
   __shared__ float sm[6][256];

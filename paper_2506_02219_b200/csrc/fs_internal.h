@@ -25,6 +25,11 @@ void set_error(const char* fmt, ...);
     if (_rc != 0) return _rc;      \
   } while (0)
 
+// Keep freed stream-ordered allocations in the device's default pool instead of
+// returning them to the OS at every synchronisation (the default threshold 0
+// would re-map large scratch buffers on every call).
+void retain_pool_memory();
+
 // stream-ordered scratch buffer
 struct Scratch {
   void* p = nullptr;
@@ -34,6 +39,7 @@ struct Scratch {
   Scratch& operator=(const Scratch&) = delete;
   int alloc(size_t bytes, cudaStream_t st) {
     s = st;
+    retain_pool_memory();
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMallocAsync(&p, bytes, st);
     if (e != cudaSuccess) {

@@ -429,7 +429,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
     const int stride = V.n1 * n_samples;  // result slots per query (walks below level 1)
     // per-block walk queues: room for one tile's worth of level-2 walks, capped
-    const int qcap = (int)std::min<int64_t>((int64_t)B * stride + B, 16384) + 2 * B;
+    const int qcap = (int)std::min<int64_t>((int64_t)B * stride + B, 4096) + 2 * B;
     Scratch res, queues;
     FS_TRY(res.alloc(sizeof(float) * (size_t)grid * B * stride, s));
     FS_TRY(queues.alloc((size_t)grid * 2 * qcap * kQueueBytesPerTask, s));

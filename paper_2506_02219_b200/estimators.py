@@ -133,9 +133,12 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
     f32 = config.precision == "f32"
     prec = 1 if f32 else 0
     raw = dev.empty(n, torch.float32 if f32 else torch.float64)
-    visited = dev.zeros(n, torch.int64)
-    steps = dev.zeros(n, torch.int64)
-    count = dev.zeros(n, torch.int64)
+    visited = dev.empty(n, torch.int64)
+    # the stochastic kernels write every counter; the other methods report none
+    if config.method == "stochastic":
+        steps, count = dev.empty(n, torch.int64), dev.empty(n, torch.int64)
+    else:
+        steps, count = dev.zeros(n, torch.int64), dev.zeros(n, torch.int64)
     kid = kernel_id(kernel)
     alpha, dfloor = float(kernel.alpha), float(kernel.distance_floor)
     if config.method == "brute_force":
