@@ -91,29 +91,48 @@ constexpr int kBlock = 256;  // threads (= queries) per tile
 #endif
 
 // Walks below level 1, held per block in global memory (structure of arrays,
-// L2-resident); two queues ping-pong between service rounds.  Field offsets
-// (per queue of capacity cap): kr u64 | meta | seq | node | j | prr | rp | cvn | resid.
-enum QField { QF_META = 0, QF_SEQ, QF_NODE, QF_J, QF_PRR, QF_RP, QF_CVN, QF_RESID };
+// L2-resident); two queues ping-pong between service rounds.  Fixed capacity,
+// so every field address is base + constant offset + 4 * index.
+constexpr int kQcap = 4096 + 2 * kBlock;
 constexpr int kQueueBytesPerTask = 40;
+constexpr size_t kQueueBytes = (size_t)kQcap * kQueueBytesPerTask;  // one queue
+enum QField { QF_META = 0, QF_SEQ, QF_NODE, QF_J, QF_PRR, QF_RP, QF_CVN, QF_RESID };
+
+struct QueueRef {
+  unsigned char* base;  // queue w of this block
+  __device__ __forceinline__ int* i32(int f) const {
+    return reinterpret_cast<int*>(base + (size_t)kQcap * (8 + 4 * f));
+  }
+  __device__ __forceinline__ float* f32(int f) const {
+    return reinterpret_cast<float*>(base + (size_t)kQcap * (8 + 4 * f));
+  }
+  __device__ __forceinline__ uint2* key() const { return reinterpret_cast<uint2*>(base); }
+};
+
+// last index in [lo, lo + cnt) whose begin (low 31 bits of b[]) is <= j; b is sorted
+__device__ __forceinline__ int child_search(const int* b, int lo, int cnt, int j) {
+  const int end = lo + cnt;
+  for (int step = cnt > 1 ? 1 << (31 - __clz(cnt - 1)) : 0; step > 0; step >>= 1) {
+    const int t = lo + step;
+    if (t < end && (b[t] & 0x7fffffff) <= j) lo = t;
+  }
+  return lo;
+}
 
 template <int KID>
-__global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, const double* __restrict__ q,
-                                                        int64_t n,
-                                                        const int32_t* __restrict__ qperm, int S,
-                                                        int rr_mode, uint64_t seed, int64_t qoff,
-                                                        KParams kp, float* __restrict__ res_g,
-                                                        int res_stride,
-                                                        unsigned char* __restrict__ queues,
-                                                        int qcap, float* __restrict__ out,
-                                                        int64_t* __restrict__ visited,
-                                                        int64_t* __restrict__ path_steps,
-                                                        int64_t* __restrict__ path_count) {
+__global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
+    k_sto_fast(FastView V, const double* __restrict__ q, int64_t n,
+               const int32_t* __restrict__ qperm, int S, int rr_mode, uint64_t seed, int64_t qoff,
+               KParams kp, float* __restrict__ res_g, int res_stride,
+               unsigned char* __restrict__ queues, float* __restrict__ out,
+               int64_t* __restrict__ visited, int64_t* __restrict__ path_steps,
+               int64_t* __restrict__ path_count) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n1 = V.n1, n2 = V.n2;
   float4* s_q = reinterpret_cast<float4*>(smem);
   int* s_seen = reinterpret_cast<int*>(s_q + kBlock);  // nodes read below level 1, per query
   int* s_steps = s_seen + kBlock;                        // descents below level 1, per query
-  int* s_count = s_steps + kBlock;                       // [0]: queue A, [1]: queue B
+  int* s_count = s_steps + kBlock;                       // queue lengths
   float4* s_cm1 = reinterpret_cast<float4*>(s_count + 4);
   int4* s_tp1 = reinterpret_cast<int4*>(s_cm1 + n1);
   float4* s_cm2 = reinterpret_cast<float4*>(s_tp1 + n1);
@@ -121,16 +140,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, c
   float2* s_w2 = s_w1 + (KID == KID_WINDING ? n1 : 0);
   int* s_b2 = reinterpret_cast<int*>(s_w2 + (KID == KID_WINDING ? n2 : 0));
 
-  unsigned char* const qbase = queues + (size_t)blockIdx.x * 2 * qcap * kQueueBytesPerTask;
-  // queue `w` (0/1), field f
-  auto QI = [&](int w, int f) -> int* {
-    return reinterpret_cast<int*>(qbase + (size_t)w * qcap * kQueueBytesPerTask +
-                                  (size_t)qcap * (8 + 4 * f));
-  };
-  auto QF = [&](int w, int f) -> float* { return reinterpret_cast<float*>(QI(w, f)); };
-  auto QK = [&](int w) -> uint2* {
-    return reinterpret_cast<uint2*>(qbase + (size_t)w * qcap * kQueueBytesPerTask);
-  };
+  unsigned char* const qbase = queues + (size_t)blockIdx.x * 2 * kQueueBytes;
 
   // ---- stage level 1 (root's children, level order 1..n1) and level 2
   for (int i = threadIdx.x; i < n1; i += blockDim.x) {
@@ -168,30 +178,42 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, c
   // sampled point, roulette); survivors go to the other queue, finished walks
   // store their residual in the owner's creation-ordered slot.
   auto drain = [&]() {
-    int src = 0;  // walks are always produced into queue 0 by the level-1 step
+    int src = 0;  // the level-1 step always produces into queue 0
     int cnt = s_count[0];
     while (cnt > 0) {
-      const int dst = src ^ 1;
+      const QueueRef in{qbase + (size_t)src * kQueueBytes};
+      const QueueRef outq{qbase + (size_t)(src ^ 1) * kQueueBytes};
       for (int i = tid; i < cnt; i += kBlock) {
-        const int meta = QI(src, QF_META)[i];
+        const int meta = in.i32(QF_META)[i];
         const int owner = meta & 0xff, lvl = (meta >> 8) & 0xff, a_ord = meta >> 16;
-        const int node = QI(src, QF_NODE)[i], jj = QI(src, QF_J)[i];
-        const float prr = QF(src, QF_PRR)[i], rp = QF(src, QF_RP)[i], cvn = QF(src, QF_CVN)[i];
-        float resid = QF(src, QF_RESID)[i];
+        const int node = in.i32(QF_NODE)[i], jj = in.i32(QF_J)[i];
+        const int seq = in.i32(QF_SEQ)[i];
+        float resid = in.f32(QF_RESID)[i];
         const float4 qq = s_q[owner];
         const int4 tp = V.topo[node];
         bool cont = false;
         if (tp.y > 0) {
+          const float prr = in.f32(QF_PRR)[i], rp = in.f32(QF_RP)[i], cvn = in.f32(QF_CVN)[i];
           const bool cmulti = lvl + 1 >= V.first_multi;
-          float ks = 0.f, tch = 0.f;
-          float4 cch = make_float4(0.f, 0.f, 0.f, 0.f);
-          int cidx = tp.x;
-#pragma unroll 4
-          for (int c = 0; c < tp.y; ++c) {
+          float ks0 = 0.f, ks1 = 0.f;
+          int le = 0;  // children whose begin <= j: the last of them holds j
+          int c = 0;
+          if (!cmulti) {
+            for (; c + 1 < tp.y; c += 2) {
+              const int r = tp.x + c;
+              const float4 c0 = V.cm[r], c1 = V.cm[r + 1];
+              const int b0 = V.lb[r], b1 = V.lb[r + 1];
+              const float2 u0 = KID == KID_WINDING ? V.m12[r] : w0;
+              const float2 u1 = KID == KID_WINDING ? V.m12[r + 1] : w0;
+              ks0 += fterm<KID>(c0, u0, qq.x, qq.y, qq.z, kp);
+              ks1 += fterm<KID>(c1, u1, qq.x, qq.y, qq.z, kp);
+              le += (b0 <= jj) + (b1 <= jj);
+            }
+          }
+          for (; c < tp.y; ++c) {
             const int r = tp.x + c;
             const float4 cr = V.cm[r];
             const float2 wr = KID == KID_WINDING ? V.m12[r] : w0;
-            const int b = V.lb[r];
             float v;
             if (cmulti) {
               int4 tc = V.topo[r];
@@ -201,13 +223,12 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, c
             } else {
               v = fterm<KID>(cr, wr, qq.x, qq.y, qq.z, kp);
             }
-            ks += v;
-            if (b <= jj) {  // children are ordered by begin: the last such holds j
-              tch = v;
-              cch = cr;
-              cidx = r;
-            }
+            ks0 += v;
+            le += V.lb[r] <= jj;
           }
+          const float ks = ks0 + ks1;
+          const int cidx = tp.x + le - 1;
+          const float4 cch = V.cm[cidx];  // L1 hit: just streamed
           atomicAdd(&s_seen[owner], tp.y + 1);
           const int4 tpa = s_tp1[a_ord];
           const float pagg = (float)(tp.w - tp.z) / (float)(tpa.w - tpa.z);
@@ -215,37 +236,36 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, c
           const float rc =
               fdist(cch, qq.x, qq.y, qq.z) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
           const float p = rr_fast(rp, rc, rr_mode);
-          const uint2 k2 = QK(src)[i];
+          const uint2 k2 = in.key()[i];
           const uint64_t kr = ((uint64_t)k2.y << 32) | k2.x;
           if (draw24(kr, (uint64_t)(lvl - 1)) < p) {  // roulette counter = levels descended
             cont = true;
             atomicAdd(&s_steps[owner], 1);
-            const int pos = atomicAdd(&s_count[dst], 1);
-            QI(dst, QF_META)[pos] = owner | ((lvl + 1) << 8) | (a_ord << 16);
-            QI(dst, QF_SEQ)[pos] = QI(src, QF_SEQ)[i];
-            QI(dst, QF_NODE)[pos] = cidx;
-            QI(dst, QF_J)[pos] = jj;
-            QF(dst, QF_PRR)[pos] = prr * p;
-            QF(dst, QF_RP)[pos] = rc;
-            QF(dst, QF_CVN)[pos] = tch;
-            QF(dst, QF_RESID)[pos] = resid;
-            QK(dst)[pos] = k2;
+            const float2 wc = KID == KID_WINDING ? V.m12[cidx] : w0;
+            const int pos = atomicAdd(&s_count[src ^ 1], 1);
+            outq.i32(QF_META)[pos] = owner | ((lvl + 1) << 8) | (a_ord << 16);
+            outq.i32(QF_SEQ)[pos] = seq;
+            outq.i32(QF_NODE)[pos] = cidx;
+            outq.i32(QF_J)[pos] = jj;
+            outq.f32(QF_PRR)[pos] = prr * p;
+            outq.f32(QF_RP)[pos] = rc;
+            outq.f32(QF_CVN)[pos] = fterm<KID>(cch, wc, qq.x, qq.y, qq.z, kp);
+            outq.f32(QF_RESID)[pos] = resid;
+            outq.key()[pos] = k2;
           }
         }
-        if (!cont) my_res[(int64_t)owner * res_stride + QI(src, QF_SEQ)[i]] = resid;
+        if (!cont) my_res[(int64_t)owner * res_stride + seq] = resid;
       }
       __syncthreads();
-      cnt = s_count[dst];
+      cnt = s_count[src ^ 1];
       __syncthreads();
       if (tid == 0) s_count[src] = 0;
-      src = dst;
-      __syncthreads();
-    }
-    if (src == 1) {  // survivors ended in queue 1 (now empty): keep queue 0 as the producer
+      src ^= 1;
       __syncthreads();
     }
   };
 
+  const QueueRef q0{qbase};
   for (int64_t base = (int64_t)blockIdx.x * kBlock; base < n; base += (int64_t)gridDim.x * kBlock) {
     const int64_t t = base + tid;
     const bool live = t < n;
@@ -276,37 +296,29 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, c
       }
       // ---- dense control variate: cv(a) and the hoisted swap over a's children
       const float cv = fterm<KID>(ca, wa, qx, qy, qz, kp);
-      const int k0 = tpa.x - V.base2, cc = tpa.y;
-      float ks0 = 0.f, ks1 = 0.f;
-      int k = 0;
-      for (; k + 1 < cc; k += 2) {
-        const int i0 = k0 + k, i1 = i0 + 1;
-        float v0, v1;
-        if (l2_multi && s_b2[i0] < 0) {
-          int4 tp = V.topo[V.base2 + i0];
-          v0 = leaf_exact<KID>(V, tp.z, tp.w, qx, qy, qz, kp);
-        } else {
-          v0 = fterm<KID>(s_cm2[i0], KID == KID_WINDING ? s_w2[i0] : w0, qx, qy, qz, kp);
+      const int k0 = tpa.x - V.base2, cc = tpa.y, kend = k0 + cc;
+      float ks0 = 0.f, ks1 = 0.f, ks2 = 0.f, ks3 = 0.f;
+      if (!l2_multi) {
+        int k = k0;
+        for (; k + 3 < kend; k += 4) {
+          ks0 += fterm<KID>(s_cm2[k], KID == KID_WINDING ? s_w2[k] : w0, qx, qy, qz, kp);
+          ks1 += fterm<KID>(s_cm2[k + 1], KID == KID_WINDING ? s_w2[k + 1] : w0, qx, qy, qz, kp);
+          ks2 += fterm<KID>(s_cm2[k + 2], KID == KID_WINDING ? s_w2[k + 2] : w0, qx, qy, qz, kp);
+          ks3 += fterm<KID>(s_cm2[k + 3], KID == KID_WINDING ? s_w2[k + 3] : w0, qx, qy, qz, kp);
         }
-        if (l2_multi && s_b2[i1] < 0) {
-          int4 tp = V.topo[V.base2 + i1];
-          v1 = leaf_exact<KID>(V, tp.z, tp.w, qx, qy, qz, kp);
-        } else {
-          v1 = fterm<KID>(s_cm2[i1], KID == KID_WINDING ? s_w2[i1] : w0, qx, qy, qz, kp);
-        }
-        ks0 += v0;
-        ks1 += v1;
-      }
-      if (k < cc) {
-        const int i0 = k0 + k;
-        if (l2_multi && s_b2[i0] < 0) {
-          int4 tp = V.topo[V.base2 + i0];
-          ks0 += leaf_exact<KID>(V, tp.z, tp.w, qx, qy, qz, kp);
-        } else {
-          ks0 += fterm<KID>(s_cm2[i0], KID == KID_WINDING ? s_w2[i0] : w0, qx, qy, qz, kp);
+        for (; k < kend; ++k)
+          ks0 += fterm<KID>(s_cm2[k], KID == KID_WINDING ? s_w2[k] : w0, qx, qy, qz, kp);
+      } else {
+        for (int k = k0; k < kend; ++k) {
+          if (s_b2[k] < 0) {
+            int4 tp = V.topo[V.base2 + k];
+            ks0 += leaf_exact<KID>(V, tp.z, tp.w, qx, qy, qz, kp);
+          } else {
+            ks0 += fterm<KID>(s_cm2[k], KID == KID_WINDING ? s_w2[k] : w0, qx, qy, qz, kp);
+          }
         }
       }
-      const float delta_a = (ks0 + ks1) - cv;
+      const float delta_a = ((ks0 + ks1) + (ks2 + ks3)) - cv;
       const int count_a = tpa.w - tpa.z;
       const float rp_a = fdist(ca, qx, qy, qz) * id1;
       const uint64_t ha = key_fold(hq, (uint64_t)a_ord);
@@ -319,14 +331,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, c
         int j = tpa.z + (int)__dmul_rn(u0, (double)count_a);
         if (j >= tpa.w) j = tpa.w - 1;
         // level-1 step from shared memory: the swap at `a` is the hoisted delta_a
-        int lo = k0, hi = k0 + cc;
-        while (hi - lo > 1) {
-          int mid = (lo + hi) >> 1;
-          if ((s_b2[mid] & 0x7fffffff) <= j)
-            lo = mid;
-          else
-            hi = mid;
-        }
+        const int lo = child_search(s_b2, k0, cc, j);
         seen += cc + 1;
         const float4 c2 = s_cm2[lo];
         const float rc = fdist(c2, qx, qy, qz) * id2;
@@ -334,24 +339,25 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB) k_sto_fast(FastView V, c
         if (live && draw24(kr, 0) < p) {  // descends: queue the deeper steps
           ++steps;
           const int pos = atomicAdd(&s_count[0], 1);
-          QI(0, QF_META)[pos] = tid | (2 << 8) | (a_ord << 16);
-          QI(0, QF_SEQ)[pos] = nseq++;
-          QI(0, QF_NODE)[pos] = V.base2 + lo;
-          QI(0, QF_J)[pos] = j;
-          QF(0, QF_PRR)[pos] = p;
-          QF(0, QF_RP)[pos] = rc;
-          QF(0, QF_CVN)[pos] = fterm<KID>(c2, KID == KID_WINDING ? s_w2[lo] : w0, qx, qy, qz, kp);
-          QF(0, QF_RESID)[pos] = 0.f;
-          QK(0)[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
+          q0.i32(QF_META)[pos] = tid | (2 << 8) | (a_ord << 16);
+          q0.i32(QF_SEQ)[pos] = nseq++;
+          q0.i32(QF_NODE)[pos] = V.base2 + lo;
+          q0.i32(QF_J)[pos] = j;
+          q0.f32(QF_PRR)[pos] = p;
+          q0.f32(QF_RP)[pos] = rc;
+          q0.f32(QF_CVN)[pos] =
+              fterm<KID>(c2, KID == KID_WINDING ? s_w2[lo] : w0, qx, qy, qz, kp);
+          q0.f32(QF_RESID)[pos] = 0.f;
+          q0.key()[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
         }
         // an iteration queues at most kBlock walks: track a block-uniform upper
         // bound of the queue length and look at the real length only near capacity
         qbound += kBlock;
-        if (qbound + kBlock > qcap) {
+        if (qbound + kBlock > kQcap) {
           __syncthreads();
           qbound = s_count[0];
           __syncthreads();
-          if (qbound + kBlock > qcap) {
+          if (qbound + kBlock > kQcap) {
             drain();
             qbound = 0;
           }
@@ -428,14 +434,12 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     int64_t tiles = (n + B - 1) / B;
     int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
     const int stride = V.n1 * n_samples;  // result slots per query (walks below level 1)
-    // per-block walk queues: room for one tile's worth of level-2 walks, capped
-    const int qcap = (int)std::min<int64_t>((int64_t)B * stride + B, 4096) + 2 * B;
     Scratch res, queues;
     FS_TRY(res.alloc(sizeof(float) * (size_t)grid * B * stride, s));
-    FS_TRY(queues.alloc((size_t)grid * 2 * qcap * kQueueBytesPerTask, s));
+    FS_TRY(queues.alloc((size_t)grid * 2 * kQueueBytes, s));
     kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, rr_mode, seed, qoff, kp,
-                                         res.as<float>(), stride, queues.as<unsigned char>(), qcap,
-                                         out, visited, path_steps, path_count);
+                                         res.as<float>(), stride, queues.as<unsigned char>(), out,
+                                         visited, path_steps, path_count);
     FS_CK(cudaGetLastError());
     return 0;
   };
