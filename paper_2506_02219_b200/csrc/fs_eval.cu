@@ -94,71 +94,81 @@ __device__ __forceinline__ double ffr(const typename Prec<F64>::V4& g, double qx
 // increasing preorder index, so every record load is one broadcast transaction
 // while each lane still sees exactly its own sequence (results unchanged).
 template <int KID, bool F64>
-__global__ void __launch_bounds__(64) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
+__global__ void __launch_bounds__(128) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
                                             const typename Prec<F64>::V4* __restrict__ pa,
                                             const typename Prec<F64>::V4* __restrict__ pb,
                                             uint32_t nn, const double* __restrict__ q, int64_t n,
                                             const int32_t* __restrict__ qperm, double beta,
                                             KParams kp, typename Prec<F64>::Out* __restrict__ out,
-                                            int64_t* __restrict__ visited) {
+                                            int64_t* __restrict__ visited,
+                                            unsigned int* __restrict__ work) {
   using V4 = typename Prec<F64>::V4;
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  bool live = t < n;
-  int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
-  double qx = 0, qy = 0, qz = 0;
-  if (live) load_query(q, qi, qx, qy, qz);
-  uint32_t i = live ? 0u : nn;
-  double acc = 0.0;
-  int64_t seen = 0;
+  const int lane = threadIdx.x & 31;
   const float beta_f = (float)beta;
+  // persistent warps take 32-query chunks (in the caller's coherent order) from a
+  // global counter: per-chunk cost varies by orders of magnitude near the surface
   while (true) {
-    uint32_t cur = warp_min_u32(i);
-    if (cur >= nn) break;
-    if (i == cur) {
-      V4 g = rec[2 * (int64_t)cur];
-      V4 mm = rec[2 * (int64_t)cur + 1];
-      ++seen;
-      uint32_t skip;
-      if constexpr (F64)
-        skip = (uint32_t)__double_as_longlong(mm.w);
-      else
-        skip = (uint32_t)__float_as_int(mm.w);
-      bool leaf = skip == cur + 1;
-      bool far;
-      if constexpr (F64) {
-        far = ffr<F64>(g, qx, qy, qz) >= beta;  // exact _ffr (_core.py:44-52)
-      } else {
-        // FP32 mode: ||q - c||^2 >= (beta * max(diam, 1e-12))^2, no sqrt / division
-        float dx = (float)qx - g.x, dy = (float)qy - g.y, dz = (float)qz - g.z;
-        float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        float thr = beta_f * fmaxf(g.w, 1e-12f);
-        far = d2 >= thr * thr;
-      }
-      if (leaf || far) {
-        double v;
-        if (g.w < 0) {  // multi-point leaf: exact per-point sum
-          int64_t b, e;
-          if constexpr (F64) {
-            b = __double_as_longlong(mm.x);
-            e = __double_as_longlong(mm.y);
-          } else {
-            b = __float_as_int(mm.x);
-            e = __float_as_int(mm.y);
-          }
-          v = leaf_points_sum<KID, F64>(pa, pb, b, e, qx, qy, qz, kp);
+    unsigned int chunk = 0;
+    if (lane == 0) chunk = atomicAdd(work, 1u);
+    chunk = __shfl_sync(0xffffffffu, chunk, 0);
+    const int64_t t = (int64_t)chunk * 32 + lane;
+    if ((int64_t)chunk * 32 >= n) break;
+    const bool live = t < n;
+    const int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
+    double qx = 0, qy = 0, qz = 0;
+    if (live) load_query(q, qi, qx, qy, qz);
+    uint32_t i = live ? 0u : nn;
+    double acc = 0.0;
+    int64_t seen = 0;
+    while (true) {
+      uint32_t cur = warp_min_u32(i);
+      if (cur >= nn) break;
+      if (i == cur) {
+        V4 g = rec[2 * (int64_t)cur];
+        V4 mm = rec[2 * (int64_t)cur + 1];
+        ++seen;
+        uint32_t skip;
+        if constexpr (F64)
+          skip = (uint32_t)__double_as_longlong(mm.w);
+        else
+          skip = (uint32_t)__float_as_int(mm.w);
+        bool leaf = skip == cur + 1;
+        bool far;
+        if constexpr (F64) {
+          far = ffr<F64>(g, qx, qy, qz) >= beta;  // exact _ffr (_core.py:44-52)
         } else {
-          v = term<KID, F64>(g, mm, qx, qy, qz, kp);
+          // FP32 mode: ||q - c||^2 >= (beta * max(diam, 1e-12))^2, no sqrt / division
+          float dx = (float)qx - g.x, dy = (float)qy - g.y, dz = (float)qz - g.z;
+          float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+          float thr = beta_f * fmaxf(g.w, 1e-12f);
+          far = d2 >= thr * thr;
         }
-        acc = dadd<F64>(acc, v);
-        i = skip;
-      } else {
-        i = cur + 1;
+        if (leaf || far) {
+          double v;
+          if (g.w < 0) {  // multi-point leaf: exact per-point sum
+            int64_t b, e;
+            if constexpr (F64) {
+              b = __double_as_longlong(mm.x);
+              e = __double_as_longlong(mm.y);
+            } else {
+              b = __float_as_int(mm.x);
+              e = __float_as_int(mm.y);
+            }
+            v = leaf_points_sum<KID, F64>(pa, pb, b, e, qx, qy, qz, kp);
+          } else {
+            v = term<KID, F64>(g, mm, qx, qy, qz, kp);
+          }
+          acc = dadd<F64>(acc, v);
+          i = skip;
+        } else {
+          i = cur + 1;
+        }
       }
     }
-  }
-  if (live) {
-    out[qi] = (typename Prec<F64>::Out)acc;
-    if (visited) visited[qi] = seen;
+    if (live) {
+      out[qi] = (typename Prec<F64>::Out)acc;
+      if (visited) visited[qi] = seen;
+    }
   }
 }
 
@@ -677,6 +687,9 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
   FS_TRY(ensure_bh(t, f64, s));
   FS_TRY(ensure_lo(t, f64, s));  // packed points for multi-point leaves
   KParams kp = make_kp(alpha, dfloor);
+  Scratch work;  // chunk counter of the persistent warps
+  FS_TRY(work.alloc(sizeof(unsigned int), s));
+  FS_CK(cudaMemsetAsync(work.p, 0, sizeof(unsigned int), s));
   return with_kid(kid, f64, [&](auto K, auto P) {
     constexpr int KID = decltype(K)::value;
     constexpr bool F64 = decltype(P)::value;
@@ -691,11 +704,14 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
       pa = t->pts32a;
       pb = t->pts32b;
     }
-    // small blocks: per-warp work varies widely, and a block holds its slot until
-    // its slowest warp finishes
-    k_bh<KID, F64><<<grid_for(n, 64), 64, 0, s>>>(rec, pa, pb, (uint32_t)t->n, q, n, qperm,
-                                                    beta, kp, (typename Prec<F64>::Out*)out,
-                                                    visited);
+    int per_sm = 1, dev = 0;
+    cudaGetDevice(&dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bh<KID, F64>, 128, 0);
+    const int64_t grid =
+        std::min<int64_t>((n + 127) / 128, (int64_t)sm_count() * std::max(per_sm, 1));
+    k_bh<KID, F64><<<(unsigned)grid, 128, 0, s>>>(rec, pa, pb, (uint32_t)t->n, q, n, qperm, beta,
+                                                   kp, (typename Prec<F64>::Out*)out, visited,
+                                                   work.as<unsigned int>());
   });
 }
 

@@ -90,31 +90,26 @@ constexpr int kBlock = 256;  // threads (= queries) per tile
 #define FSB_STO_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
 
-// Walks below level 1, held per block in global memory (structure of arrays,
-// L2-resident); two queues ping-pong between service rounds.  Fixed capacity,
-// so every field address is base + constant offset + 4 * index.
+// Walks below level 1, held per block in global memory (array of 48-byte
+// records, L2-resident); two queues ping-pong between service rounds.
+// Record: int4 {meta = owner | lvl << 8 | a_ord << 16, seq, node, j},
+//         float4 {prr, rp, cvn, resid}, uint4 {kr.lo, kr.hi, -, -}.
 constexpr int kQcap = 4096 + 2 * kBlock;
-constexpr int kQueueBytesPerTask = 40;
-constexpr size_t kQueueBytes = (size_t)kQcap * kQueueBytesPerTask;  // one queue
-enum QField { QF_META = 0, QF_SEQ, QF_NODE, QF_J, QF_PRR, QF_RP, QF_CVN, QF_RESID };
+constexpr size_t kQueueBytes = (size_t)kQcap * 48;  // one queue
 
-struct QueueRef {
-  unsigned char* base;  // queue w of this block
-  __device__ __forceinline__ int* i32(int f) const {
-    return reinterpret_cast<int*>(base + (size_t)kQcap * (8 + 4 * f));
-  }
-  __device__ __forceinline__ float* f32(int f) const {
-    return reinterpret_cast<float*>(base + (size_t)kQcap * (8 + 4 * f));
-  }
-  __device__ __forceinline__ uint2* key() const { return reinterpret_cast<uint2*>(base); }
+struct Walk {
+  int4 a;
+  float4 f;
+  uint4 k;
 };
 
-// last index in [lo, lo + cnt) whose begin (low 31 bits of b[]) is <= j; b is sorted
-__device__ __forceinline__ int child_search(const int* b, int lo, int cnt, int j) {
-  const int end = lo + cnt;
+extern __shared__ int sh_i[];
+// last index k in [lo, lo + cnt) whose begin (low 31 bits of sh_i[ob + k]) is <= j
+__device__ __forceinline__ int child_search(int ob, int lo, int cnt, int j) {
+  const int last = lo + cnt - 1;
   for (int step = cnt > 1 ? 1 << (31 - __clz(cnt - 1)) : 0; step > 0; step >>= 1) {
-    const int t = lo + step;
-    if (t < end && (b[t] & 0x7fffffff) <= j) lo = t;
+    const int t = min(lo + step, last);  // branch-free: probe a clamped index
+    lo = (sh_i[ob + t] & 0x7fffffff) <= j ? t : lo;
   }
   return lo;
 }
@@ -127,44 +122,59 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
                unsigned char* __restrict__ queues, float* __restrict__ out,
                int64_t* __restrict__ visited, int64_t* __restrict__ path_steps,
                int64_t* __restrict__ path_count) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  // Dynamic shared memory, addressed by element index off the extern arrays
+  // (all alias the same window), so every access is LDS [index + imm] with no
+  // generic-pointer reconstruction.  Layout in 16-byte units:
+  //   [0, kBlock)          s_q    float4  query coordinates of this tile
+  //   [o_cm1, +n1)         s_cm1  float4  level-1 {com, m0}
+  //   [o_tp1, +n1)         s_tp1  int4    level-1 topology
+  //   [o_cm2, +n2)         s_cm2  float4  level-2 {com, m0}
+  //   then float2 s_w1[n1], s_w2[n2] (winding) and int s_b2[n2], s_seen, s_steps, s_count
+  extern __shared__ float4 sh_f4[];
+  extern __shared__ int4 sh_i4[];
+  extern __shared__ float2 sh_f2[];
+  extern __shared__ int sh_i[];
   const int n1 = V.n1, n2 = V.n2;
-  float4* s_q = reinterpret_cast<float4*>(smem);
-  int* s_seen = reinterpret_cast<int*>(s_q + kBlock);  // nodes read below level 1, per query
-  int* s_steps = s_seen + kBlock;                        // descents below level 1, per query
-  int* s_count = s_steps + kBlock;                       // queue lengths
-  float4* s_cm1 = reinterpret_cast<float4*>(s_count + 4);
-  int4* s_tp1 = reinterpret_cast<int4*>(s_cm1 + n1);
-  float4* s_cm2 = reinterpret_cast<float4*>(s_tp1 + n1);
-  float2* s_w1 = reinterpret_cast<float2*>(s_cm2 + n2);
-  float2* s_w2 = s_w1 + (KID == KID_WINDING ? n1 : 0);
-  int* s_b2 = reinterpret_cast<int*>(s_w2 + (KID == KID_WINDING ? n2 : 0));
+  const int o_cm1 = kBlock, o_tp1 = o_cm1 + n1, o_cm2 = o_tp1 + n1;
+  const int o_w1 = 2 * (o_cm2 + n2), o_w2 = o_w1 + (KID == KID_WINDING ? n1 : 0);
+  const int o_b2 = 2 * (o_w2 + (KID == KID_WINDING ? n2 : 0));
+  const int o_seen = o_b2 + n2, o_steps = o_seen + kBlock, o_count = o_steps + kBlock;
+#define s_q(i) sh_f4[(i)]
+#define s_cm1(i) sh_f4[o_cm1 + (i)]
+#define s_tp1(i) sh_i4[o_tp1 + (i)]
+#define s_cm2(i) sh_f4[o_cm2 + (i)]
+#define s_w1(i) sh_f2[o_w1 + (i)]
+#define s_w2(i) sh_f2[o_w2 + (i)]
+#define s_b2(i) sh_i[o_b2 + (i)]
+#define s_seen(i) sh_i[o_seen + (i)]
+#define s_steps(i) sh_i[o_steps + (i)]
+#define s_count(i) sh_i[o_count + (i)]
 
   unsigned char* const qbase = queues + (size_t)blockIdx.x * 2 * kQueueBytes;
 
   // ---- stage level 1 (root's children, level order 1..n1) and level 2
   for (int i = threadIdx.x; i < n1; i += blockDim.x) {
-    s_cm1[i] = V.cm[1 + i];
-    s_tp1[i] = V.topo[1 + i];
-    if (KID == KID_WINDING) s_w1[i] = V.m12[1 + i];
+    s_cm1(i) = V.cm[1 + i];
+    s_tp1(i) = V.topo[1 + i];
+    if (KID == KID_WINDING) s_w1(i) = V.m12[1 + i];
   }
   const bool l2_multi = V.first_multi <= 2;
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    s_cm2[i] = V.cm[V.base2 + i];
-    if (KID == KID_WINDING) s_w2[i] = V.m12[V.base2 + i];
+    s_cm2(i) = V.cm[V.base2 + i];
+    if (KID == KID_WINDING) s_w2(i) = V.m12[V.base2 + i];
     int b = V.lb[V.base2 + i];
     if (l2_multi) {
       int4 tp = V.topo[V.base2 + i];
       if (tp.y == 0 && tp.w - tp.z > 1) b |= 0x80000000;
     }
-    s_b2[i] = b;
+    s_b2(i) = b;
   }
   if (threadIdx.x == 0) {
-    s_count[0] = 0;
-    s_count[1] = 0;
+    s_count(0) = 0;
+    s_count(1) = 0;
   }
-  s_seen[threadIdx.x] = 0;
-  s_steps[threadIdx.x] = 0;
+  s_seen(threadIdx.x) = 0;
+  s_steps(threadIdx.x) = 0;
   __syncthreads();
 
   const int tid = threadIdx.x;
@@ -179,21 +189,22 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   // store their residual in the owner's creation-ordered slot.
   auto drain = [&]() {
     int src = 0;  // the level-1 step always produces into queue 0
-    int cnt = s_count[0];
+    int cnt = s_count(0);
     while (cnt > 0) {
-      const QueueRef in{qbase + (size_t)src * kQueueBytes};
-      const QueueRef outq{qbase + (size_t)(src ^ 1) * kQueueBytes};
+      Walk* in = reinterpret_cast<Walk*>(qbase + (size_t)src * kQueueBytes);
+      Walk* outq = reinterpret_cast<Walk*>(qbase + (size_t)(src ^ 1) * kQueueBytes);
       for (int i = tid; i < cnt; i += kBlock) {
-        const int meta = in.i32(QF_META)[i];
+        const int4 wa = in[i].a;
+        const int meta = wa.x;
         const int owner = meta & 0xff, lvl = (meta >> 8) & 0xff, a_ord = meta >> 16;
-        const int node = in.i32(QF_NODE)[i], jj = in.i32(QF_J)[i];
-        const int seq = in.i32(QF_SEQ)[i];
-        float resid = in.f32(QF_RESID)[i];
-        const float4 qq = s_q[owner];
+        const int seq = wa.y, node = wa.z, jj = wa.w;
+        const float4 wf = in[i].f;
+        float resid = wf.w;
+        const float4 qq = s_q(owner);
         const int4 tp = V.topo[node];
         bool cont = false;
         if (tp.y > 0) {
-          const float prr = in.f32(QF_PRR)[i], rp = in.f32(QF_RP)[i], cvn = in.f32(QF_CVN)[i];
+          const float prr = wf.x, rp = wf.y, cvn = wf.z;
           const bool cmulti = lvl + 1 >= V.first_multi;
           float ks0 = 0.f, ks1 = 0.f;
           int le = 0;  // children whose begin <= j: the last of them holds j
@@ -229,43 +240,37 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
           const float ks = ks0 + ks1;
           const int cidx = tp.x + le - 1;
           const float4 cch = V.cm[cidx];  // L1 hit: just streamed
-          atomicAdd(&s_seen[owner], tp.y + 1);
-          const int4 tpa = s_tp1[a_ord];
+          atomicAdd(&s_seen(owner), tp.y + 1);
+          const int4 tpa = s_tp1(a_ord);
           const float pagg = (float)(tp.w - tp.z) / (float)(tpa.w - tpa.z);
           resid += (ks - cvn) * rcp_ftz(pagg * prr);
           const float rc =
               fdist(cch, qq.x, qq.y, qq.z) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
           const float p = rr_fast(rp, rc, rr_mode);
-          const uint2 k2 = in.key()[i];
+          const uint4 k2 = in[i].k;
           const uint64_t kr = ((uint64_t)k2.y << 32) | k2.x;
           if (draw24(kr, (uint64_t)(lvl - 1)) < p) {  // roulette counter = levels descended
             cont = true;
-            atomicAdd(&s_steps[owner], 1);
+            atomicAdd(&s_steps(owner), 1);
             const float2 wc = KID == KID_WINDING ? V.m12[cidx] : w0;
-            const int pos = atomicAdd(&s_count[src ^ 1], 1);
-            outq.i32(QF_META)[pos] = owner | ((lvl + 1) << 8) | (a_ord << 16);
-            outq.i32(QF_SEQ)[pos] = seq;
-            outq.i32(QF_NODE)[pos] = cidx;
-            outq.i32(QF_J)[pos] = jj;
-            outq.f32(QF_PRR)[pos] = prr * p;
-            outq.f32(QF_RP)[pos] = rc;
-            outq.f32(QF_CVN)[pos] = fterm<KID>(cch, wc, qq.x, qq.y, qq.z, kp);
-            outq.f32(QF_RESID)[pos] = resid;
-            outq.key()[pos] = k2;
+            const int pos = atomicAdd(&s_count(src ^ 1), 1);
+            outq[pos].a = make_int4(owner | ((lvl + 1) << 8) | (a_ord << 16), seq, cidx, jj);
+            outq[pos].f = make_float4(prr * p, rc, fterm<KID>(cch, wc, qq.x, qq.y, qq.z, kp), resid);
+            outq[pos].k = k2;
           }
         }
         if (!cont) my_res[(int64_t)owner * res_stride + seq] = resid;
       }
       __syncthreads();
-      cnt = s_count[src ^ 1];
+      cnt = s_count(src ^ 1);
       __syncthreads();
-      if (tid == 0) s_count[src] = 0;
+      if (tid == 0) s_count(src) = 0;
       src ^= 1;
       __syncthreads();
     }
   };
 
-  const QueueRef q0{qbase};
+  Walk* const q0 = reinterpret_cast<Walk*>(qbase);
   for (int64_t base = (int64_t)blockIdx.x * kBlock; base < n; base += (int64_t)gridDim.x * kBlock) {
     const int64_t t = base + tid;
     const bool live = t < n;
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
       qy = (float)q[3 * qi + 1];
       qz = (float)q[3 * qi + 2];
     }
-    s_q[tid] = make_float4(qx, qy, qz, 0.f);
+    s_q(tid) = make_float4(qx, qy, qz, 0.f);
     const uint64_t hq = key_fold(hseed, (uint64_t)(qi + qoff));
     double acc = 0.0;  // control variates + level-1 residuals, (a, s) order
     int seen = 0, steps = 0, paths = 0;
@@ -285,9 +290,9 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 
     for (int a_ord = 0; a_ord < n1; ++a_ord) {  // block-uniform
       ++seen;
-      const int4 tpa = s_tp1[a_ord];
-      const float4 ca = s_cm1[a_ord];
-      const float2 wa = KID == KID_WINDING ? s_w1[a_ord] : w0;
+      const int4 tpa = s_tp1(a_ord);
+      const float4 ca = s_cm1(a_ord);
+      const float2 wa = KID == KID_WINDING ? s_w1(a_ord) : w0;
       if (tpa.y == 0) {  // leaf subdomain: exact term, never sampled
         float v = (tpa.w - tpa.z > 1) ? leaf_exact<KID>(V, tpa.z, tpa.w, qx, qy, qz, kp)
                                       : fterm<KID>(ca, wa, qx, qy, qz, kp);
@@ -301,20 +306,20 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
       if (!l2_multi) {
         int k = k0;
         for (; k + 3 < kend; k += 4) {
-          ks0 += fterm<KID>(s_cm2[k], KID == KID_WINDING ? s_w2[k] : w0, qx, qy, qz, kp);
-          ks1 += fterm<KID>(s_cm2[k + 1], KID == KID_WINDING ? s_w2[k + 1] : w0, qx, qy, qz, kp);
-          ks2 += fterm<KID>(s_cm2[k + 2], KID == KID_WINDING ? s_w2[k + 2] : w0, qx, qy, qz, kp);
-          ks3 += fterm<KID>(s_cm2[k + 3], KID == KID_WINDING ? s_w2[k + 3] : w0, qx, qy, qz, kp);
+          ks0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
+          ks1 += fterm<KID>(s_cm2(k + 1), KID == KID_WINDING ? s_w2(k + 1) : w0, qx, qy, qz, kp);
+          ks2 += fterm<KID>(s_cm2(k + 2), KID == KID_WINDING ? s_w2(k + 2) : w0, qx, qy, qz, kp);
+          ks3 += fterm<KID>(s_cm2(k + 3), KID == KID_WINDING ? s_w2(k + 3) : w0, qx, qy, qz, kp);
         }
         for (; k < kend; ++k)
-          ks0 += fterm<KID>(s_cm2[k], KID == KID_WINDING ? s_w2[k] : w0, qx, qy, qz, kp);
+          ks0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
       } else {
         for (int k = k0; k < kend; ++k) {
-          if (s_b2[k] < 0) {
+          if (s_b2(k) < 0) {
             int4 tp = V.topo[V.base2 + k];
             ks0 += leaf_exact<KID>(V, tp.z, tp.w, qx, qy, qz, kp);
           } else {
-            ks0 += fterm<KID>(s_cm2[k], KID == KID_WINDING ? s_w2[k] : w0, qx, qy, qz, kp);
+            ks0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
           }
         }
       }
@@ -331,31 +336,25 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
         int j = tpa.z + (int)__dmul_rn(u0, (double)count_a);
         if (j >= tpa.w) j = tpa.w - 1;
         // level-1 step from shared memory: the swap at `a` is the hoisted delta_a
-        const int lo = child_search(s_b2, k0, cc, j);
+        const int lo = child_search(o_b2, k0, cc, j);
         seen += cc + 1;
-        const float4 c2 = s_cm2[lo];
+        const float4 c2 = s_cm2(lo);
         const float rc = fdist(c2, qx, qy, qz) * id2;
         const float p = rr_fast(rp_a, rc, rr_mode);
         if (live && draw24(kr, 0) < p) {  // descends: queue the deeper steps
           ++steps;
-          const int pos = atomicAdd(&s_count[0], 1);
-          q0.i32(QF_META)[pos] = tid | (2 << 8) | (a_ord << 16);
-          q0.i32(QF_SEQ)[pos] = nseq++;
-          q0.i32(QF_NODE)[pos] = V.base2 + lo;
-          q0.i32(QF_J)[pos] = j;
-          q0.f32(QF_PRR)[pos] = p;
-          q0.f32(QF_RP)[pos] = rc;
-          q0.f32(QF_CVN)[pos] =
-              fterm<KID>(c2, KID == KID_WINDING ? s_w2[lo] : w0, qx, qy, qz, kp);
-          q0.f32(QF_RESID)[pos] = 0.f;
-          q0.key()[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
+          const int pos = atomicAdd(&s_count(0), 1);
+          q0[pos].a = make_int4(tid | (2 << 8) | (a_ord << 16), nseq++, V.base2 + lo, j);
+          q0[pos].f = make_float4(
+              p, rc, fterm<KID>(c2, KID == KID_WINDING ? s_w2(lo) : w0, qx, qy, qz, kp), 0.f);
+          q0[pos].k = make_uint4((uint32_t)kr, (uint32_t)(kr >> 32), 0u, 0u);
         }
         // an iteration queues at most kBlock walks: track a block-uniform upper
         // bound of the queue length and look at the real length only near capacity
         qbound += kBlock;
         if (qbound + kBlock > kQcap) {
           __syncthreads();
-          qbound = s_count[0];
+          qbound = s_count(0);
           __syncthreads();
           if (qbound + kBlock > kQcap) {
             drain();
@@ -371,10 +370,10 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     // owners fold their deeper residuals in creation order (query-intrinsic)
     double acc_deep = 0.0;
     for (int k2 = 0; k2 < nseq; ++k2) acc_deep += (double)my_res[(int64_t)tid * res_stride + k2];
-    seen += s_seen[tid];
-    steps += s_steps[tid];
-    s_seen[tid] = 0;
-    s_steps[tid] = 0;
+    seen += s_seen(tid);
+    steps += s_steps(tid);
+    s_seen(tid) = 0;
+    s_steps(tid) = 0;
     const double total = acc + acc_deep / (double)S;
     if (live) {
       out[qi] = (float)total;
@@ -384,6 +383,16 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     }
     __syncthreads();
   }
+#undef s_q
+#undef s_cm1
+#undef s_tp1
+#undef s_cm2
+#undef s_w1
+#undef s_w2
+#undef s_b2
+#undef s_seen
+#undef s_steps
+#undef s_count
 }
 
 // returns 1 if the fast path does not apply (caller falls back), 0 on launch
@@ -413,9 +422,9 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   }
   bool wind = kid == KID_WINDING;
   if ((int64_t)V.n1 * n_samples > (1 << 20)) return 0;
-  size_t smem = kBlock * (sizeof(float4) + 2 * sizeof(int)) + 16 +
-                (size_t)V.n1 * (sizeof(float4) + sizeof(int4)) + (size_t)V.n2 * sizeof(float4) +
-                (wind ? (size_t)(V.n1 + V.n2) * sizeof(float2) : 0) + (size_t)V.n2 * sizeof(int);
+  const size_t n1 = (size_t)V.n1, n2 = (size_t)V.n2;
+  size_t smem = 16 * ((size_t)kBlock + 2 * n1 + n2) + (wind ? 8 * (n1 + n2) : 0) +
+                4 * (n2 + 2 * (size_t)kBlock + 4);
   if (smem > 200 * 1024) return 0;
   KParams kp;
   kp.alpha = alpha;
