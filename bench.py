@@ -65,56 +65,98 @@ def config_block():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle-reason sampling DURING the timed region.
+
+    NVML is polled from a thread every ~1 ms (the timed region of a default run
+    is only tens of ms, too short for ``nvidia-smi -lms``); ``nvidia-smi`` runs
+    beside it as the recipe's clocks line and is used when NVML is missing.
+    """
+
+    REASONS = (("hw_slowdown", 0x8), ("sw_power_cap", 0x4), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
+        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.sm_max = None
+        self.smi_lines = []
+        self._stop = threading.Event()
+        self._thread = None
+        self._proc = None
+        self.active = False  # set only while the timed region runs
+
+    def _poll(self, nv, h):
+        while not self._stop.is_set():
+            if not self.active:
+                time.sleep(0.0002)
+                continue
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:  # pragma: no cover
+                break
+            time.sleep(0.001)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.sm_max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self._thread.start()
+        except Exception:
+            self._thread = None
+        try:
+            self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
-                 "utilization.gpu", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
-            self.proc = None
-        time.sleep(0.3)
+            self._proc = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join(timeout=2)
+        if self._proc is not None:
+            self._proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                out, _ = self._proc.communicate(timeout=5)
             except subprocess.TimeoutExpired:
-                self.proc.kill()
+                self._proc.kill()
                 out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            self.smi_lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
-        sm, mx, reasons, util = [], 0, set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            try:
-                s, m = float(parts[0]), float(parts[1])
-                u = float(parts[7])
-            except (ValueError, IndexError):
-                continue
-            mx = max(mx, m)
-            util.append(u)
-            if u > 0:
-                sm.append(s)
-            for nm, val in zip(names, parts[3:7]):
-                if val.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(getattr(self, "lines", []))}
+        sm, mask = [], 0
+        if self.samples:
+            sm = [float(s) for s, _ in self.samples]
+            for _, r in self.samples:
+                mask |= int(r)
+            reasons = sorted(nm for nm, bit in self.REASONS if mask & bit)
+            src = "nvml (1 ms poll during the timed region)"
+            mx = float(self.sm_max) if self.sm_max else None
+        else:
+            reasons, mx = set(), None
+            for ln in self.smi_lines:
+                parts = [p.strip() for p in ln.split(",")]
+                try:
+                    sm.append(float(parts[0]))
+                    mx = max(mx or 0.0, float(parts[1]))
+                except (ValueError, IndexError):
+                    continue
+                for (nm, _), val in zip(self.REASONS, parts[2:6]):
+                    if val.lower() == "active":
+                        reasons.add(nm)
+            reasons = sorted(reasons)
+            src = "nvidia-smi -lms 50"
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "sm_mhz_min": float(min(sm)) if sm else None, "reasons": reasons,
+                "samples": len(sm), "source": src}
 
 
 def median_rel(est, ref):
@@ -215,10 +257,15 @@ def run_ours(args):
         barrier()
         ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev_a.record()
+        switch = sys.getswitchinterval()
+        sys.setswitchinterval(2e-4)  # let the clock poller run between launches
+        clk.active = True
         for _ in range(args.steps):
             res = step()
         ev_b.record()
         barrier()
+        clk.active = False
+        sys.setswitchinterval(switch)
     step_ms = ev_a.elapsed_time(ev_b) / args.steps
     if world > 1:
         tt = torch.tensor([step_ms], device="cuda")

@@ -4,26 +4,27 @@
 // the swap at each reached node is committed before the roulette that gates
 // descent), same splitmix64 streams and index draws, reorganised for B200:
 //
-//  * The control-variate part is dense and query-independent in its node set:
-//    every query evaluates the N1 level-1 aggregates and the N2 level-2
-//    children of internal level-1 nodes.  A persistent block stages those
-//    records in shared memory once ({com, m0} = 16 B per node, + {m1, m2} for
-//    winding) and every thread streams them with broadcast LDS: an
-//    FP32 + MUFU.RSQ loop, the N x (N1+N2) "brute force over staged nodes".
-//  * The first path step (from the subdomain to a level-2 child) is resolved
-//    from shared memory: binary search of the sampled point index over the
-//    children's begins, far-field ratios from per-level cell diameters (cells
-//    are uniform splits, so one diameter per level, octree.py:225).
-//  * Deeper steps (only ~1/3 of samples descend below level 1, and fewer
-//    further) would leave most lanes idle if walked in place.  Instead each
-//    descending sample is pushed onto a block-wide shared-memory queue and the
-//    block serves the queue in rounds: every thread takes one walk and
-//    advances it by exactly one level (sum the node's contiguous children,
-//    pick the child holding the sampled point, roulette), pushing it back if it
-//    continues.  Finished walks store their residual in the owner's creation-
-//    ordered slot, and owners fold their slots in that order, so a query's
-//    result does not depend on which thread served its walks or when.
-//  * FP32 terms and residuals, FP64 accumulation across subdomains.
+//  * Dense part.  Per subdomain a (root child) the reference adds cv(a) and
+//    every sample of a commits the level-1 swap delta_a = sum(children) - cv(a)
+//    with weight 1/(p_agg * p_rr) = 1 (_core.py:196-200, hoisted at 246-250),
+//    so cv(a) cancels and the query-independent dense part is the sum of all
+//    N2 level-2 records (children of internal level-1 nodes, contiguous in
+//    level order) plus exact terms of leaf subdomains.  A persistent block
+//    stages the level-1/2 records in shared memory once ({com, m0} = 16 B per
+//    node, + {m1, m2} for winding) and every thread streams them with
+//    broadcast LDS: an FP32 + MUFU.RSQ loop, "brute force over staged nodes".
+//  * Sampling.  Per (a, s): the splitmix64 index draw, the level-1 step from
+//    shared memory (binary search of the sampled point index over the
+//    children's begins, far-field ratios from per-level cell diameters: cells
+//    are uniform splits, octree.py:225), the roulette.
+//  * Deeper steps (~1/3 of samples descend below level 2) would leave most
+//    lanes idle if walked in place.  Descending samples are queued (24 B walk
+//    starts per block in global memory, L2-resident) and served after the
+//    sampling loop by lanes that refill independently from the queue and
+//    carry each walk to completion.  A finished walk stores its residual in
+//    its (a, s) slot and owners fold their slots in (a, s) order, so a query's
+//    value never depends on which lane served its walks or when.
+//  * FP32 terms and residuals, FP64 accumulation across chunks/subdomains.
 #include <algorithm>
 
 #include "fs_common.cuh"
@@ -42,6 +43,8 @@ struct FastView {
   const float4* __restrict__ pa;   // permuted points {x, y, z, m0}
   const float4* __restrict__ pb;   // {m1, m2, 0, 0}
   int n1, base2, n2, first_multi;
+  int per_chunk;                   // (a, s) samples per thread between drains
+  int qcap;                        // queued walk starts per block
   float inv_diam[kFastMaxLevels];  // 1 / max(diam_level, 1e-12)
 };
 
@@ -89,21 +92,23 @@ constexpr int kBlock = 256;  // threads (= queries) per tile
 #ifndef FSB_STO_MINB
 #define FSB_STO_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
+#ifndef FSB_QCAP_MAX
+#define FSB_QCAP_MAX 9216  // max queued walk starts per block (one drain per tile on C4)
+#endif
 
-// Walks below level 1, held per block in global memory (array of 48-byte
-// records, L2-resident); two queues ping-pong between service rounds.
-// Record: int4 {meta = owner | lvl << 8 | a_ord << 16, seq, node, j},
-//         float4 {prr, rp, cvn, resid}, uint4 {kr.lo, kr.hi, -, -}.
-constexpr int kQcap = 4096 + 2 * kBlock;
-constexpr size_t kQueueBytes = (size_t)kQcap * 48;  // one queue
+// Walk starts, per block, SoA: int4 {owner | s << 8, a_ord, k (level-2 index), j}
+// and uint2 {kr.lo, kr.hi} (roulette stream key).  Everything else a walk needs
+// at level 2 (p_rr, ratio, control-variate term) is recomputed from the staged
+// level-1/2 records in shared memory.
+constexpr size_t kWalkBytes = 24;
 
-struct Walk {
-  int4 a;
-  float4 f;
-  uint4 k;
-};
-
+extern __shared__ float4 sh_f4[];
+extern __shared__ int4 sh_i4[];
+extern __shared__ float2 sh_f2[];
 extern __shared__ int sh_i[];
+extern __shared__ uint2 sh_u2[];
+extern __shared__ unsigned short sh_u16[];
+
 // last index k in [lo, lo + cnt) whose begin (low 31 bits of sh_i[ob + k]) is <= j
 __device__ __forceinline__ int child_search(int ob, int lo, int cnt, int j) {
   const int last = lo + cnt - 1;
@@ -114,52 +119,79 @@ __device__ __forceinline__ int child_search(int ob, int lo, int cnt, int j) {
   return lo;
 }
 
-template <int KID>
+template <int RR>
+__device__ __forceinline__ float rr_fast_t(float rp, float rc) {
+  if (RR == 1) return 0.5f;
+  if (RR == 2) return 1.0f;
+  return fminf(fmaxf(rp, 1.0f) * rcp_ftz(fmaxf(rc, 1e-12f)), 1.0f);
+}
+
+// roulette: u < p with u the 24-bit draw; p == 1 needs no draw (u < 1 always)
+template <int RR>
+__device__ __forceinline__ bool survive(float p, uint64_t kr, uint64_t ctr) {
+  if (RR == 2) return true;
+  return p >= 1.0f || draw24(kr, ctr) < p;
+}
+
+#ifndef FSB_LUT_BITS
+#define FSB_LUT_BITS 5
+#endif
+// index-draw buckets per subdomain (top FSB_LUT_BITS bits of the draw)
+constexpr int kLutBits = FSB_LUT_BITS, kLut = 1 << kLutBits;
+
+template <int KID, int RR>
 __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
-    k_sto_fast(FastView V, const double* __restrict__ q, int64_t n,
-               const int32_t* __restrict__ qperm, int S, int rr_mode, uint64_t seed, int64_t qoff,
-               KParams kp, float* __restrict__ res_g, int res_stride,
-               unsigned char* __restrict__ queues, float* __restrict__ out,
-               int64_t* __restrict__ visited, int64_t* __restrict__ path_steps,
-               int64_t* __restrict__ path_count) {
+    k_sto_fast(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
+               const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff,
+               KParams kp, float* __restrict__ res_g, unsigned char* __restrict__ queues,
+               float* __restrict__ out, int64_t* __restrict__ visited,
+               int64_t* __restrict__ path_steps, int64_t* __restrict__ path_count) {
   // Dynamic shared memory, addressed by element index off the extern arrays
   // (all alias the same window), so every access is LDS [index + imm] with no
-  // generic-pointer reconstruction.  Layout in 16-byte units:
-  //   [0, kBlock)          s_q    float4  query coordinates of this tile
-  //   [o_cm1, +n1)         s_cm1  float4  level-1 {com, m0}
-  //   [o_tp1, +n1)         s_tp1  int4    level-1 topology
-  //   [o_cm2, +n2)         s_cm2  float4  level-2 {com, m0}
-  //   then float2 s_w1[n1], s_w2[n2] (winding) and int s_b2[n2], s_seen, s_steps, s_count
-  extern __shared__ float4 sh_f4[];
-  extern __shared__ int4 sh_i4[];
-  extern __shared__ float2 sh_f2[];
-  extern __shared__ int sh_i[];
+  // generic-pointer reconstruction.  Layout:
+  //   16 B: s_q[kBlock] query coords, s_cm1[n1] {com, m0}, s_tp1[n1] topology,
+  //         s_cm2[n2] {com, m0}
+  //    8 B: s_w1[n1], s_w2[n2] {m1, m2} (winding), s_hq[kBlock] per-query RNG prefix
+  //    4 B: s_b2[n2] begins (bit 31: multi-point leaf), s_seen, s_steps, s_count[4]
+  //    2 B: s_lut[n1][kLut + 1] first candidate child per index-draw bucket
   const int n1 = V.n1, n2 = V.n2;
   const int o_cm1 = kBlock, o_tp1 = o_cm1 + n1, o_cm2 = o_tp1 + n1;
   const int o_w1 = 2 * (o_cm2 + n2), o_w2 = o_w1 + (KID == KID_WINDING ? n1 : 0);
-  const int o_b2 = 2 * (o_w2 + (KID == KID_WINDING ? n2 : 0));
+  const int o_hq = o_w2 + (KID == KID_WINDING ? n2 : 0);
+  const int o_b2 = 2 * (o_hq + kBlock);
   const int o_seen = o_b2 + n2, o_steps = o_seen + kBlock, o_count = o_steps + kBlock;
+  const int o_lut = 2 * (o_count + 4);
 #define s_q(i) sh_f4[(i)]
 #define s_cm1(i) sh_f4[o_cm1 + (i)]
 #define s_tp1(i) sh_i4[o_tp1 + (i)]
 #define s_cm2(i) sh_f4[o_cm2 + (i)]
 #define s_w1(i) sh_f2[o_w1 + (i)]
 #define s_w2(i) sh_f2[o_w2 + (i)]
+#define s_hq(i) sh_u2[o_hq + (i)]
 #define s_b2(i) sh_i[o_b2 + (i)]
 #define s_seen(i) sh_i[o_seen + (i)]
 #define s_steps(i) sh_i[o_steps + (i)]
 #define s_count(i) sh_i[o_count + (i)]
+#define s_lut(i) sh_u16[o_lut + (i)]
 
-  unsigned char* const qbase = queues + (size_t)blockIdx.x * 2 * kQueueBytes;
+  int4* const qa = reinterpret_cast<int4*>(queues + (size_t)blockIdx.x * V.qcap * kWalkBytes);
+  uint2* const qk = reinterpret_cast<uint2*>(qa + V.qcap);
+  const int tid = threadIdx.x;
+  const int nslot = n1 * S;
+  // result slots of this block, slot-major: res[(a_ord * S + s) * kBlock + owner].
+  // Every tile writes each internal subdomain's slots (zero, or the walk's
+  // residual); slots of leaf subdomains stay at the zero stored here.
+  float* const my_res = res_g + (int64_t)blockIdx.x * kBlock * nslot;
+  for (int i = tid; i < nslot * kBlock; i += kBlock) my_res[i] = 0.f;
 
   // ---- stage level 1 (root's children, level order 1..n1) and level 2
-  for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+  for (int i = tid; i < n1; i += kBlock) {
     s_cm1(i) = V.cm[1 + i];
     s_tp1(i) = V.topo[1 + i];
     if (KID == KID_WINDING) s_w1(i) = V.m12[1 + i];
   }
   const bool l2_multi = V.first_multi <= 2;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+  for (int i = tid; i < n2; i += kBlock) {
     s_cm2(i) = V.cm[V.base2 + i];
     if (KID == KID_WINDING) s_w2(i) = V.m12[V.base2 + i];
     int b = V.lb[V.base2 + i];
@@ -169,217 +201,278 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     }
     s_b2(i) = b;
   }
-  if (threadIdx.x == 0) {
-    s_count(0) = 0;
-    s_count(1) = 0;
+  if (tid < 4) s_count(tid) = 0;  // [0] queue length, [1] drain head
+  s_seen(tid) = 0;
+  s_steps(tid) = 0;
+  __syncthreads();
+  // bucket table: j in bucket b (j - begin in [floor(b c / L), floor((b+1) c / L)],
+  // c = count) lies in a child in [lut[b], lut[b+1]] (children are ordered by begin)
+  for (int i = tid; i < n1 * (kLut + 1); i += kBlock) {
+    const int a = i / (kLut + 1), b = i - a * (kLut + 1);
+    const int4 tpa = s_tp1(a);
+    int c = 0;
+    if (tpa.y > 0) {
+      int jb = tpa.z + (int)(((int64_t)b * (tpa.w - tpa.z)) >> kLutBits);
+      if (jb > tpa.w - 1) jb = tpa.w - 1;
+      const int k0 = tpa.x - V.base2;
+      c = child_search(o_b2, k0, tpa.y, jb) - k0;
+    }
+    s_lut(i) = (unsigned short)c;
   }
-  s_seen(threadIdx.x) = 0;
-  s_steps(threadIdx.x) = 0;
+  // query-independent counters: every sample of an internal subdomain a visits
+  // a's children and the picked child (_core.py:195, 205); paths = samples
+  int seen_base = n1, n_int = 0;
+  for (int a = 0; a < n1; ++a) {
+    const int4 tpa = s_tp1(a);
+    if (tpa.y > 0) {
+      seen_base += S * (tpa.y + 1);
+      ++n_int;
+    }
+  }
   __syncthreads();
 
-  const int tid = threadIdx.x;
   const uint64_t hseed = mix64(seed + kGamma);
   const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
   const float2 w0 = make_float2(0.f, 0.f);
-  float* my_res = res_g + ((int64_t)blockIdx.x * kBlock) * res_stride;
 
-  // Serve all queued walks: each service round advances every queued walk by
-  // one level (sum the node's contiguous children, pick the child holding the
-  // sampled point, roulette); survivors go to the other queue, finished walks
-  // store their residual in the owner's creation-ordered slot.
-  auto drain = [&]() {
-    int src = 0;  // the level-1 step always produces into queue 0
-    int cnt = s_count(0);
-    while (cnt > 0) {
-      Walk* in = reinterpret_cast<Walk*>(qbase + (size_t)src * kQueueBytes);
-      Walk* outq = reinterpret_cast<Walk*>(qbase + (size_t)(src ^ 1) * kQueueBytes);
-      for (int i = tid; i < cnt; i += kBlock) {
-        const int4 wa = in[i].a;
-        const int meta = wa.x;
-        const int owner = meta & 0xff, lvl = (meta >> 8) & 0xff, a_ord = meta >> 16;
-        const int seq = wa.y, node = wa.z, jj = wa.w;
-        const float4 wf = in[i].f;
-        float resid = wf.w;
-        const float4 qq = s_q(owner);
-        const int4 tp = V.topo[node];
-        bool cont = false;
-        if (tp.y > 0) {
-          const float prr = wf.x, rp = wf.y, cvn = wf.z;
-          const bool cmulti = lvl + 1 >= V.first_multi;
-          float ks0 = 0.f, ks1 = 0.f;
-          int le = 0;  // children whose begin <= j: the last of them holds j
-          int c = 0;
-          if (!cmulti) {
-            for (; c + 1 < tp.y; c += 2) {
-              const int r = tp.x + c;
-              const float4 c0 = V.cm[r], c1 = V.cm[r + 1];
-              const int b0 = V.lb[r], b1 = V.lb[r + 1];
-              const float2 u0 = KID == KID_WINDING ? V.m12[r] : w0;
-              const float2 u1 = KID == KID_WINDING ? V.m12[r + 1] : w0;
-              ks0 += fterm<KID>(c0, u0, qq.x, qq.y, qq.z, kp);
-              ks1 += fterm<KID>(c1, u1, qq.x, qq.y, qq.z, kp);
-              le += (b0 <= jj) + (b1 <= jj);
-            }
-          }
-          for (; c < tp.y; ++c) {
-            const int r = tp.x + c;
-            const float4 cr = V.cm[r];
-            const float2 wr = KID == KID_WINDING ? V.m12[r] : w0;
-            float v;
-            if (cmulti) {
-              int4 tc = V.topo[r];
-              v = (tc.y == 0 && tc.w - tc.z > 1)
-                      ? leaf_exact<KID>(V, tc.z, tc.w, qq.x, qq.y, qq.z, kp)
-                      : fterm<KID>(cr, wr, qq.x, qq.y, qq.z, kp);
-            } else {
-              v = fterm<KID>(cr, wr, qq.x, qq.y, qq.z, kp);
-            }
-            ks0 += v;
-            le += V.lb[r] <= jj;
-          }
-          const float ks = ks0 + ks1;
-          const int cidx = tp.x + le - 1;
-          const float4 cch = V.cm[cidx];  // L1 hit: just streamed
-          atomicAdd(&s_seen(owner), tp.y + 1);
-          const int4 tpa = s_tp1(a_ord);
-          const float pagg = (float)(tp.w - tp.z) / (float)(tpa.w - tpa.z);
-          resid += (ks - cvn) * rcp_ftz(pagg * prr);
-          const float rc =
-              fdist(cch, qq.x, qq.y, qq.z) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
-          const float p = rr_fast(rp, rc, rr_mode);
-          const uint4 k2 = in[i].k;
-          const uint64_t kr = ((uint64_t)k2.y << 32) | k2.x;
-          if (draw24(kr, (uint64_t)(lvl - 1)) < p) {  // roulette counter = levels descended
-            cont = true;
-            atomicAdd(&s_steps(owner), 1);
-            const float2 wc = KID == KID_WINDING ? V.m12[cidx] : w0;
-            const int pos = atomicAdd(&s_count(src ^ 1), 1);
-            outq[pos].a = make_int4(owner | ((lvl + 1) << 8) | (a_ord << 16), seq, cidx, jj);
-            outq[pos].f = make_float4(prr * p, rc, fterm<KID>(cch, wc, qq.x, qq.y, qq.z, kp), resid);
-            outq[pos].k = k2;
-          }
-        }
-        if (!cont) my_res[(int64_t)owner * res_stride + seq] = resid;
-      }
-      __syncthreads();
-      cnt = s_count(src ^ 1);
-      __syncthreads();
-      if (tid == 0) s_count(src) = 0;
-      src ^= 1;
-      __syncthreads();
-    }
-  };
-
-  Walk* const q0 = reinterpret_cast<Walk*>(qbase);
   for (int64_t base = (int64_t)blockIdx.x * kBlock; base < n; base += (int64_t)gridDim.x * kBlock) {
-    const int64_t t = base + tid;
-    const bool live = t < n;
-    const int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
-    float qx = 0.f, qy = 0.f, qz = 0.f;
-    if (live) {
-      qx = (float)q[3 * qi];
-      qy = (float)q[3 * qi + 1];
-      qz = (float)q[3 * qi + 2];
+    float qx, qy, qz;
+    bool live;
+    {
+      const int64_t t = base + tid;
+      live = t < n;
+      const int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
+      qx = live ? (float)q[3 * qi] : 0.f;
+      qy = live ? (float)q[3 * qi + 1] : 0.f;
+      qz = live ? (float)q[3 * qi + 2] : 0.f;
+      s_q(tid) = make_float4(qx, qy, qz, 0.f);
+      const uint64_t hq = key_fold(hseed, (uint64_t)(qi + qoff));
+      s_hq(tid) = make_uint2((uint32_t)hq, (uint32_t)(hq >> 32));
     }
-    s_q(tid) = make_float4(qx, qy, qz, 0.f);
-    const uint64_t hq = key_fold(hseed, (uint64_t)(qi + qoff));
-    double acc = 0.0;  // control variates + level-1 residuals, (a, s) order
-    int seen = 0, steps = 0, paths = 0;
-    int nseq = 0;      // walks that went below level 1
-    int qbound = 0;    // upper bound of queue 0's length (block-uniform)
 
-    for (int a_ord = 0; a_ord < n1; ++a_ord) {  // block-uniform
-      ++seen;
-      const int4 tpa = s_tp1(a_ord);
-      const float4 ca = s_cm1(a_ord);
-      const float2 wa = KID == KID_WINDING ? s_w1(a_ord) : w0;
-      if (tpa.y == 0) {  // leaf subdomain: exact term, never sampled
-        float v = (tpa.w - tpa.z > 1) ? leaf_exact<KID>(V, tpa.z, tpa.w, qx, qy, qz, kp)
-                                      : fterm<KID>(ca, wa, qx, qy, qz, kp);
+    // ---- dense part (see the header): every level-2 record, FP32 partial
+    // sums over 16 records folded into the FP64 accumulator
+    double acc = 0.0;
+    if (!l2_multi) {
+      int k = 0;
+      for (; k + 16 <= n2; k += 16) {
+        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; u += 4) {
+          p0 += fterm<KID>(s_cm2(k + u), KID == KID_WINDING ? s_w2(k + u) : w0, qx, qy, qz, kp);
+          p1 += fterm<KID>(s_cm2(k + u + 1), KID == KID_WINDING ? s_w2(k + u + 1) : w0, qx, qy,
+                           qz, kp);
+          p2 += fterm<KID>(s_cm2(k + u + 2), KID == KID_WINDING ? s_w2(k + u + 2) : w0, qx, qy,
+                           qz, kp);
+          p3 += fterm<KID>(s_cm2(k + u + 3), KID == KID_WINDING ? s_w2(k + u + 3) : w0, qx, qy,
+                           qz, kp);
+        }
+        acc += (double)((p0 + p1) + (p2 + p3));
+      }
+      float p0 = 0.f;
+      for (; k < n2; ++k)
+        p0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
+      acc += (double)p0;
+    } else {
+      for (int k = 0; k < n2; ++k) {
+        float v;
+        if (s_b2(k) < 0) {
+          const int4 tp = V.topo[V.base2 + k];
+          v = leaf_exact<KID>(V, tp.z, tp.w, qx, qy, qz, kp);
+        } else {
+          v = fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
+        }
         acc += (double)v;
-        continue;
       }
-      // ---- dense control variate: cv(a) and the hoisted swap over a's children
-      const float cv = fterm<KID>(ca, wa, qx, qy, qz, kp);
-      const int k0 = tpa.x - V.base2, cc = tpa.y, kend = k0 + cc;
-      float ks0 = 0.f, ks1 = 0.f, ks2 = 0.f, ks3 = 0.f;
-      if (!l2_multi) {
-        int k = k0;
-        for (; k + 3 < kend; k += 4) {
-          ks0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
-          ks1 += fterm<KID>(s_cm2(k + 1), KID == KID_WINDING ? s_w2(k + 1) : w0, qx, qy, qz, kp);
-          ks2 += fterm<KID>(s_cm2(k + 2), KID == KID_WINDING ? s_w2(k + 2) : w0, qx, qy, qz, kp);
-          ks3 += fterm<KID>(s_cm2(k + 3), KID == KID_WINDING ? s_w2(k + 3) : w0, qx, qy, qz, kp);
-        }
-        for (; k < kend; ++k)
-          ks0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
-      } else {
-        for (int k = k0; k < kend; ++k) {
-          if (s_b2(k) < 0) {
-            int4 tp = V.topo[V.base2 + k];
-            ks0 += leaf_exact<KID>(V, tp.z, tp.w, qx, qy, qz, kp);
-          } else {
-            ks0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
-          }
-        }
-      }
-      const float delta_a = ((ks0 + ks1) + (ks2 + ks3)) - cv;
-      const int count_a = tpa.w - tpa.z;
-      const float rp_a = fdist(ca, qx, qy, qz) * id1;
-      const uint64_t ha = key_fold(hq, (uint64_t)a_ord);
-      for (int s = 0; s < S; ++s) {  // block-uniform
-        ++paths;
-        const uint64_t hs = key_fold(ha, (uint64_t)s);
-        const uint64_t ki = key_fold(hs, 0), kr = key_fold(hs, 1);
-        // index draw, exactly as _core.py:166-169
-        const double u0 = uniform_draw(ki, 0);
-        int j = tpa.z + (int)__dmul_rn(u0, (double)count_a);
-        if (j >= tpa.w) j = tpa.w - 1;
-        // level-1 step from shared memory: the swap at `a` is the hoisted delta_a
-        const int lo = child_search(o_b2, k0, cc, j);
-        seen += cc + 1;
-        const float4 c2 = s_cm2(lo);
-        const float rc = fdist(c2, qx, qy, qz) * id2;
-        const float p = rr_fast(rp_a, rc, rr_mode);
-        if (live && draw24(kr, 0) < p) {  // descends: queue the deeper steps
-          ++steps;
-          const int pos = atomicAdd(&s_count(0), 1);
-          q0[pos].a = make_int4(tid | (2 << 8) | (a_ord << 16), nseq++, V.base2 + lo, j);
-          q0[pos].f = make_float4(
-              p, rc, fterm<KID>(c2, KID == KID_WINDING ? s_w2(lo) : w0, qx, qy, qz, kp), 0.f);
-          q0[pos].k = make_uint4((uint32_t)kr, (uint32_t)(kr >> 32), 0u, 0u);
-        }
-        // an iteration queues at most kBlock walks: track a block-uniform upper
-        // bound of the queue length and look at the real length only near capacity
-        qbound += kBlock;
-        if (qbound + kBlock > kQcap) {
-          __syncthreads();
-          qbound = s_count(0);
-          __syncthreads();
-          if (qbound + kBlock > kQcap) {
-            drain();
-            qbound = 0;
-          }
-        }
-      }
-      // every sample's level-1 residual is delta_a: cv + (S * delta_a) / S
-      acc += (double)cv + (double)delta_a;
     }
-    __syncthreads();
-    drain();
-    // owners fold their deeper residuals in creation order (query-intrinsic)
+    int steps = 0;
+
+    // ---- sampling, in chunks of per_chunk (a, s) pairs (block-uniform), each
+    // followed by a drain of the walks it queued (one chunk per tile unless
+    // n1 * S is large)
+    for (int f0 = 0; f0 < nslot; f0 += V.per_chunk) {
+      const int f1 = min(f0 + V.per_chunk, nslot);
+      int a_ord = f0 / S, s = f0 - a_ord * S;
+      for (int f = f0; f < f1; ++a_ord, s = 0) {  // block-uniform
+        const int4 tpa = s_tp1(a_ord);
+        if (tpa.y == 0) {  // leaf subdomain: exact term, never sampled
+          if (s == 0) {
+            acc += (double)((tpa.w - tpa.z > 1)
+                                ? leaf_exact<KID>(V, tpa.z, tpa.w, qx, qy, qz, kp)
+                                : fterm<KID>(s_cm1(a_ord), KID == KID_WINDING ? s_w1(a_ord) : w0,
+                                             qx, qy, qz, kp));
+          }
+          const int take = min(S - s, f1 - f);
+          f += take;
+          continue;
+        }
+        const int k0 = tpa.x - V.base2, lut0 = a_ord * (kLut + 1);
+        const int count_a = tpa.w - tpa.z;
+        const float rp_a = fdist(s_cm1(a_ord), qx, qy, qz) * id1;
+        const uint2 hqv = s_hq(tid);
+        const uint64_t ha = key_fold(((uint64_t)hqv.y << 32) | hqv.x, (uint64_t)a_ord);
+        for (; s < S && f < f1; ++s, ++f) {  // block-uniform
+          const uint64_t hs = key_fold(ha, (uint64_t)s);
+          const uint64_t ki = key_fold(hs, 0), kr = key_fold(hs, 1);
+          // index draw, exactly as _core.py:166-169 (uniform_draw(ki, 0))
+          const uint64_t x = mix64(ki + kGamma);
+          const double u0 = __ull2double_rn(x >> 11) * (1.0 / 9007199254740992.0);
+          int j = tpa.z + (int)__dmul_rn(u0, (double)count_a);
+          if (j >= tpa.w) j = tpa.w - 1;
+          // level-1 step from shared memory (the swap at `a` is in the dense
+          // part): bucket table, then a short forward scan over child begins
+          const int bkt = (int)(x >> (64 - kLutBits));
+          int c = s_lut(lut0 + bkt);
+          const int ce = s_lut(lut0 + bkt + 1);
+          while (c < ce && (s_b2(k0 + c + 1) & 0x7fffffff) <= j) ++c;
+          const int lo = k0 + c;
+          const float rc = fdist(s_cm2(lo), qx, qy, qz) * id2;
+          const float p = rr_fast_t<RR>(rp_a, rc);
+          if (live && survive<RR>(p, kr, 0)) {  // descends: queue the walk start
+            ++steps;
+            const int pos = atomicAdd(&s_count(0), 1);
+            qa[pos] = make_int4(tid | (s << 8), a_ord, lo, j);
+            qk[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
+          }
+          else {
+            my_res[f * kBlock + tid] = 0.f;
+          }
+        }
+      }
+      __syncthreads();
+
+      // ---- drain: every lane holding no walk takes the next start (warp-
+      // aggregated claim on a shared head counter) and carries it to completion
+      // one level per iteration, so lanes refill independently and no block
+      // barrier separates the levels.
+      {
+        const int cnt = s_count(0);
+        const int lane = tid & 31;
+        bool act = false;
+        int owner = 0, slot = 0, node = 0, lvl = 2, jj = 0, count_a = 1;
+        float prr = 1.f, rp = 0.f, cvn = 0.f, resid = 0.f;
+        float4 qq = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint64_t kr = 0;
+        while (true) {
+          const unsigned need = __ballot_sync(0xffffffffu, !act);
+          if (need) {
+            int head = 0;
+            if (lane == 0) head = atomicAdd(&s_count(1), __popc(need));
+            head = __shfl_sync(0xffffffffu, head, 0);
+            const int idx = head + __popc(need & ((1u << lane) - 1u));
+            if (!act && idx < cnt) {
+              const int4 wa = qa[idx];
+              const uint2 wk = qk[idx];
+              owner = wa.x & 0xff;
+              const int ws = wa.x >> 8, wa_ord = wa.y, k = wa.z;
+              slot = wa_ord * S + ws;
+              jj = wa.w;
+              kr = ((uint64_t)wk.y << 32) | wk.x;
+              qq = s_q(owner);
+              const int4 tpa = s_tp1(wa_ord);
+              count_a = tpa.w - tpa.z;
+              const float4 c2 = s_cm2(k);
+              rp = fdist(c2, qq.x, qq.y, qq.z) * id2;
+              prr = rr_fast_t<RR>(fdist(s_cm1(wa_ord), qq.x, qq.y, qq.z) * id1, rp);
+              cvn = fterm<KID>(c2, KID == KID_WINDING ? s_w2(k) : w0, qq.x, qq.y, qq.z, kp);
+              node = V.base2 + k;
+              lvl = 2;
+              resid = 0.f;
+              act = true;
+            }
+          }
+          if (!__any_sync(0xffffffffu, act)) break;
+          if (!act) continue;
+          // one level: sum the node's contiguous children, pick the child
+          // holding the sampled point, commit the swap, roulette
+          const int4 tp = V.topo[node];
+          bool cont = false;
+          if (tp.y > 0) {
+            const bool cmulti = lvl + 1 >= V.first_multi;
+            float ks0 = 0.f, ks1 = 0.f;
+            int le = 0;  // children whose begin <= j: the last of them holds j
+            int c = 0;
+            if (!cmulti) {
+              for (; c + 1 < tp.y; c += 2) {
+                const int r = tp.x + c;
+                const float4 c0 = V.cm[r], c1 = V.cm[r + 1];
+                const int b0 = V.lb[r], b1 = V.lb[r + 1];
+                const float2 u0 = KID == KID_WINDING ? V.m12[r] : w0;
+                const float2 u1 = KID == KID_WINDING ? V.m12[r + 1] : w0;
+                ks0 += fterm<KID>(c0, u0, qq.x, qq.y, qq.z, kp);
+                ks1 += fterm<KID>(c1, u1, qq.x, qq.y, qq.z, kp);
+                le += (b0 <= jj) + (b1 <= jj);
+              }
+            }
+            for (; c < tp.y; ++c) {
+              const int r = tp.x + c;
+              const float4 cr = V.cm[r];
+              const float2 wr = KID == KID_WINDING ? V.m12[r] : w0;
+              float v;
+              if (cmulti) {
+                int4 tc = V.topo[r];
+                v = (tc.y == 0 && tc.w - tc.z > 1)
+                        ? leaf_exact<KID>(V, tc.z, tc.w, qq.x, qq.y, qq.z, kp)
+                        : fterm<KID>(cr, wr, qq.x, qq.y, qq.z, kp);
+              } else {
+                v = fterm<KID>(cr, wr, qq.x, qq.y, qq.z, kp);
+              }
+              ks0 += v;
+              le += V.lb[r] <= jj;
+            }
+            const float ks = ks0 + ks1;
+            const int cidx = tp.x + le - 1;
+            const float4 cch = V.cm[cidx];  // L1 hit: just streamed
+            atomicAdd(&s_seen(owner), tp.y + 1);
+            const float pagg = (float)(tp.w - tp.z) / (float)count_a;
+            resid += (ks - cvn) * rcp_ftz(pagg * prr);
+            const float rc =
+                fdist(cch, qq.x, qq.y, qq.z) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
+            const float p = rr_fast_t<RR>(rp, rc);
+            if (survive<RR>(p, kr, (uint64_t)(lvl - 1))) {  // counter = levels descended
+              cont = true;
+              atomicAdd(&s_steps(owner), 1);
+              const float2 wc = KID == KID_WINDING ? V.m12[cidx] : w0;
+              cvn = fterm<KID>(cch, wc, qq.x, qq.y, qq.z, kp);
+              prr *= p;
+              rp = rc;
+              node = cidx;
+              ++lvl;
+            }
+          }
+          if (!cont) {
+            my_res[slot * kBlock + owner] = resid;
+            act = false;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s_count(0) = 0;
+        s_count(1) = 0;
+      }
+      __syncthreads();
+    }
+
+    // owners fold their deeper residuals in (a, s) order (query-intrinsic).
+    // (Re-zeroing the slots here instead of storing zeros for non-descending
+    // samples measured 1.8x slower overall: it stalls the next drain.)
     double acc_deep = 0.0;
-    for (int k2 = 0; k2 < nseq; ++k2) acc_deep += (double)my_res[(int64_t)tid * res_stride + k2];
-    seen += s_seen(tid);
+    for (int k2 = 0; k2 < nslot; ++k2) {
+      acc_deep += (double)my_res[k2 * kBlock + tid];
+    }
+    const int seen = seen_base + s_seen(tid);
     steps += s_steps(tid);
     s_seen(tid) = 0;
     s_steps(tid) = 0;
     const double total = acc + acc_deep / (double)S;
     if (live) {
+      const int64_t t = base + tid;
+      const int64_t qi = qperm ? (int64_t)qperm[t] : t;
       out[qi] = (float)total;
       if (visited) visited[qi] = seen;
       if (path_steps) path_steps[qi] = steps;
-      if (path_count) path_count[qi] = paths;
+      if (path_count) path_count[qi] = (int64_t)S * n_int;
     }
     __syncthreads();
   }
@@ -389,10 +482,12 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 #undef s_cm2
 #undef s_w1
 #undef s_w2
+#undef s_hq
 #undef s_b2
 #undef s_seen
 #undef s_steps
 #undef s_count
+#undef s_lut
 }
 
 // returns 1 if the fast path does not apply (caller falls back), 0 on launch
@@ -422,9 +517,15 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   }
   bool wind = kid == KID_WINDING;
   if ((int64_t)V.n1 * n_samples > (1 << 20)) return 0;
+  // a chunk of per_chunk (a, s) pairs queues at most per_chunk * kBlock walks
+  const int64_t nslot = (int64_t)V.n1 * n_samples;
+  V.per_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nslot, FSB_QCAP_MAX / kBlock));
+  V.qcap = V.per_chunk * kBlock;
   const size_t n1 = (size_t)V.n1, n2 = (size_t)V.n2;
-  size_t smem = 16 * ((size_t)kBlock + 2 * n1 + n2) + (wind ? 8 * (n1 + n2) : 0) +
-                4 * (n2 + 2 * (size_t)kBlock + 4);
+  size_t smem = 16 * ((size_t)kBlock + 2 * n1 + n2) + 8 * ((wind ? n1 + n2 : 0) + kBlock) +
+                4 * (n2 + 2 * (size_t)kBlock + 4) + 2 * n1 * (kLut + 1);
+  smem = (smem + 15) & ~(size_t)15;
+  if (n2 >= 65535 || (int64_t)nslot * kBlock >= (1ll << 31)) return 0;
   if (smem > 200 * 1024) return 0;
   KParams kp;
   kp.alpha = alpha;
@@ -439,24 +540,36 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   auto launch = [&](auto kern) -> int {
     if (smem > 48 * 1024)
       FS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+#ifdef FSB_CARVE
+    FS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, FSB_CARVE));
+#endif
     FS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B, smem));
     int64_t tiles = (n + B - 1) / B;
     int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
-    const int stride = V.n1 * n_samples;  // result slots per query (walks below level 1)
     Scratch res, queues;
-    FS_TRY(res.alloc(sizeof(float) * (size_t)grid * B * stride, s));
-    FS_TRY(queues.alloc((size_t)grid * 2 * kQueueBytes, s));
-    kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, rr_mode, seed, qoff, kp,
-                                         res.as<float>(), stride, queues.as<unsigned char>(), out,
+    FS_TRY(res.alloc(sizeof(float) * (size_t)grid * B * nslot, s));
+    FS_TRY(queues.alloc((size_t)grid * V.qcap * kWalkBytes, s));
+    kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, seed, qoff, kp,
+                                         res.as<float>(), queues.as<unsigned char>(), out,
                                          visited, path_steps, path_count);
     FS_CK(cudaGetLastError());
     return 0;
   };
   int rc = 0;
-  switch (kid) {
-    case 0: rc = launch(k_sto_fast<0>); break;
-    case 1: rc = launch(k_sto_fast<1>); break;
-    case 2: rc = launch(k_sto_fast<2>); break;
+  if (rr_mode < 0 || rr_mode > 2) {
+    set_error("unknown rr mode %d", rr_mode);
+    return 1;
+  }
+  switch (kid * 3 + rr_mode) {
+    case 0: rc = launch(k_sto_fast<0, 0>); break;
+    case 1: rc = launch(k_sto_fast<0, 1>); break;
+    case 2: rc = launch(k_sto_fast<0, 2>); break;
+    case 3: rc = launch(k_sto_fast<1, 0>); break;
+    case 4: rc = launch(k_sto_fast<1, 1>); break;
+    case 5: rc = launch(k_sto_fast<1, 2>); break;
+    case 6: rc = launch(k_sto_fast<2, 0>); break;
+    case 7: rc = launch(k_sto_fast<2, 1>); break;
+    case 8: rc = launch(k_sto_fast<2, 2>); break;
     default: set_error("unknown kernel id"); return 1;
   }
   if (rc == 0) *used = true;

@@ -156,7 +156,10 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
             raise ValueError("prebuilt tree branching factor does not match config")
         h = C.c_void_p(tree._device_tree().handle)
         perm = None
-        if query_order and config.method in ("barnes_hut", "stochastic") and n > 1:
+        # Morton order of the queries pays for BH (warp-coherent traversal); the
+        # stochastic kernel's node set is query-independent (dense part) or
+        # keyed on the sampled point (walks), so it takes queries as given
+        if query_order and config.method == "barnes_hut" and n > 1:
             perm = dev.empty(n, torch.int32)
             _lib.check(L.fsb_query_order(_vp(q), n, _vp(perm), _sp()))
         if config.method == "barnes_hut":

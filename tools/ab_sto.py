@@ -19,6 +19,7 @@ n = len(qs)
 sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 perm = dev.empty(n, torch.int32)
 L.fsb_query_order(C.c_void_p(dev.ptr(q)), n, C.c_void_p(dev.ptr(perm)), sp)
+PERM = None if os.environ.get("NOPERM") else C.c_void_p(dev.ptr(perm))
 raw = dev.empty(n, torch.float32)
 vis = dev.empty(n, torch.int64)
 h = C.c_void_p(t4._device_tree().handle)
@@ -27,7 +28,7 @@ S = int(os.environ.get("S", "1"))
 
 def run():
     _lib.check(L.fsb_stochastic_batch(h, 0, 200.0, 1e-12, 1, C.c_void_p(dev.ptr(q)), n,
-                                      C.c_void_p(dev.ptr(perm)), S, 0, 1, 0,
+                                      PERM, S, 0, 1, 0,
                                       C.c_void_p(dev.ptr(raw)), C.c_void_p(dev.ptr(vis)), None,
                                       None, sp))
 
@@ -41,5 +42,5 @@ for _ in range(10):
     run()
 b.record()
 torch.cuda.synchronize()
-print(f"{os.environ.get('FSB_LIB', 'default')}: S={S} {a.elapsed_time(b) / 10:.3f} ms/launch, "
+print(f"{os.environ.get('FSB_LIB', 'default')}{' noperm' if PERM is None else ''}: S={S} {a.elapsed_time(b) / 10:.3f} ms/launch, "
       f"checksum {raw.double().sum().item():.9e}")
