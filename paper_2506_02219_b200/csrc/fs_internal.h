@@ -76,6 +76,7 @@ int level_order(FsTree* t, const int32_t* nb, const int32_t* nd, int max_dep,
 int ensure_bh(FsTree* t, bool f64, cudaStream_t s);
 int ensure_lo(FsTree* t, bool f64, cudaStream_t s);
 int ensure_fast(FsTree* t, cudaStream_t s);
+int ensure_path(FsTree* t, cudaStream_t s);
 void free_tree(FsTree* t);
 
 }  // namespace fsb

@@ -21,7 +21,7 @@ void free_tree(FsTree* t) {
                   t->perm, t->points, t->masses, t->weights, t->lo2pre, t->pre2lo, t->skip,
                   t->fc_lo, t->bh32, t->bh64, t->lo_geo32, t->lo_mass32, t->lo_geo64,
                   t->lo_mass64, t->lo_topo, t->pts32a, t->pts32b, t->pts64a, t->pts64b,
-                  t->lo_cm32, t->lo_m12_32, t->lo_begin};
+                  t->lo_cm32, t->lo_m12_32, t->lo_begin, t->pt_path};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;
@@ -285,6 +285,58 @@ __global__ void k_level_check(int64_t r0, int64_t r1, int level, const int32_t* 
   int64_t i = lo2pre[r];
   if (diam[i] != diam[lo2pre[r0]]) flags[0] = 1;
   if (cc[i] == 0 && e[i] - b[i] > 1) atomicMin(&flags[1], level);
+}
+
+// rank of point j's ancestor among its siblings, per level, packed LSB-first
+__global__ void k_point_path(const int4* __restrict__ topo, int64_t m, int bits, int levels,
+                             uint64_t* __restrict__ path) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  uint64_t p = 0;
+  int node = 0;
+  for (int l = 1; l <= levels; ++l) {
+    const int4 tp = topo[node];  // {first child, count, begin, end}
+    if (tp.y == 0) break;
+    int lo = 0, hi = tp.y;  // last child whose begin <= j
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (topo[tp.x + mid].z <= j)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    p |= (uint64_t)lo << (bits * (l - 1));
+    node = tp.x + lo;
+  }
+  path[j] = p;
+}
+
+__global__ void k_max_children(const int4* __restrict__ topo, int64_t n, int* __restrict__ out) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int v = r < n ? topo[r].y : 0;
+  v = __reduce_max_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && v > 0) atomicMax(out, v);
+}
+
+int ensure_path(FsTree* t, cudaStream_t s) {
+  if (t->pt_path) return 0;
+  FS_TRY(ensure_lo(t, false, s));
+  Scratch mx;
+  FS_TRY(mx.alloc(sizeof(int), s));
+  FS_CK(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+  k_max_children<<<grid_for(t->n, 256), 256, 0, s>>>(t->lo_topo, t->n, mx.as<int>());
+  int kids = 0;
+  FS_CK(cudaMemcpyAsync(&kids, mx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FS_CK(cudaStreamSynchronize(s));
+  int bits = 1;
+  while ((1ll << bits) < kids) ++bits;
+  FS_TRY(dalloc(&t->pt_path, t->m));
+  t->path_bits = bits;
+  t->path_levels = bits <= 16 ? 64 / bits : 0;
+  k_point_path<<<grid_for(t->m, 256), 256, 0, s>>>(t->lo_topo, t->m, bits, t->path_levels,
+                                                   t->pt_path);
+  FS_CK(cudaGetLastError());
+  return 0;
 }
 
 int ensure_fast(FsTree* t, cudaStream_t s) {

@@ -42,6 +42,8 @@ struct FastView {
   const int32_t* __restrict__ lb;  // begin
   const float4* __restrict__ pa;   // permuted points {x, y, z, m0}
   const float4* __restrict__ pb;   // {m1, m2, 0, 0}
+  const uint64_t* __restrict__ path;  // per point: sibling rank per level (ensure_path)
+  int path_bits, path_levels;
   int n1, base2, n2, first_multi;
   int per_chunk;                   // (a, s) samples per thread between drains
   int qcap;                        // queued walk starts per block
@@ -350,6 +352,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
         const int lane = tid & 31;
         bool act = false;
         int owner = 0, slot = 0, node = 0, lvl = 2, jj = 0, count_a = 1;
+        uint64_t path = 0;
         float prr = 1.f, rp = 0.f, cvn = 0.f, resid = 0.f;
         float4 qq = make_float4(0.f, 0.f, 0.f, 0.f);
         uint64_t kr = 0;
@@ -367,6 +370,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
               const int ws = wa.x >> 8, wa_ord = wa.y, k = wa.z;
               slot = wa_ord * S + ws;
               jj = wa.w;
+              path = V.path[jj];
               kr = ((uint64_t)wk.y << 32) | wk.x;
               qq = s_q(owner);
               const int4 tpa = s_tp1(wa_ord);
@@ -392,7 +396,25 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
             float ks0 = 0.f, ks1 = 0.f;
             int le = 0;  // children whose begin <= j: the last of them holds j
             int c = 0;
-            if (!cmulti) {
+            if (!cmulti && lvl < V.path_levels) {
+              // the sampled point's path gives the child's rank: only the
+              // aggregates are read (one 16-byte load per child)
+              le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
+              for (; c + 3 < tp.y; c += 4) {
+                const int r = tp.x + c;
+                const float4 c0 = V.cm[r], c1 = V.cm[r + 1], c2 = V.cm[r + 2], c3 = V.cm[r + 3];
+                ks0 += fterm<KID>(c0, KID == KID_WINDING ? V.m12[r] : w0, qq.x, qq.y, qq.z, kp);
+                ks1 += fterm<KID>(c1, KID == KID_WINDING ? V.m12[r + 1] : w0, qq.x, qq.y, qq.z,
+                                  kp);
+                ks0 += fterm<KID>(c2, KID == KID_WINDING ? V.m12[r + 2] : w0, qq.x, qq.y, qq.z,
+                                  kp);
+                ks1 += fterm<KID>(c3, KID == KID_WINDING ? V.m12[r + 3] : w0, qq.x, qq.y, qq.z,
+                                  kp);
+              }
+              for (; c < tp.y; ++c)
+                ks0 += fterm<KID>(V.cm[tp.x + c], KID == KID_WINDING ? V.m12[tp.x + c] : w0, qq.x,
+                                  qq.y, qq.z, kp);
+            } else if (!cmulti) {
               for (; c + 1 < tp.y; c += 2) {
                 const int r = tp.x + c;
                 const float4 c0 = V.cm[r], c1 = V.cm[r + 1];
@@ -507,6 +529,10 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   V.lb = t->lo_begin;
   V.pa = t->pts32a;
   V.pb = t->pts32b;
+  FS_TRY(ensure_path(t, s));
+  V.path = t->pt_path;
+  V.path_bits = t->path_bits;
+  V.path_levels = t->path_levels;
   V.n1 = t->root_kids;
   V.base2 = t->num_levels > 2 ? (int)t->level_off[2] : (int)t->n;
   V.n2 = t->num_levels > 2 ? (int)(t->level_off[3] - t->level_off[2]) : 0;

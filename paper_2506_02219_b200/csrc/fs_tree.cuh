@@ -56,6 +56,10 @@ struct FsTree {
   float4* lo_cm32 = nullptr;     // {cx, cy, cz, m0} per level-order node
   float2* lo_m12_32 = nullptr;   // {m1, m2} (winding)
   int32_t* lo_begin = nullptr;   // point-range begin per level-order node
+  // per (permuted) point: rank of its ancestor among its siblings at levels
+  // 1..path_levels, path_bits bits per level (child pick without begins)
+  uint64_t* pt_path = nullptr;
+  int path_bits = 0, path_levels = 0;
 };
 
 }  // namespace fsb
