@@ -110,6 +110,45 @@ int fsb_query_order(const double *queries, int64_t n, int32_t *perm_out, void *s
 int fsb_post_transform(const void *raw, int raw_is_f32, int64_t n, int smooth, double alpha,
                        double *values, double *raw64, uint8_t *flagged, void *stream);
 
+/* evaluate_field (estimators.py:260-323) from HOST queries to HOST results, the
+ * call a host-memory caller of the reference API makes.  The query set is split
+ * into `chunks` slabs whose host->device copies, evaluation and device->host
+ * copies overlap on three streams (pinned host buffers give full overlap;
+ * pageable ones work but serialise the copies).  Stochastic RNG streams are keyed
+ * on global query indices (query_offset + slab start), so results do not depend
+ * on `chunks`.  Outputs (n,): values, raw (double; may be NULL), flagged (uint8;
+ * may be NULL), visited / path_steps / path_count (int64; may be NULL); the
+ * counters the method does not report are zero, visited = m for brute force
+ * (FieldResult, estimators.py:45-64).  Synchronises. */
+enum {
+  FSB_METHOD_BRUTE_FORCE = 0,
+  FSB_METHOD_BARNES_HUT = 1,
+  FSB_METHOD_TELESCOPING = 2,
+  FSB_METHOD_STOCHASTIC = 3
+};
+typedef struct fsb_eval_args {
+  int method;             /* FSB_METHOD_* (EstimatorConfig.method, types.py:189-229) */
+  int kid;                /* kernel id */
+  double alpha, dfloor;   /* KernelSpec */
+  int precision;          /* 0 f64, 1 f32 */
+  double beta;            /* barnes_hut opening parameter */
+  int64_t n_samples;      /* stochastic samples per subdomain */
+  int rr_mode;            /* stochastic roulette mode */
+  uint64_t seed;          /* stochastic seed */
+  int64_t query_offset;   /* stochastic: global index of query 0 */
+  int smooth;             /* post-transform: kernel is smooth_exp */
+  int query_order;        /* barnes_hut: evaluate in Morton order (result-invariant) */
+  const double *src_pts;  /* brute force: device sources (m,3) */
+  const double *src_ms;   /* brute force: device masses (m,c) */
+  int64_t m;
+  int c;
+} fsb_eval_args;
+
+int fsb_evaluate_field_host(fsb_tree *tree, const fsb_eval_args *args, const double *queries,
+                            int64_t n, double *values, double *raw, uint8_t *flagged,
+                            int64_t *visited, int64_t *path_steps, int64_t *path_count,
+                            int chunks, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,17 @@ _I64 = C.c_int64
 _I = C.c_int
 _D = C.c_double
 
+
+class EvalArgs(C.Structure):
+    """fsb_eval_args (include/fastsum_b200.h)."""
+    _fields_ = [("method", _I), ("kid", _I), ("alpha", _D), ("dfloor", _D), ("precision", _I),
+                ("beta", _D), ("n_samples", _I64), ("rr_mode", _I), ("seed", C.c_uint64),
+                ("query_offset", _I64), ("smooth", _I), ("query_order", _I),
+                ("src_pts", _P), ("src_ms", _P), ("m", _I64), ("c", _I)]
+
+
+METHOD_CODES = {"brute_force": 0, "barnes_hut": 1, "telescoping_exhaustive": 2, "stochastic": 3}
+
 # name -> argtypes (restype int unless listed in _RESTYPES)
 SIGNATURES = {
     "fsb_abi_version": [],
@@ -42,6 +53,8 @@ SIGNATURES = {
     "fsb_telescoping_batch": [_P, _I, _D, _D, _I, _P, _I64, _P, _P, _P],
     "fsb_query_order": [_P, _I64, _P, _P],
     "fsb_post_transform": [_P, _I, _I64, _I, _D, _P, _P, _P, _P],
+    "fsb_evaluate_field_host": [_P, C.POINTER(EvalArgs), _P, _I64, _P, _P, _P, _P, _P, _P, _I,
+                                _P],
 }
 _RESTYPES = {"fsb_last_error": C.c_char_p}
 

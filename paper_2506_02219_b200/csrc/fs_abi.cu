@@ -96,7 +96,7 @@ __global__ void k_qmorton(const double* __restrict__ q, int64_t n, const float* 
   idx[i] = (int32_t)i;
 }
 
-static int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s) {
+int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s) {
   if (n <= 0) return 0;
   Scratch bb, code, code2, idx;
   const int nb = (int)std::min<int64_t>(296, (n + 255) / 256);

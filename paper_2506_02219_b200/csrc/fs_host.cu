@@ -1,0 +1,245 @@
+// fs_host.cu -- evaluate_field from host memory to host memory, pipelined.
+//
+// The reference's evaluate_field (estimators.py:260-323) takes host arrays and
+// returns host arrays.  On the device the cost of that contract is the PCIe
+// traffic (24 B in, up to 41 B out per query), so the query set is split into
+// slabs and three streams overlap slab k's evaluation with slab k+1's
+// host->device copy and slab k-1's device->host copies.  The RNG streams of the
+// stochastic estimator are keyed on global query indices (query_offset + slab
+// start, _core.py:219, 258), so the result is identical to one whole launch.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../../include/fastsum_b200.h"
+#include "fs_eval.h"
+#include "fs_internal.h"
+
+struct fsb_tree {
+  fsb::FsTree* t;
+};
+
+namespace fsb {
+
+int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s);
+
+namespace {
+
+__global__ void k_fill_i64(int64_t* __restrict__ a, int64_t n, int64_t v) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
+// Streams and events of the host pipeline, created once per (thread, device)
+// and reused: creating them per call costs more than a small evaluation.
+struct Streams {
+  cudaStream_t h2d = nullptr, d2h = nullptr, c2 = nullptr;
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  int init() {
+    if (h2d) return 0;
+    FS_CK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    FS_CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    FS_CK(cudaStreamCreateWithFlags(&c2, cudaStreamNonBlocking));
+    return 0;
+  }
+  int event(cudaEvent_t* out) {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      FS_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+    *out = ev[used++];
+    return 0;
+  }
+};
+
+Streams& streams_for_device() {
+  static thread_local Streams per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Streams& st = per_dev[dev & 63];
+  st.used = 0;
+  return st;
+}
+
+}  // namespace
+
+static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host, int64_t n,
+                         double* values, double* raw_h, uint8_t* flagged, int64_t* visited,
+                         int64_t* path_steps, int64_t* path_count, int chunks, cudaStream_t s) {
+  const bool f32 = a->precision == 1;
+  const size_t rsz = f32 ? sizeof(float) : sizeof(double);
+  // device buffers (stream-ordered pool allocations on the compute stream)
+  Scratch qd, raw, val, raw64, flg, vis, stp, cnt, perm;
+  FS_TRY(qd.alloc(sizeof(double) * 3 * (size_t)n, s));
+  FS_TRY(raw.alloc(rsz * (size_t)n, s));
+  FS_TRY(val.alloc(sizeof(double) * (size_t)n, s));
+  if (raw_h) FS_TRY(raw64.alloc(sizeof(double) * (size_t)n, s));
+  FS_TRY(flg.alloc((size_t)n, s));
+  FS_TRY(vis.alloc(sizeof(int64_t) * (size_t)n, s));
+  FS_TRY(stp.alloc(sizeof(int64_t) * (size_t)n, s));
+  FS_TRY(cnt.alloc(sizeof(int64_t) * (size_t)n, s));
+  if (a->method == FSB_METHOD_BARNES_HUT && a->query_order)
+    FS_TRY(perm.alloc(sizeof(int32_t) * (size_t)n, s));
+
+  Streams& st = streams_for_device();
+  FS_TRY(st.init());
+  cudaEvent_t ready;
+  FS_TRY(st.event(&ready));
+  FS_CK(cudaEventRecord(ready, s));  // allocations visible to the other streams
+  FS_CK(cudaStreamWaitEvent(st.h2d, ready, 0));
+  FS_CK(cudaStreamWaitEvent(st.c2, ready, 0));
+
+  // FSB_TRACE=1: per-slab timeline (ms from the first H2D) on stderr
+  const bool trace = std::getenv("FSB_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t on) -> int {
+    if (!trace) return 0;
+    cudaEvent_t e;
+    FS_CK(cudaEventCreate(&e));
+    FS_CK(cudaEventRecord(e, on));
+    tev.push_back(e);
+    return 0;
+  };
+  // slab boundaries: the first and last slabs are half-size, since the first
+  // H2D and the last D2H copies cannot overlap any evaluation
+  chunks = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, n));
+  std::vector<int64_t> cut(chunks + 1, 0);
+  for (int k = 1; k < chunks; ++k)
+    cut[k] = (int64_t)((double)n * (k - 0.5) / (chunks - 1.0));
+  cut[chunks] = n;
+  const bool counters = a->method == FSB_METHOD_STOCHASTIC;
+  // Slabs alternate between two compute streams so that one slab's last
+  // blocks overlap the next slab's first ones (no launch tail per slab).
+  for (int k = 0; k < chunks; ++k) {
+    const int64_t lo = cut[k], m = cut[k + 1] - cut[k];
+    if (m <= 0) continue;
+    const cudaStream_t cs = (k & 1) ? st.c2 : s;
+    cudaEvent_t in_done, out_ready;
+    FS_TRY(st.event(&in_done));
+    FS_TRY(st.event(&out_ready));
+    double* qs = qd.as<double>() + 3 * lo;
+    FS_TRY(mark(st.h2d));
+    FS_CK(cudaMemcpyAsync(qs, q_host + 3 * lo, sizeof(double) * 3 * (size_t)m,
+                          cudaMemcpyHostToDevice, st.h2d));
+    FS_TRY(mark(st.h2d));
+    FS_CK(cudaEventRecord(in_done, st.h2d));
+    FS_CK(cudaStreamWaitEvent(cs, in_done, 0));
+    FS_TRY(mark(cs));
+
+    void* r = static_cast<char*>(raw.p) + rsz * (size_t)lo;
+    int64_t* v = vis.as<int64_t>() + lo;
+    int64_t* ps = stp.as<int64_t>() + lo;
+    int64_t* pc = cnt.as<int64_t>() + lo;
+    switch (a->method) {
+      case FSB_METHOD_BRUTE_FORCE:
+        FS_TRY(brute_force(a->kid, a->alpha, a->dfloor, !f32, a->src_pts, a->src_ms, a->m, a->c,
+                           qs, m, r, cs));
+        k_fill_i64<<<grid_for(m, 256), 256, 0, cs>>>(v, m, a->m);
+        break;
+      case FSB_METHOD_BARNES_HUT: {
+        int32_t* pp = nullptr;
+        if (a->query_order && m > 1) {
+          pp = perm.as<int32_t>() + lo;
+          FS_TRY(query_order(qs, m, pp, cs));
+        }
+        FS_TRY(barnes_hut(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, pp, a->beta, r, v, cs));
+        break;
+      }
+      case FSB_METHOD_TELESCOPING:
+        FS_TRY(telescoping(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, r, v, cs));
+        break;
+      default:
+        FS_TRY(stochastic(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, nullptr,
+                          (int)a->n_samples, a->rr_mode, a->seed, a->query_offset + lo, r, v, ps,
+                          pc, cs));
+    }
+    if (!counters) {
+      FS_CK(cudaMemsetAsync(ps, 0, sizeof(int64_t) * (size_t)m, cs));
+      FS_CK(cudaMemsetAsync(pc, 0, sizeof(int64_t) * (size_t)m, cs));
+    }
+    double* vd = val.as<double>() + lo;
+    double* r64 = raw_h ? raw64.as<double>() + lo : nullptr;
+    uint8_t* fd = flg.as<uint8_t>() + lo;
+    FS_TRY(post_transform(r, f32 ? 1 : 0, m, a->smooth, a->alpha, vd, r64, fd, cs));
+    FS_TRY(mark(cs));
+    FS_CK(cudaEventRecord(out_ready, cs));
+    FS_CK(cudaStreamWaitEvent(st.d2h, out_ready, 0));
+    FS_TRY(mark(st.d2h));
+    auto d2h = [&](void* dst, const void* src, size_t bytes) -> int {
+      if (dst) FS_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st.d2h));
+      return 0;
+    };
+    FS_TRY(d2h(values + lo, vd, sizeof(double) * (size_t)m));
+    if (raw_h) FS_TRY(d2h(raw_h + lo, r64, sizeof(double) * (size_t)m));
+    FS_TRY(d2h(flagged ? flagged + lo : nullptr, fd, (size_t)m));
+    FS_TRY(d2h(visited ? visited + lo : nullptr, v, sizeof(int64_t) * (size_t)m));
+    FS_TRY(d2h(path_steps ? path_steps + lo : nullptr, ps, sizeof(int64_t) * (size_t)m));
+    FS_TRY(d2h(path_count ? path_count + lo : nullptr, pc, sizeof(int64_t) * (size_t)m));
+    FS_TRY(mark(st.d2h));
+  }
+  // device buffers are freed on `s` after the last D2H copy
+  cudaEvent_t done;
+  FS_TRY(st.event(&done));
+  FS_CK(cudaEventRecord(done, st.d2h));
+  FS_CK(cudaStreamWaitEvent(s, done, 0));  // (d2h waited on every slab, c2's included)
+  FS_CK(cudaStreamSynchronize(st.d2h));
+  FS_CK(cudaStreamSynchronize(s));
+  if (trace) {
+    for (size_t k = 0; k + 6 <= tev.size(); k += 6) {
+      float t[6];
+      for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&t[i], tev[0], tev[k + i]);
+      fprintf(stderr, "slab %zu: h2d %.3f-%.3f  compute %.3f-%.3f  d2h %.3f-%.3f\n", k / 6, t[0],
+              t[1], t[2], t[3], t[4], t[5]);
+    }
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace fsb
+
+extern "C" int fsb_evaluate_field_host(fsb_tree* tree, const fsb_eval_args* a,
+                                       const double* queries, int64_t n, double* values,
+                                       double* raw, uint8_t* flagged, int64_t* visited,
+                                       int64_t* path_steps, int64_t* path_count, int chunks,
+                                       void* stream) {
+  using fsb::set_error;
+  if (!a || !values || (n > 0 && !queries)) {
+    set_error("null argument");
+    return 1;
+  }
+  if (a->kid < 0 || a->kid > 2 || (a->precision != 0 && a->precision != 1) || n < 0) {
+    set_error("bad kernel id / precision / query count");
+    return 1;
+  }
+  if (a->method < FSB_METHOD_BRUTE_FORCE || a->method > FSB_METHOD_STOCHASTIC) {
+    set_error("unknown method %d", a->method);
+    return 1;
+  }
+  if (a->method == FSB_METHOD_BRUTE_FORCE) {
+    if (!a->src_pts || !a->src_ms || a->m < 1 || (a->kid == 1 ? a->c != 3 : a->c < 1)) {
+      set_error("brute force needs device sources (m >= 1, channels matching the kernel)");
+      return 1;
+    }
+  } else if (!tree || !tree->t) {
+    set_error("null tree");
+    return 1;
+  }
+  if (a->method == FSB_METHOD_BARNES_HUT && !(a->beta > 0)) {
+    set_error("beta must be positive");
+    return 1;
+  }
+  if (a->method == FSB_METHOD_STOCHASTIC &&
+      (a->n_samples < 1 || a->n_samples > (1LL << 30) || a->rr_mode < 0 || a->rr_mode > 2)) {
+    set_error("bad samples_per_subdomain / rr mode");
+    return 1;
+  }
+  if (n == 0) return 0;
+  return fsb::evaluate_host(tree ? tree->t : nullptr, a, queries, n, values, raw, flagged,
+                            visited, path_steps, path_count, chunks,
+                            reinterpret_cast<cudaStream_t>(stream));
+}

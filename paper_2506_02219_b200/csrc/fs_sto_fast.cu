@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     k_sto_fast(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
                const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff,
                KParams kp, float* __restrict__ res_g, unsigned char* __restrict__ queues,
-               float* __restrict__ out, int64_t* __restrict__ visited,
+               unsigned int* __restrict__ tile_ctr, float* __restrict__ out, int64_t* __restrict__ visited,
                int64_t* __restrict__ path_steps, int64_t* __restrict__ path_count) {
   // Dynamic shared memory, addressed by element index off the extern arrays
   // (all alias the same window), so every access is LDS [index + imm] with no
@@ -237,7 +237,15 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
   const float2 w0 = make_float2(0.f, 0.f);
 
-  for (int64_t base = (int64_t)blockIdx.x * kBlock; base < n; base += (int64_t)gridDim.x * kBlock) {
+  // tiles are handed out dynamically (a block's tile count would otherwise
+  // differ by one across blocks: up to 1/3 idle time on short launches)
+  const int64_t ntiles = (n + kBlock - 1) / kBlock;
+  while (true) {
+    if (tid == 0) s_count(2) = (int)atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const int64_t tile = s_count(2);
+    if (tile >= ntiles) break;
+    const int64_t base = tile * kBlock;
     float qx, qy, qz;
     bool live;
     {
@@ -572,12 +580,15 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     FS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B, smem));
     int64_t tiles = (n + B - 1) / B;
     int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
-    Scratch res, queues;
+    Scratch res, queues, ctr;
     FS_TRY(res.alloc(sizeof(float) * (size_t)grid * B * nslot, s));
     FS_TRY(queues.alloc((size_t)grid * V.qcap * kWalkBytes, s));
+    FS_TRY(ctr.alloc(sizeof(unsigned int), s));
+    FS_CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned int), s));
     kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, seed, qoff, kp,
-                                         res.as<float>(), queues.as<unsigned char>(), out,
-                                         visited, path_steps, path_count);
+                                         res.as<float>(), queues.as<unsigned char>(),
+                                         ctr.as<unsigned int>(), out, visited, path_steps,
+                                         path_count);
     FS_CK(cudaGetLastError());
     return 0;
   };

@@ -184,10 +184,67 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
                        path_steps=steps, path_count=count, method=config.method)
 
 
+def _pipeline_chunks(n: int) -> int:
+    """Slabs for the host pipeline: enough to overlap PCIe with compute, each
+    slab still several waves of 148 SMs x 4 blocks x 256 queries."""
+    return int(max(1, min(8, n // 125_000)))
+
+
 def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSpec,
-                   queries: QuerySet, tree: Octree | None = None) -> FieldResult:
-    """estimators.py:260-323: dispatch on config.method, then post-transform."""
-    return evaluate_field_device(config, sources, kernel, queries, tree).to_host()
+                   queries: QuerySet, tree: Octree | None = None, *,
+                   chunks: int | None = None) -> FieldResult:
+    """estimators.py:260-323: dispatch on config.method, then post-transform.
+
+    Host queries in, host results out, through fsb_evaluate_field_host: slabs
+    of queries are copied, evaluated and copied back on overlapping streams
+    (results are independent of the slab count).  Outputs land in pinned host
+    buffers returned as numpy arrays.
+    """
+    _check_channels(sources, kernel)
+    L = _lib.lib()
+    torch = dev.torch()
+    q = np.ascontiguousarray(queries.positions, dtype=np.float64)
+    n = q.shape[0]
+    args = _lib.EvalArgs()
+    args.method = _lib.METHOD_CODES[config.method]
+    args.kid = kernel_id(kernel)
+    args.alpha, args.dfloor = float(kernel.alpha), float(kernel.distance_floor)
+    args.precision = 1 if config.precision == "f32" else 0
+    args.beta = float(config.beta)
+    args.n_samples = int(config.samples_per_subdomain)
+    args.rr_mode = _RR_CODES[config.rr_mode]
+    args.seed = int(config.seed) & ((1 << 64) - 1)
+    args.query_offset = 0
+    args.smooth = 1 if kernel.kind == "smooth_exp" else 0
+    args.query_order = 1
+    h = None
+    keep = []
+    if config.method == "brute_force":
+        pts, ms = dev.to_device(sources.positions), dev.to_device(sources.masses)
+        keep += [pts, ms]
+        args.src_pts, args.src_ms = dev.ptr(pts), dev.ptr(ms)
+        args.m, args.c = len(sources), sources.channel_count
+    else:
+        if tree is None:
+            tree = build_tree(sources, config.resolved_branching, config.max_depth)
+        elif tree.branching_per_dim != config.resolved_branching:
+            raise ValueError("prebuilt tree branching factor does not match config")
+        h = C.c_void_p(tree._device_tree().handle)
+    # one pinned block for all outputs: 5 x 8-byte columns, then the flags
+    block = torch.empty(41 * n + 8, dtype=torch.uint8, pin_memory=True)
+    base = block.data_ptr()
+    ptrs = [base + 8 * n * k for k in range(5)] + [base + 40 * n]
+    _lib.check(L.fsb_evaluate_field_host(
+        h, C.byref(args), q.ctypes.data_as(C.c_void_p), n,
+        C.c_void_p(ptrs[0]), C.c_void_p(ptrs[1]), C.c_void_p(ptrs[5]), C.c_void_p(ptrs[2]),
+        C.c_void_p(ptrs[3]), C.c_void_p(ptrs[4]),
+        int(chunks if chunks is not None else _pipeline_chunks(n)), _sp()))
+    mem = block.numpy()
+    cols = [mem[8 * n * k: 8 * n * (k + 1)] for k in range(5)]
+    return FieldResult(values=cols[0].view(np.float64), raw=cols[1].view(np.float64),
+                       flagged=mem[40 * n: 41 * n].view(bool),
+                       visited_nodes=cols[2].view(np.int64), path_steps=cols[3].view(np.int64),
+                       path_count=cols[4].view(np.int64), method=config.method)
 
 
 # ------------------------------------------------------- single-query wrappers

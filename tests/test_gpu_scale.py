@@ -149,3 +149,29 @@ def test_query_order_and_offset_invariance(fs):
                                        query_offset=a).to_host().values
                  for a, b in ((0, 1500), (1500, 2600), (2600, 4000))]
         np.testing.assert_array_equal(np.concatenate(parts), full)
+
+
+@pytest.mark.parametrize("method", ["stochastic", "barnes_hut", "brute_force",
+                                    "telescoping_exhaustive"])
+def test_host_pipeline_slab_invariance(fs, method):
+    """evaluate_field (host in / host out, fsb_evaluate_field_host) gives the same
+    bytes for any slab count as one device-resident evaluation (F8 + query_offset)."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 14, seed=19))
+    rng = np.random.default_rng(4)
+    q = fs.QuerySet(rng.uniform(-0.7, 0.7, (3001 if method != "telescoping_exhaustive" else 301,
+                                            3)))
+    for kind in ("coulomb", "smooth_exp"):
+        kern = fs.KernelSpec(kind)
+        src = s if kind == "coulomb" else fs.SourceSet(s.positions, np.ones((len(s), 1)))
+        for prec in ("f64", "f32"):
+            extra = dict(seed=5, samples_per_subdomain=2) if method == "stochastic" else {}
+            cfg = fs.EstimatorConfig(method, precision=prec, **extra)
+            t = None if method == "brute_force" else fs.build_tree(src, cfg.resolved_branching)
+            ref = evaluate_field_device(cfg, src, kern, q, t).to_host()
+            for chunks in (1, 2, 5):
+                r = fs.evaluate_field(cfg, src, kern, q, tree=t, chunks=chunks)
+                for k in ("values", "raw", "flagged", "visited_nodes", "path_steps",
+                          "path_count"):
+                    np.testing.assert_array_equal(getattr(r, k), getattr(ref, k),
+                                                  err_msg=f"{method} {kind} {prec} {chunks} {k}")
