@@ -274,16 +274,13 @@ def run_ours(args):
     value = world * n / (step_ms * 1e-3)
 
     # ---- the stochastic kernel alone (events on the launching stream), for the roofline
-    perm = dev.empty(n, torch.int32)
-    _lib.check(L.fsb_query_order(C.c_void_p(dev.ptr(q_dev)), n, C.c_void_p(dev.ptr(perm)), sp))
     raw = dev.empty(n, torch.float32)
     vis = dev.empty(n, torch.int64)
     h = C.c_void_p(tree4._device_tree().handle)
 
     def kernel_only():
         _lib.check(L.fsb_stochastic_batch(h, 0, kern.alpha, kern.distance_floor, 1,
-                                          C.c_void_p(dev.ptr(q_dev)), n,
-                                          C.c_void_p(dev.ptr(perm)), 1, 0, 1, qoff,
+                                          C.c_void_p(dev.ptr(q_dev)), n, None, 1, 0, 1, qoff,
                                           C.c_void_p(dev.ptr(raw)), C.c_void_p(dev.ptr(vis)),
                                           None, None, sp))
     kernel_only()
@@ -345,23 +342,42 @@ def run_ours(args):
         out["tree_build_ms"] = {"d4_first_call": build4_ms, "d2_first_call": build2_ms,
                                 "d4_warm": build4_warm_ms}
 
-        # ---- roofline of the stochastic kernel: FP32+MUFU bound
+        # ---- roofline of the stochastic kernel.  Work unit: one
+        # node-term evaluation ("interaction": 8 FP32-pipe ops + 1 MUFU.RSQ, 10
+        # flops).  Per query the kernel evaluates the N2 level-2 records (dense
+        # part) plus the children of every walk step below level 2; the walk
+        # part is visited - (n1 + S * sum_a(children(a) + 1)) (_core.py:195,205).
         pk = peaks()
         f_mhz = float(pk.get("sm_max_mhz", 1965.0))
         sms = torch.cuda.get_device_properties(local).multi_processor_count
-        # dense control-variate part: N1 + N2 interactions per query (level-1 + level-2)
-        info = (C.c_int64 * 8)()
-        L.fsb_tree_info(h, info)
-        n_dense = _dense_interactions(tree4)
-        inter = n_dense * n
-        ach = inter / (kern_ms * 1e-3)
+        n1, n2, n_int = _level_sizes(tree4)
+        S = 1
+        visited_base = n1 + S * (n2 + n_int)
+        walk_inter = max(visited_mean - visited_base, 0.0)
+        inter_q = n2 + walk_inter
+        samples_q = S * n_int
+        ach = inter_q * n / (kern_ms * 1e-3)
         limit = min(128 * sms * f_mhz * 1e6 / 8, 16 * sms * f_mhz * 1e6 / 1)  # coulomb I=8, U=1
-        out["roofline"] = {"bound": "fp32+mufu", "achieved": ach * 10 / 1e12, "peak": limit * 10 / 1e12,
-                           "unit": "TFLOP/s", "frac": ach / limit,
-                           "traffic": _profiled_traffic("k_sto_fast<0>"),
-                           "kernel": "k_stochastic<coulomb,f32>", "kernel_ms": kern_ms,
-                           "work": f"{n_dense} dense interactions/query x 10 flops (SURVEY 8d)",
-                           "peak_source": f"pipe rates x {sms} SMs x sm_max_mhz {f_mhz} (MEASURED_PEAKS.json)"}
+        # pipe floor with the integer RNG work (6 splitmix64 per sample: 6 IMAD on
+        # the FMA-heavy pipe + 14 ALU ops each): max over FMA / ALU / MUFU pipes
+        fma_cyc = (7 * inter_q + 2 * 36 * samples_q) / 128.0
+        alu_cyc = (1 * inter_q + 84 * samples_q) / 64.0
+        mufu_cyc = (inter_q + samples_q) / 16.0
+        floor_ms = max(fma_cyc, alu_cyc, mufu_cyc) * n / (sms * f_mhz * 1e6) * 1e3
+        out["roofline"] = {
+            "bound": "fp32+mufu", "achieved": ach * 10 / 1e12, "peak": limit * 10 / 1e12,
+            "unit": "TFLOP/s", "frac": ach / limit,
+            "traffic": _profiled_traffic("k_sto_fast<0"),
+            "kernel": "k_sto_fast<coulomb, paper_ratio> (FP32)", "kernel_ms": kern_ms,
+            "work": (f"{inter_q:.1f} interactions/query = {n2} dense level-2 records + "
+                     f"{walk_inter:.1f} walk children; 10 flops each"),
+            "peak_source": (f"FP32 128/clk/SM over 8 ops, MUFU 16/clk/SM over 1 op, {sms} SMs "
+                            f"x {f_mhz:.0f} MHz (nominal pipe rates; no MEASURED_PEAKS.json "
+                            f"entry for FP32/MUFU)"),
+            "pipe_floor_ms": floor_ms, "frac_of_pipe_floor": floor_ms / kern_ms,
+            "pipe_floor_note": (f"FMA/ALU/MUFU pipe floor incl. {samples_q} samples/query x 6 "
+                                f"splitmix64 mixes; cycles/query fma {fma_cyc:.1f} alu "
+                                f"{alu_cyc:.1f} mufu {mufu_cyc:.1f}")}
         # ---- e2e through the public API from pinned host memory
         out["e2e"] = _e2e(args, fs, src, kern, qs, tree4, cfg_s1, world)
         if args.cpu_baseline:
@@ -388,13 +404,13 @@ def _profiled_traffic(kernel_key: str):
     return None
 
 
-def _dense_interactions(tree) -> int:
-    """N1 + N2 for the d=4 tree: level-1 nodes plus children of internal level-1 nodes."""
+def _level_sizes(tree):
+    """(n1, n2, internal level-1 nodes) of the d=4 tree: level-1 nodes, their children."""
     cc = tree.child_count
     cs = tree.child_start
     ci = tree.child_index
     lvl1 = ci[cs[0]:cs[0] + cc[0]]
-    return int(len(lvl1) + sum(int(cc[a]) for a in lvl1))
+    return int(len(lvl1)), int(sum(int(cc[a]) for a in lvl1)), int(np.count_nonzero(cc[lvl1]))
 
 
 def _e2e(args, fs, src, kern, qs, tree, cfg, world):

@@ -35,6 +35,14 @@ KEYS = {
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio": "stall_long_sb",
     "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio": "stall_barrier",
     "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active": "l1tex_throughput_pct",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
+    "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "sm__cycles_active.avg": "sm_cycles_active_avg",
+    "sm__cycles_active.max": "sm_cycles_active_max",
+    "sm__cycles_elapsed.avg": "sm_cycles_elapsed_avg",
 }
 
 
