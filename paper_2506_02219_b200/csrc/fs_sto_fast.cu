@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   const int o_hq = o_w2 + (KID == KID_WINDING ? n2 : 0);
   const int o_b2 = 2 * (o_hq + kBlock);
   const int o_seen = o_b2 + n2, o_steps = o_seen + kBlock, o_count = o_steps + kBlock;
-  const int o_lut = 2 * (o_count + 4);
+  const int o_hist = o_count + 4;  // walk starts per level-2 node, then their offsets
+  const int o_lut = 2 * (o_hist + n2 + (n2 & 1));
 #define s_q(i) sh_f4[(i)]
 #define s_cm1(i) sh_f4[o_cm1 + (i)]
 #define s_tp1(i) sh_i4[o_tp1 + (i)]
@@ -175,9 +176,13 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 #define s_steps(i) sh_i[o_steps + (i)]
 #define s_count(i) sh_i[o_count + (i)]
 #define s_lut(i) sh_u16[o_lut + (i)]
+#define s_hist(i) sh_i[o_hist + (i)]
 
-  int4* const qa = reinterpret_cast<int4*>(queues + (size_t)blockIdx.x * V.qcap * kWalkBytes);
+  // two walk-start buffers: creation order (qa, qk) and sorted by level-2 node (sa, sk)
+  int4* const qa = reinterpret_cast<int4*>(queues + (size_t)blockIdx.x * 2 * V.qcap * kWalkBytes);
   uint2* const qk = reinterpret_cast<uint2*>(qa + V.qcap);
+  int4* const sa = reinterpret_cast<int4*>(qk + V.qcap);
+  uint2* const sk = reinterpret_cast<uint2*>(sa + V.qcap);
   const int tid = threadIdx.x;
   const int nslot = n1 * S;
   // result slots of this block, slot-major: res[(a_ord * S + s) * kBlock + owner].
@@ -206,6 +211,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   if (tid < 4) s_count(tid) = 0;  // [0] queue length, [1] drain head
   s_seen(tid) = 0;
   s_steps(tid) = 0;
+  for (int i = tid; i < n2; i += kBlock) s_hist(i) = 0;
   __syncthreads();
   // bucket table: j in bucket b (j - begin in [floor(b c / L), floor((b+1) c / L)],
   // c = count) lies in a child in [lut[b], lut[b+1]] (children are ordered by begin)
@@ -341,6 +347,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
           if (live && survive<RR>(p, kr, 0)) {  // descends: queue the walk start
             ++steps;
             const int pos = atomicAdd(&s_count(0), 1);
+            atomicAdd(&s_hist(lo), 1);
             qa[pos] = make_int4(tid | (s << 8), a_ord, lo, j);
             qk[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
           }
@@ -351,6 +358,44 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
       }
       __syncthreads();
 
+      // ---- counting sort of the walk starts by level-2 node into (sa, sk):
+      // lanes of a warp then sum the same node's children with the same load
+      // instructions (one request per distinct node rather than per lane), and
+      // the walk-start reads themselves are coalesced
+      {
+        const int cnt = s_count(0);
+        const int per = (n2 + kBlock - 1) / kBlock, b0 = min(tid * per, n2),
+                  b1 = min(b0 + per, n2);
+        int seg = 0;
+        for (int b = b0; b < b1; ++b) seg += s_hist(b);
+        const int lane = tid & 31, wid = tid >> 5;
+        int incl = seg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        __shared__ int s_wtot[kBlock / 32];  // per-warp totals of the scan
+        if (lane == 31) s_wtot[wid] = incl;
+        __syncthreads();
+        int run = incl - seg;
+        for (int w = 0; w < wid; ++w) run += s_wtot[w];
+        for (int b = b0; b < b1; ++b) {
+          const int c = s_hist(b);
+          s_hist(b) = run;
+          run += c;
+        }
+        __syncthreads();
+        for (int i = tid; i < cnt; i += kBlock) {
+          const int4 wa = qa[i];
+          const uint2 wk = qk[i];
+          const int pos = atomicAdd(&s_hist(wa.z), 1);
+          sa[pos] = wa;
+          sk[pos] = wk;
+        }
+        __syncthreads();
+        for (int b = tid; b < n2; b += kBlock) s_hist(b) = 0;
+      }
       // ---- drain: every lane holding no walk takes the next start (warp-
       // aggregated claim on a shared head counter) and carries it to completion
       // one level per iteration, so lanes refill independently and no block
@@ -372,8 +417,8 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
             head = __shfl_sync(0xffffffffu, head, 0);
             const int idx = head + __popc(need & ((1u << lane) - 1u));
             if (!act && idx < cnt) {
-              const int4 wa = qa[idx];
-              const uint2 wk = qk[idx];
+              const int4 wa = sa[idx];  // consecutive lanes, consecutive records
+              const uint2 wk = sk[idx];
               owner = wa.x & 0xff;
               const int ws = wa.x >> 8, wa_ord = wa.y, k = wa.z;
               slot = wa_ord * S + ws;
@@ -518,6 +563,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 #undef s_steps
 #undef s_count
 #undef s_lut
+#undef s_hist
 }
 
 // returns 1 if the fast path does not apply (caller falls back), 0 on launch
@@ -557,7 +603,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   V.qcap = V.per_chunk * kBlock;
   const size_t n1 = (size_t)V.n1, n2 = (size_t)V.n2;
   size_t smem = 16 * ((size_t)kBlock + 2 * n1 + n2) + 8 * ((wind ? n1 + n2 : 0) + kBlock) +
-                4 * (n2 + 2 * (size_t)kBlock + 4) + 2 * n1 * (kLut + 1);
+                4 * (2 * n2 + 2 * (size_t)kBlock + 6) + 2 * n1 * (kLut + 1);
   smem = (smem + 15) & ~(size_t)15;
   if (n2 >= 65535 || (int64_t)nslot * kBlock >= (1ll << 31)) return 0;
   if (smem > 200 * 1024) return 0;
@@ -582,7 +628,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * std::max(per_sm, 1));
     Scratch res, queues, ctr;
     FS_TRY(res.alloc(sizeof(float) * (size_t)grid * B * nslot, s));
-    FS_TRY(queues.alloc((size_t)grid * V.qcap * kWalkBytes, s));
+    FS_TRY(queues.alloc((size_t)grid * 2 * V.qcap * kWalkBytes, s));
     FS_TRY(ctr.alloc(sizeof(unsigned int), s));
     FS_CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned int), s));
     kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, seed, qoff, kp,
