@@ -109,6 +109,7 @@ extern __shared__ int4 sh_i4[];
 extern __shared__ float2 sh_f2[];
 extern __shared__ int sh_i[];
 extern __shared__ uint2 sh_u2[];
+extern __shared__ int2 sh_i2[];
 extern __shared__ unsigned short sh_u16[];
 
 // last index k in [lo, lo + cnt) whose begin (low 31 bits of sh_i[ob + k]) is <= j
@@ -162,7 +163,8 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   const int o_hq = o_w2 + (KID == KID_WINDING ? n2 : 0);
   const int o_b2 = 2 * (o_hq + kBlock);
   const int o_seen = o_b2 + n2, o_steps = o_seen + kBlock, o_count = o_steps + kBlock;
-  const int o_hist = o_count + 4;  // walk starts per level-2 node, then their offsets
+  const int o_t2 = (o_count + 5) / 2;  // (8-byte units, aligned) level-2 {first child | count << 25, points}
+  const int o_hist = 2 * (o_t2 + n2);  // walk starts per level-2 node, then their offsets
   const int o_lut = 2 * (o_hist + n2 + (n2 & 1));
 #define s_q(i) sh_f4[(i)]
 #define s_cm1(i) sh_f4[o_cm1 + (i)]
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 #define s_count(i) sh_i[o_count + (i)]
 #define s_lut(i) sh_u16[o_lut + (i)]
 #define s_hist(i) sh_i[o_hist + (i)]
+#define s_t2(i) sh_i2[o_t2 + (i)]
 
   // two walk-start buffers: creation order (qa, qk) and sorted by level-2 node (sa, sk)
   int4* const qa = reinterpret_cast<int4*>(queues + (size_t)blockIdx.x * 2 * V.qcap * kWalkBytes);
@@ -202,11 +205,10 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     s_cm2(i) = V.cm[V.base2 + i];
     if (KID == KID_WINDING) s_w2(i) = V.m12[V.base2 + i];
     int b = V.lb[V.base2 + i];
-    if (l2_multi) {
-      int4 tp = V.topo[V.base2 + i];
-      if (tp.y == 0 && tp.w - tp.z > 1) b |= 0x80000000;
-    }
+    const int4 tp = V.topo[V.base2 + i];
+    if (l2_multi && tp.y == 0 && tp.w - tp.z > 1) b |= 0x80000000;
     s_b2(i) = b;
+    s_t2(i) = make_int2(tp.y > 0 ? (tp.x | (tp.y << 25)) : 0, tp.w - tp.z);
   }
   if (tid < 4) s_count(tid) = 0;  // [0] queue length, [1] drain head
   s_seen(tid) = 0;
@@ -404,7 +406,8 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
         const int cnt = s_count(0);
         const int lane = tid & 31;
         bool act = false;
-        int owner = 0, slot = 0, node = 0, lvl = 2, jj = 0, count_a = 1;
+        int owner = 0, slot = 0, lvl = 2, jj = 0, count_a = 1;
+        int4 tp = make_int4(0, 0, 0, 0);  // {first child, count, begin, end} of the walk's node
         uint64_t path = 0;
         float prr = 1.f, rp = 0.f, cvn = 0.f, resid = 0.f;
         float4 qq = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -432,7 +435,9 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
               rp = fdist(c2, qq.x, qq.y, qq.z) * id2;
               prr = rr_fast_t<RR>(fdist(s_cm1(wa_ord), qq.x, qq.y, qq.z) * id1, rp);
               cvn = fterm<KID>(c2, KID == KID_WINDING ? s_w2(k) : w0, qq.x, qq.y, qq.z, kp);
-              node = V.base2 + k;
+              // level-2 topology from shared memory (begin only feeds end - begin)
+              const int2 t2 = s_t2(k);
+              tp = make_int4(t2.x & 0x1ffffff, (int)((unsigned)t2.x >> 25), 0, t2.y);
               lvl = 2;
               resid = 0.f;
               act = true;
@@ -442,7 +447,6 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
           if (!act) continue;
           // one level: sum the node's contiguous children, pick the child
           // holding the sampled point, commit the swap, roulette
-          const int4 tp = V.topo[node];
           bool cont = false;
           if (tp.y > 0) {
             const bool cmulti = lvl + 1 >= V.first_multi;
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
               cvn = fterm<KID>(cch, wc, qq.x, qq.y, qq.z, kp);
               prr *= p;
               rp = rc;
-              node = cidx;
+              tp = V.topo[cidx];
               ++lvl;
             }
           }
@@ -564,6 +568,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 #undef s_count
 #undef s_lut
 #undef s_hist
+#undef s_t2
 }
 
 // returns 1 if the fast path does not apply (caller falls back), 0 on launch
@@ -603,9 +608,9 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   V.qcap = V.per_chunk * kBlock;
   const size_t n1 = (size_t)V.n1, n2 = (size_t)V.n2;
   size_t smem = 16 * ((size_t)kBlock + 2 * n1 + n2) + 8 * ((wind ? n1 + n2 : 0) + kBlock) +
-                4 * (2 * n2 + 2 * (size_t)kBlock + 6) + 2 * n1 * (kLut + 1);
+                4 * (2 * n2 + 2 * (size_t)kBlock + 6) + 8 * n2 + 2 * n1 * (kLut + 1);
   smem = (smem + 15) & ~(size_t)15;
-  if (n2 >= 65535 || (int64_t)nslot * kBlock >= (1ll << 31)) return 0;
+  if (n2 >= 65535 || (int64_t)nslot * kBlock >= (1ll << 31) || t->n >= (1ll << 25)) return 0;
   if (smem > 200 * 1024) return 0;
   KParams kp;
   kp.alpha = alpha;
