@@ -188,11 +188,9 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   uint2* const sk = reinterpret_cast<uint2*>(sa + V.qcap);
   const int tid = threadIdx.x;
   const int nslot = n1 * S;
-  // result slots of this block, slot-major: res[(a_ord * S + s) * kBlock + owner].
-  // Every tile writes each internal subdomain's slots (zero, or the walk's
-  // residual); slots of leaf subdomains stay at the zero stored here.
+  // result slots of this block, slot-major: res[seq * kBlock + owner], seq = the
+  // walk's creation index among its owner's walks this tile ((a, s) order)
   float* const my_res = res_g + (int64_t)blockIdx.x * kBlock * nslot;
-  for (int i = tid; i < nslot * kBlock; i += kBlock) my_res[i] = 0.f;
 
   // ---- stage level 1 (root's children, level order 1..n1) and level 2
   for (int i = tid; i < n1; i += kBlock) {
@@ -346,15 +344,13 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
           const int lo = k0 + c;
           const float rc = fdist(s_cm2(lo), qx, qy, qz) * id2;
           const float p = rr_fast_t<RR>(rp_a, rc);
-          if (live && survive<RR>(p, kr, 0)) {  // descends: queue the walk start
-            ++steps;
+          // (lanes past the end of the query set sample too; results dropped)
+          if (survive<RR>(p, kr, 0)) {  // descends: queue the walk start
             const int pos = atomicAdd(&s_count(0), 1);
             atomicAdd(&s_hist(lo), 1);
-            qa[pos] = make_int4(tid | (s << 8), a_ord, lo, j);
+            qa[pos] = make_int4(tid | (steps << 8), a_ord, lo, j);
             qk[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
-          }
-          else {
-            my_res[f * kBlock + tid] = 0.f;
+            ++steps;
           }
         }
       }
@@ -423,8 +419,8 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
               const int4 wa = sa[idx];  // consecutive lanes, consecutive records
               const uint2 wk = sk[idx];
               owner = wa.x & 0xff;
-              const int ws = wa.x >> 8, wa_ord = wa.y, k = wa.z;
-              slot = wa_ord * S + ws;
+              const int wa_ord = wa.y, k = wa.z;
+              slot = wa.x >> 8;  // creation index among the owner's walks
               jj = wa.w;
               path = V.path[jj];
               kr = ((uint64_t)wk.y << 32) | wk.x;
@@ -533,13 +529,10 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
       __syncthreads();
     }
 
-    // owners fold their deeper residuals in (a, s) order (query-intrinsic).
-    // (Re-zeroing the slots here instead of storing zeros for non-descending
-    // samples measured 1.8x slower overall: it stalls the next drain.)
+    // owners fold their walks' residuals in creation ((a, s)) order: the value
+    // is query-intrinsic whatever lane served which walk
     double acc_deep = 0.0;
-    for (int k2 = 0; k2 < nslot; ++k2) {
-      acc_deep += (double)my_res[k2 * kBlock + tid];
-    }
+    for (int k2 = 0; k2 < steps; ++k2) acc_deep += (double)my_res[k2 * kBlock + tid];
     const int seen = seen_base + s_seen(tid);
     steps += s_steps(tid);
     s_seen(tid) = 0;
