@@ -50,6 +50,8 @@ struct FastView {
   float inv_diam[kFastMaxLevels];  // 1 / max(diam_level, 1e-12)
 };
 
+
+
 template <int KID>
 __device__ __forceinline__ float fterm(float4 c, float2 w, float qx, float qy, float qz,
                                        const KParams& kp) {
@@ -306,52 +308,70 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     // ---- sampling, in chunks of per_chunk (a, s) pairs (block-uniform), each
     // followed by a drain of the walks it queued (one chunk per tile unless
     // n1 * S is large)
+    // one sample (a, s): index draw, level-1 step from shared memory, roulette
+    auto sample = [&](int a_ord, int sm, const int4& tpa, int k0, int lut0, float rp_a,
+                      uint64_t ha) {
+      const uint64_t hs = key_fold(ha, (uint64_t)sm);
+      const uint64_t ki = key_fold(hs, 0), kr = key_fold(hs, 1);
+      // index draw, exactly as _core.py:166-169 (uniform_draw(ki, 0))
+      const uint64_t x = mix64(ki + kGamma);
+      const double u0 = __ull2double_rn(x >> 11) * (1.0 / 9007199254740992.0);
+      int j = tpa.z + (int)__dmul_rn(u0, (double)(tpa.w - tpa.z));
+      if (j >= tpa.w) j = tpa.w - 1;
+      // level-1 step from shared memory (the swap at `a` is in the dense
+      // part): bucket table, then a short forward scan over child begins
+      const int bkt = (int)(x >> (64 - kLutBits));
+      int c = s_lut(lut0 + bkt);
+      const int ce = s_lut(lut0 + bkt + 1);
+      while (c < ce && (s_b2(k0 + c + 1) & 0x7fffffff) <= j) ++c;
+      const int lo = k0 + c;
+      const float rc = fdist(s_cm2(lo), qx, qy, qz) * id2;
+      const float p = rr_fast_t<RR>(rp_a, rc);
+      // (lanes past the end of the query set sample too; results dropped)
+      if (survive<RR>(p, kr, 0)) {  // descends: queue the walk start
+        const int pos = atomicAdd(&s_count(0), 1);
+        atomicAdd(&s_hist(lo), 1);
+        qa[pos] = make_int4(tid | (steps << 8), a_ord, lo, j);
+        qk[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
+        ++steps;
+      }
+    };
+    auto leaf_term = [&](int a_ord, const int4& tpa) {
+      return (double)((tpa.w - tpa.z > 1)
+                          ? leaf_exact<KID>(V, tpa.z, tpa.w, qx, qy, qz, kp)
+                          : fterm<KID>(s_cm1(a_ord), KID == KID_WINDING ? s_w1(a_ord) : w0, qx,
+                                       qy, qz, kp));
+    };
+    const uint2 hqv = s_hq(tid);
+    const uint64_t hq = ((uint64_t)hqv.y << 32) | hqv.x;
+
     for (int f0 = 0; f0 < nslot; f0 += V.per_chunk) {
       const int f1 = min(f0 + V.per_chunk, nslot);
-      int a_ord = f0 / S, s = f0 - a_ord * S;
-      for (int f = f0; f < f1; ++a_ord, s = 0) {  // block-uniform
-        const int4 tpa = s_tp1(a_ord);
-        if (tpa.y == 0) {  // leaf subdomain: exact term, never sampled
-          if (s == 0) {
-            acc += (double)((tpa.w - tpa.z > 1)
-                                ? leaf_exact<KID>(V, tpa.z, tpa.w, qx, qy, qz, kp)
-                                : fterm<KID>(s_cm1(a_ord), KID == KID_WINDING ? s_w1(a_ord) : w0,
-                                             qx, qy, qz, kp));
+      if (S == 1 && f1 - f0 == n1) {  // the common case: one sample per subdomain
+        for (int a_ord = 0; a_ord < n1; ++a_ord) {  // block-uniform
+          const int4 tpa = s_tp1(a_ord);
+          if (tpa.y == 0) {  // leaf subdomain: exact term, never sampled
+            acc += leaf_term(a_ord, tpa);
+            continue;
           }
-          const int take = min(S - s, f1 - f);
-          f += take;
-          continue;
+          const float rp_a = fdist(s_cm1(a_ord), qx, qy, qz) * id1;
+          sample(a_ord, 0, tpa, tpa.x - V.base2, a_ord * (kLut + 1), rp_a,
+                 key_fold(hq, (uint64_t)a_ord));
         }
-        const int k0 = tpa.x - V.base2, lut0 = a_ord * (kLut + 1);
-        const int count_a = tpa.w - tpa.z;
-        const float rp_a = fdist(s_cm1(a_ord), qx, qy, qz) * id1;
-        const uint2 hqv = s_hq(tid);
-        const uint64_t ha = key_fold(((uint64_t)hqv.y << 32) | hqv.x, (uint64_t)a_ord);
-        for (; s < S && f < f1; ++s, ++f) {  // block-uniform
-          const uint64_t hs = key_fold(ha, (uint64_t)s);
-          const uint64_t ki = key_fold(hs, 0), kr = key_fold(hs, 1);
-          // index draw, exactly as _core.py:166-169 (uniform_draw(ki, 0))
-          const uint64_t x = mix64(ki + kGamma);
-          const double u0 = __ull2double_rn(x >> 11) * (1.0 / 9007199254740992.0);
-          int j = tpa.z + (int)__dmul_rn(u0, (double)count_a);
-          if (j >= tpa.w) j = tpa.w - 1;
-          // level-1 step from shared memory (the swap at `a` is in the dense
-          // part): bucket table, then a short forward scan over child begins
-          const int bkt = (int)(x >> (64 - kLutBits));
-          int c = s_lut(lut0 + bkt);
-          const int ce = s_lut(lut0 + bkt + 1);
-          while (c < ce && (s_b2(k0 + c + 1) & 0x7fffffff) <= j) ++c;
-          const int lo = k0 + c;
-          const float rc = fdist(s_cm2(lo), qx, qy, qz) * id2;
-          const float p = rr_fast_t<RR>(rp_a, rc);
-          // (lanes past the end of the query set sample too; results dropped)
-          if (survive<RR>(p, kr, 0)) {  // descends: queue the walk start
-            const int pos = atomicAdd(&s_count(0), 1);
-            atomicAdd(&s_hist(lo), 1);
-            qa[pos] = make_int4(tid | (steps << 8), a_ord, lo, j);
-            qk[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
-            ++steps;
+      } else {
+        int a_ord = f0 / S, s = f0 - a_ord * S;
+        for (int f = f0; f < f1; ++a_ord, s = 0) {  // block-uniform
+          const int4 tpa = s_tp1(a_ord);
+          if (tpa.y == 0) {  // leaf subdomain: exact term, never sampled
+            if (s == 0) acc += leaf_term(a_ord, tpa);
+            const int take = min(S - s, f1 - f);
+            f += take;
+            continue;
           }
+          const int k0 = tpa.x - V.base2, lut0 = a_ord * (kLut + 1);
+          const float rp_a = fdist(s_cm1(a_ord), qx, qy, qz) * id1;
+          const uint64_t ha = key_fold(hq, (uint64_t)a_ord);
+          for (; s < S && f < f1; ++s, ++f) sample(a_ord, s, tpa, k0, lut0, rp_a, ha);
         }
       }
       __syncthreads();
