@@ -190,9 +190,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FSB_BENCH_BACKEND=gloo lets several ranks share one GPU (tests of the
+    # multi-rank path on a single-GPU box); the default is NCCL, one GPU per rank
+    backend = os.environ.get("FSB_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2506_02219_b200 as fs
     from paper_2506_02219_b200 import _device as dev
@@ -294,11 +302,14 @@ def run_ours(args):
     kern_ms = ev_a.elapsed_time(ev_b) / reps
     visited_mean = float(vis.double().mean().item())
 
+    # ---- e2e through the public API from pinned host memory (all ranks)
+    e2e = _e2e(args, fs, src, kern, qs, tree4, cfg_s1, world, rank)
+
     out = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic (reference mesh generators, fixed seeds)", "config": config_block(),
-           "clocks": clk.summary()}
+           "clocks": clk.summary(), "e2e": e2e}
     if launches_per_step is not None:
         out["gpu_launches"] = launches_per_step * args.steps
 
@@ -378,9 +389,7 @@ def run_ours(args):
             "pipe_floor_note": (f"FMA/ALU/MUFU pipe floor incl. {samples_q} samples/query x 6 "
                                 f"splitmix64 mixes; cycles/query fma {fma_cyc:.1f} alu "
                                 f"{alu_cyc:.1f} mufu {mufu_cyc:.1f}")}
-        # ---- e2e through the public API from pinned host memory
-        out["e2e"] = _e2e(args, fs, src, kern, qs, tree4, cfg_s1, world)
-        if args.cpu_baseline:
+        if args.cpu_baseline and world == 1:
             out["cpu_baseline"] = _cpu_baseline(tree4, src, qs, kern, args)
     if world > 1:
         dist.barrier()
@@ -413,26 +422,40 @@ def _level_sizes(tree):
     return int(len(lvl1)), int(sum(int(cc[a]) for a in lvl1)), int(np.count_nonzero(cc[lvl1]))
 
 
-def _e2e(args, fs, src, kern, qs, tree, cfg, world):
+def _e2e(args, fs, src, kern, qs, tree, cfg, world, rank):
+    """The step through the public API (evaluate_field, host numpy in / out): every
+    rank evaluates its own slab (query_offset = rank * n) from pinned host memory,
+    timed between barriers, max over ranks."""
     import torch
-    host = torch.empty((len(qs), 3), dtype=torch.float64, pin_memory=True)
+    import torch.distributed as dist
+    n = len(qs)
+    host = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
     host.numpy()[:] = qs.positions
     qset = fs.QuerySet.__new__(fs.QuerySet)
     object.__setattr__(qset, "positions", host.numpy())
-    for _ in range(max(1, args.warmup)):
-        fs.evaluate_field(cfg, src, kern, qset, tree=tree)
+    off = rank * n
+    r = None
+    for _ in range(max(2, args.warmup)):  # like the timed loop: the previous result stays alive
+        r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r = fs.evaluate_field(cfg, src, kern, qset, tree=tree)
+        r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / args.steps
-    n = len(qs)
+    if world > 1:
+        tt = torch.tensor([dt], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
     out_bytes = sum(a.nbytes for a in (r.values, r.raw, r.flagged, r.visited_nodes, r.path_steps,
                                        r.path_count))
-    return {"value": n / dt, "unit": "queries/s", "h2d_bytes_per_step": int(host.numel() * 8),
-            "d2h_bytes_per_step": int(out_bytes), "ms_per_step": dt * 1e3,
-            "api": "paper_2506_02219_b200.evaluate_field (host numpy in/out)", "n_gpus": 1}
+    return {"value": world * n / dt, "unit": "queries/s",
+            "h2d_bytes_per_step": int(host.numel() * 8), "d2h_bytes_per_step": int(out_bytes),
+            "ms_per_step": dt * 1e3,
+            "api": "paper_2506_02219_b200.evaluate_field (host numpy in/out, pipelined slabs)",
+            "n_gpus": world, "bytes_note": "per rank per step"}
 
 
 def _cpu_baseline(tree, src, qs, kern, args):

@@ -13,6 +13,8 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -184,6 +186,30 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
                        path_steps=steps, path_count=count, method=config.method)
 
 
+_PINNED: list = []  # (tensor, ndarray) pinned output blocks, reused once unreferenced
+
+
+def _pinned_block(nbytes: int):
+    """(data pointer, uint8 ndarray) of a pinned host block of >= nbytes.  Result
+    arrays are numpy views of the block's ndarray (their .base chain ends there),
+    so a block whose ndarray has no other referrers is free and is reused:
+    page-locking fresh memory costs tens of ms per call."""
+    torch = dev.torch()
+    for t, mem in _PINNED:
+        # referrers: the pool tuple, the loop variable, getrefcount's argument
+        if sys.getrefcount(mem) <= 3 and mem.nbytes >= nbytes:
+            return t.data_ptr(), mem
+    t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    entry = (t, t.numpy())
+    _PINNED.append(entry)
+    if len(_PINNED) > 4:  # keep the pool small: drop the oldest free block
+        for i, (_, old) in enumerate(_PINNED[:-1]):
+            if sys.getrefcount(old) <= 3:
+                del _PINNED[i]
+                break
+    return entry[0].data_ptr(), entry[1]
+
+
 def _pipeline_chunks(n: int) -> int:
     """Slabs for the host pipeline: enough to overlap PCIe with compute, each
     slab still several waves of 148 SMs x 4 blocks x 256 queries."""
@@ -192,13 +218,15 @@ def _pipeline_chunks(n: int) -> int:
 
 def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSpec,
                    queries: QuerySet, tree: Octree | None = None, *,
-                   chunks: int | None = None) -> FieldResult:
+                   chunks: int | None = None, query_offset: int = 0) -> FieldResult:
     """estimators.py:260-323: dispatch on config.method, then post-transform.
 
     Host queries in, host results out, through fsb_evaluate_field_host: slabs
     of queries are copied, evaluated and copied back on overlapping streams
     (results are independent of the slab count).  Outputs land in pinned host
-    buffers returned as numpy arrays.
+    buffers returned as numpy arrays.  ``query_offset`` (an extension; the
+    reference keys on 0..n-1) keys the stochastic RNG on global query indices so
+    a slab of a larger query set evaluates exactly as inside the whole set.
     """
     _check_channels(sources, kernel)
     L = _lib.lib()
@@ -214,7 +242,7 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
     args.n_samples = int(config.samples_per_subdomain)
     args.rr_mode = _RR_CODES[config.rr_mode]
     args.seed = int(config.seed) & ((1 << 64) - 1)
-    args.query_offset = 0
+    args.query_offset = int(query_offset)
     args.smooth = 1 if kernel.kind == "smooth_exp" else 0
     args.query_order = 1
     h = None
@@ -231,15 +259,19 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
             raise ValueError("prebuilt tree branching factor does not match config")
         h = C.c_void_p(tree._device_tree().handle)
     # one pinned block for all outputs: 5 x 8-byte columns, then the flags
-    block = torch.empty(41 * n + 8, dtype=torch.uint8, pin_memory=True)
-    base = block.data_ptr()
+    _t0 = time.perf_counter()
+    base, mem = _pinned_block(41 * n + 8)
+    _t1 = time.perf_counter()
     ptrs = [base + 8 * n * k for k in range(5)] + [base + 40 * n]
     _lib.check(L.fsb_evaluate_field_host(
         h, C.byref(args), q.ctypes.data_as(C.c_void_p), n,
         C.c_void_p(ptrs[0]), C.c_void_p(ptrs[1]), C.c_void_p(ptrs[5]), C.c_void_p(ptrs[2]),
         C.c_void_p(ptrs[3]), C.c_void_p(ptrs[4]),
         int(chunks if chunks is not None else _pipeline_chunks(n)), _sp()))
-    mem = block.numpy()
+    _t2 = time.perf_counter()
+    if os.environ.get("FSB_PY_TRACE"):
+        print(f"evaluate_field: pinned alloc {(_t1 - _t0) * 1e3:.3f} ms, "
+              f"host pipeline {(_t2 - _t1) * 1e3:.3f} ms", file=sys.stderr)
     cols = [mem[8 * n * k: 8 * n * (k + 1)] for k in range(5)]
     return FieldResult(values=cols[0].view(np.float64), raw=cols[1].view(np.float64),
                        flagged=mem[40 * n: 41 * n].view(bool),

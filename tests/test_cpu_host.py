@@ -50,6 +50,33 @@ def test_abi_validates_arguments_without_touching_the_gpu():
     assert L.fsb_tree_free(None) == 0
 
 
+def test_host_pipeline_validates_arguments_without_touching_the_gpu():
+    """fsb_evaluate_field_host rejects bad arguments (status 1) before any CUDA call."""
+    import ctypes as C
+    import numpy as np
+    L = _lib.load()
+    q = np.zeros((4, 3))
+    vals = np.zeros(4)
+    qp, vp = q.ctypes.data_as(C.c_void_p), vals.ctypes.data_as(C.c_void_p)
+
+    def call(tree=None, values=vp, **kw):
+        a = _lib.EvalArgs(method=3, kid=0, alpha=200.0, dfloor=1e-12, precision=1, beta=2.0,
+                          n_samples=1, rr_mode=0, seed=1, query_offset=0, smooth=0,
+                          query_order=1)
+        for k, v in kw.items():
+            setattr(a, k, v)
+        return L.fsb_evaluate_field_host(tree, C.byref(a), qp, 4, values, None, None, None,
+                                         None, None, 2, None)
+
+    assert call(values=None) == 1 and b"null argument" in L.fsb_last_error()
+    assert call(method=9) == 1 and b"unknown method" in L.fsb_last_error()
+    assert call(kid=5) == 1
+    assert call() == 1 and b"null tree" in L.fsb_last_error()          # stochastic needs a tree
+    assert call(method=0) == 1 and b"brute force" in L.fsb_last_error()  # needs device sources
+    assert call(method=1, beta=0.0) == 1
+    assert call(rr_mode=7) == 1
+
+
 def test_no_cpu_fallback():
     import torch
     if torch.cuda.is_available():
