@@ -149,6 +149,15 @@ int fsb_evaluate_field_host(fsb_tree *tree, const fsb_eval_args *args, const dou
                             int64_t *visited, int64_t *path_steps, int64_t *path_count,
                             int chunks, void *stream);
 
+/* error_stats + rmse (reference bench.py:66-95) on device arrays: absolute errors
+ * |estimates - reference| over entries flagged in neither flags_a nor flags_b
+ * (uint8, either may be NULL).  out4 = {mean, lower median, max, rmse}, count =
+ * entries kept (0 -> all four NaN).  Deterministic (fixed reduction order).
+ * Synchronises. */
+int fsb_error_stats(const double *estimates, const double *reference, const uint8_t *flags_a,
+                    const uint8_t *flags_b, int64_t n, double *out4, int64_t *count,
+                    void *stream);
+
 #ifdef __cplusplus
 }
 #endif

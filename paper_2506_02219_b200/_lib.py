@@ -55,6 +55,7 @@ SIGNATURES = {
     "fsb_post_transform": [_P, _I, _I64, _I, _D, _P, _P, _P, _P],
     "fsb_evaluate_field_host": [_P, C.POINTER(EvalArgs), _P, _I64, _P, _P, _P, _P, _P, _P, _I,
                                 _P],
+    "fsb_error_stats": [_P, _P, _P, _P, _I64, _P, C.POINTER(_I64), _P],
 }
 _RESTYPES = {"fsb_last_error": C.c_char_p}
 

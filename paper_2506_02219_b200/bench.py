@@ -1,0 +1,281 @@
+"""Error/efficiency measurement harness (reference ``fastsum.bench``, bench.py:1-272).
+
+Same names, records and file formats as the reference; the metric path runs on
+the device: the brute-force oracle field is computed by the CUDA brute force
+and cached on input content (bench.py:102-132), error statistics (mean, lower
+median, max, RMSE over unflagged entries, bench.py:66-95) are reduced by
+``fsb_error_stats`` next to the fields, and sweeps evaluate through
+``evaluate_field_device`` so only scalars cross PCIe.  Work is reported as mean
+visited nodes per query; wall times are device-synchronised host timings, as
+in the reference (informational only).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+import hashlib
+import json
+import time
+
+import numpy as np
+
+from . import _device as dev
+from . import _lib
+from .estimators import DeviceField, FieldResult, evaluate_field_device
+from .octree import build_tree
+from .types import EstimatorConfig, KernelSpec, QuerySet, SourceSet
+
+__all__ = [
+    "ErrorStats",
+    "SweepRecord",
+    "error_stats",
+    "rmse",
+    "run_sweep",
+    "convergence_slope",
+    "rr_ablation",
+    "classify_inside_outside",
+    "write_sweep_csv",
+    "write_sweep_json",
+    "oracle_field",
+    "oracle_cache_stats",
+]
+
+SWEEP_CSV_HEADER = ("method,parameter,wall_time_s,mean_abs,median_abs,max_abs,"
+                    "rmse,visited_nodes_mean,flagged_count")
+
+
+@dataclass(frozen=True)
+class ErrorStats:
+    mean_abs: float
+    median_abs: float
+    max_abs: float
+    count: int
+
+
+@dataclass(frozen=True)
+class SweepRecord:
+    method: str
+    parameter: float
+    wall_time_s: float
+    stats: ErrorStats
+    rmse: float
+    visited_nodes_mean: float
+    flagged_count: int
+    mean_path_length: float = 0.0
+
+
+def _as_device(x, dtype):
+    torch = dev.torch()
+    if isinstance(x, torch.Tensor):
+        t = x if x.is_cuda else x.to(dev.device())
+        return t.to(dtype).contiguous()
+    return dev.to_device(np.asarray(x), dtype)
+
+
+def _device_stats(estimates, reference, flags_a=None, flags_b=None):
+    """(mean_abs, lower median, max_abs, rmse, count) on the device."""
+    torch = dev.torch()
+    L = _lib.lib()
+    est = _as_device(estimates, torch.float64).reshape(-1)
+    ref = _as_device(reference, torch.float64).reshape(-1)
+    if est.shape != ref.shape:
+        raise ValueError("estimates and reference lengths differ")
+    if est.numel() == 0:
+        raise ValueError("empty inputs")
+    fl = [None if f is None else _as_device(f, torch.uint8).reshape(-1)
+          for f in (flags_a, flags_b)]
+    out = (C.c_double * 4)()
+    cnt = C.c_int64()
+    _lib.check(L.fsb_error_stats(C.c_void_p(dev.ptr(est)), C.c_void_p(dev.ptr(ref)),
+                                 C.c_void_p(dev.ptr(fl[0])), C.c_void_p(dev.ptr(fl[1])),
+                                 est.numel(), out, C.byref(cnt), C.c_void_p(dev.stream_ptr())))
+    return out[0], out[1], out[2], out[3], int(cnt.value)
+
+
+def error_stats(estimates, reference, flags=None) -> ErrorStats:
+    """bench.py:66-84: absolute-error statistics; flagged entries are excluded.
+
+    The median is the lower median for even counts.  Inputs may be numpy
+    arrays or CUDA tensors (reduced in place, no host copy)."""
+    mean, med, mx, _, cnt = _device_stats(estimates, reference, flags)
+    if cnt == 0:
+        return ErrorStats(np.nan, np.nan, np.nan, 0)
+    return ErrorStats(float(mean), float(med), float(mx), cnt)
+
+
+def rmse(estimates, reference, flags=None) -> float:
+    """bench.py:87-92."""
+    return float(_device_stats(estimates, reference, flags)[3])
+
+
+# ---------------------------------------------------------------------------
+# Oracle caching (bench.py:98-136)
+# ---------------------------------------------------------------------------
+
+_ORACLE_CACHE: dict[str, DeviceField] = {}
+_CACHE_STATS = {"hits": 0, "misses": 0}
+
+
+def content_hash(sources: SourceSet, kernel: KernelSpec, queries: QuerySet) -> str:
+    h = hashlib.sha256()
+    h.update(sources.positions.tobytes())
+    h.update(sources.masses.tobytes())
+    h.update(sources.weights.tobytes())
+    h.update(repr(kernel).encode())
+    h.update(queries.positions.tobytes())
+    return h.hexdigest()
+
+
+def _oracle_device(sources: SourceSet, kernel: KernelSpec, queries: QuerySet) -> DeviceField:
+    key = content_hash(sources, kernel, queries)
+    if key in _ORACLE_CACHE:
+        _CACHE_STATS["hits"] += 1
+        return _ORACLE_CACHE[key]
+    _CACHE_STATS["misses"] += 1
+    result = evaluate_field_device(EstimatorConfig("brute_force"), sources, kernel, queries)
+    _ORACLE_CACHE[key] = result
+    return result
+
+
+def oracle_field(sources: SourceSet, kernel: KernelSpec, queries: QuerySet) -> FieldResult:
+    """Brute-force reference field (FP64 parity brute force on the GPU), cached on
+    input content; the device copy stays cached for the sweeps."""
+    return _oracle_device(sources, kernel, queries).to_host()
+
+
+def oracle_cache_stats() -> dict[str, int]:
+    return dict(_CACHE_STATS)
+
+
+# ---------------------------------------------------------------------------
+# Sweeps (bench.py:139-222)
+# ---------------------------------------------------------------------------
+
+def _record_from_run(method: str, parameter: float, result: DeviceField, oracle: DeviceField,
+                     wall: float) -> SweepRecord:
+    mean, med, mx, r, cnt = _device_stats(result.values, oracle.values, result.flagged,
+                                          oracle.flagged)
+    stats = ErrorStats(np.nan, np.nan, np.nan, 0) if cnt == 0 else ErrorStats(
+        float(mean), float(med), float(mx), cnt)
+    paths = int(result.path_count.sum().item())
+    mean_len = (float(result.path_steps.sum().item()) / paths) if paths else 0.0
+    return SweepRecord(
+        method=method, parameter=float(parameter), wall_time_s=wall, stats=stats,
+        rmse=float(r) if cnt else float("nan"),
+        visited_nodes_mean=float(result.visited.double().mean().item()),
+        flagged_count=int(result.flagged.sum().item()), mean_path_length=mean_len)
+
+
+def _timed(cfg, sources, kernel, q, tree):
+    torch = dev.torch()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    result = evaluate_field_device(cfg, sources, kernel, q, tree)
+    torch.cuda.synchronize()
+    return result, time.perf_counter() - t0
+
+
+def run_sweep(sources: SourceSet, kernel: KernelSpec, method: str, parameters,
+              queries: QuerySet, seed: int = 0, branching_per_dim: int | None = None,
+              rr_mode: str = "paper_ratio") -> list[SweepRecord]:
+    """One record per parameter value (beta for barnes_hut, S for stochastic).
+
+    The oracle field is computed once and cached; the tree is built once per
+    sweep and excluded from the timed section; a discarded warm-up run precedes
+    the first timed evaluation (bench.py:152-188)."""
+    if method not in ("barnes_hut", "stochastic"):
+        raise ValueError("sweeps support barnes_hut and stochastic methods")
+    oracle = _oracle_device(sources, kernel, queries)
+
+    def config(p) -> EstimatorConfig:
+        if method == "barnes_hut":
+            return EstimatorConfig("barnes_hut", beta=float(p), seed=seed,
+                                   branching_per_dim=branching_per_dim)
+        return EstimatorConfig("stochastic", samples_per_subdomain=int(p), rr_mode=rr_mode,
+                               seed=seed, branching_per_dim=branching_per_dim)
+
+    tree = build_tree(sources, config(parameters[0]).resolved_branching)
+    q = dev.to_device(queries.positions)
+    evaluate_field_device(config(parameters[0]), sources, kernel, q, tree)  # warm-up
+    records = []
+    for p in parameters:
+        result, wall = _timed(config(p), sources, kernel, q, tree)
+        records.append(_record_from_run(method, float(p), result, oracle, wall))
+    return records
+
+
+def convergence_slope(records: list[SweepRecord]) -> float:
+    """bench.py:191-203: least-squares slope of log(RMSE) vs log(S)."""
+    if len(records) < 4:
+        raise ValueError("need at least 4 sweep points")
+    s = np.array([r.parameter for r in records], dtype=np.float64)
+    if len(np.unique(s)) != len(s):
+        raise ValueError("sweep parameters must be distinct")
+    e = np.array([r.rmse for r in records], dtype=np.float64)
+    if np.any(e <= 0):
+        raise ValueError("RMSE must be positive to take logs")
+    slope, _ = np.polyfit(np.log(s), np.log(e), 1)
+    return float(slope)
+
+
+def rr_ablation(sources: SourceSet, kernel: KernelSpec, queries: QuerySet,
+                samples_per_subdomain: int = 1, seed: int = 0,
+                branching_per_dim: int | None = None) -> dict[str, SweepRecord]:
+    """bench.py:206-222: error and work for the three roulette modes on one scene."""
+    oracle = _oracle_device(sources, kernel, queries)
+    cfg0 = EstimatorConfig("stochastic", branching_per_dim=branching_per_dim)
+    tree = build_tree(sources, cfg0.resolved_branching)
+    q = dev.to_device(queries.positions)
+    out = {}
+    for mode in ("paper_ratio", "fixed_half", "disabled"):
+        cfg = EstimatorConfig("stochastic", samples_per_subdomain=samples_per_subdomain,
+                              rr_mode=mode, seed=seed, branching_per_dim=branching_per_dim)
+        evaluate_field_device(cfg, sources, kernel, q, tree)  # warm-up
+        result, wall = _timed(cfg, sources, kernel, q, tree)
+        out[mode] = _record_from_run("stochastic", samples_per_subdomain, result, oracle, wall)
+    return out
+
+
+def classify_inside_outside(estimates, reference, threshold: float = 0.5):
+    """bench.py:225-237: threshold winding estimates; accuracy vs the oracle."""
+    est = np.asarray(estimates, dtype=np.float64)
+    ref = np.asarray(reference, dtype=np.float64)
+    if est.shape != ref.shape:
+        raise ValueError("estimates and reference lengths differ")
+    labels = est > threshold
+    oracle_labels = ref > threshold
+    return labels, float(np.mean(labels == oracle_labels))
+
+
+# ---------------------------------------------------------------------------
+# Writers (bench.py:244-272): byte-identical formats
+# ---------------------------------------------------------------------------
+
+def write_sweep_csv(records: list[SweepRecord], path) -> None:
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(SWEEP_CSV_HEADER + "\n")
+        for r in records:
+            fh.write(f"{r.method},{r.parameter:.17g},{r.wall_time_s:.6g},"
+                     f"{r.stats.mean_abs:.17g},{r.stats.median_abs:.17g},"
+                     f"{r.stats.max_abs:.17g},{r.rmse:.17g},"
+                     f"{r.visited_nodes_mean:.17g},{r.flagged_count}\n")
+
+
+def write_sweep_json(path, config_echo: dict, sources: SourceSet, kernel: KernelSpec,
+                     queries: QuerySet, records: list[SweepRecord]) -> None:
+    payload = {
+        "config": config_echo,
+        "input_hash": content_hash(sources, kernel, queries),
+        "records": [
+            {"method": r.method, "parameter": r.parameter, "wall_time_s": r.wall_time_s,
+             "mean_abs": r.stats.mean_abs, "median_abs": r.stats.median_abs,
+             "max_abs": r.stats.max_abs, "rmse": r.rmse,
+             "visited_nodes_mean": r.visited_nodes_mean, "flagged_count": r.flagged_count,
+             "mean_path_length": r.mean_path_length}
+            for r in records
+        ],
+    }
+    with open(path, "w", encoding="utf-8") as fh:
+        json.dump(payload, fh, indent=2, sort_keys=True)
+        fh.write("\n")
