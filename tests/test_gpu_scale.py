@@ -175,3 +175,29 @@ def test_host_pipeline_slab_invariance(fs, method):
                           "path_count"):
                     np.testing.assert_array_equal(getattr(r, k), getattr(ref, k),
                                                   err_msg=f"{method} {kind} {prec} {chunks} {k}")
+
+
+def test_fast_fp32_estimator_unbiased_over_seeds(fs):
+    """Acceptance check 3 on the production kernel: the FP32 stochastic estimator's
+    mean over 128 seeds converges to brute force (|mean - truth| <= 4 SE for >= 95 %
+    of the queries), and its error shrinks like seeds^-1/2."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 16, seed=23))
+    rng = np.random.default_rng(6)
+    q = rng.uniform(-0.6, 0.6, (2048, 3))
+    kern = fs.KernelSpec("coulomb")
+    truth = fs.evaluate_field(fs.EstimatorConfig("brute_force"), s, kern, fs.QuerySet(q)).values
+    t = fs.build_tree(s, 4)
+    qd = dev.to_device(q)
+    runs = np.stack([evaluate_field_device(fs.EstimatorConfig("stochastic", seed=k,
+                                                              precision="f32"),
+                                           s, kern, qd, t).values.cpu().numpy()
+                     for k in range(128)])
+    mean = runs.mean(axis=0)
+    se = runs.std(axis=0, ddof=1) / np.sqrt(len(runs))
+    ok = np.abs(mean - truth) <= 4 * se + 1e-6 * np.abs(truth)
+    assert ok.mean() >= 0.95, ok.mean()
+    e1 = np.median(np.abs(runs[0] - truth))
+    e128 = np.median(np.abs(mean - truth))
+    assert e128 < e1 / 4  # ~sqrt(128) = 11x in expectation
