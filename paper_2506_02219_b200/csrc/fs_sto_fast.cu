@@ -52,6 +52,13 @@ struct FastView {
 
 
 
+// two consecutive 16-byte records with one 256-bit read-only load (p 32-byte aligned)
+__device__ __forceinline__ void ld_pair(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+
 template <int KID>
 __device__ __forceinline__ float fterm(float4 c, float2 w, float qx, float qy, float qz,
                                        const KParams& kp) {
@@ -473,9 +480,17 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
               // the sampled point's path gives the child's rank: only the
               // aggregates are read (one 16-byte load per child)
               le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
+              // 32-byte loads of child pairs (one request per two children)
+              if (tp.x & 1) {
+                ks0 += fterm<KID>(V.cm[tp.x], KID == KID_WINDING ? V.m12[tp.x] : w0, qq.x, qq.y,
+                                  qq.z, kp);
+                c = 1;
+              }
               for (; c + 3 < tp.y; c += 4) {
                 const int r = tp.x + c;
-                const float4 c0 = V.cm[r], c1 = V.cm[r + 1], c2 = V.cm[r + 2], c3 = V.cm[r + 3];
+                float4 c0, c1, c2, c3;
+                ld_pair(V.cm + r, c0, c1);
+                ld_pair(V.cm + r + 2, c2, c3);
                 ks0 += fterm<KID>(c0, KID == KID_WINDING ? V.m12[r] : w0, qq.x, qq.y, qq.z, kp);
                 ks1 += fterm<KID>(c1, KID == KID_WINDING ? V.m12[r + 1] : w0, qq.x, qq.y, qq.z,
                                   kp);
