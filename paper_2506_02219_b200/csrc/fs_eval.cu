@@ -687,6 +687,13 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
   FS_TRY(ensure_bh(t, f64, s));
   FS_TRY(ensure_lo(t, f64, s));  // packed points for multi-point leaves
   KParams kp = make_kp(alpha, dfloor);
+  const char* split_env = std::getenv("FSB_BH_SPLIT");
+  if (!f64 && !(split_env && split_env[0] == '0')) {  // load-balanced FP32 BH
+    bool done = false;
+    FS_TRY(barnes_hut_split(t, kid, alpha, dfloor, q, n, qperm, beta, (float*)out, visited, s,
+                            &done));
+    if (done) return 0;
+  }
   Scratch work;  // chunk counter of the persistent warps
   FS_TRY(work.alloc(sizeof(unsigned int), s));
   FS_CK(cudaMemsetAsync(work.p, 0, sizeof(unsigned int), s));

@@ -28,6 +28,9 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
                     const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                     int64_t qoff, float* out, int64_t* visited, int64_t* path_steps,
                     int64_t* path_count, cudaStream_t s, bool* used);
+int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
+                     const int32_t* qperm, double beta, float* out, int64_t* visited,
+                     cudaStream_t s, bool* done);
 int post_transform(const void* raw, int raw_f32, int64_t n, int smooth, double alpha,
                    double* values, double* raw64, uint8_t* flagged, cudaStream_t s);
 }  // namespace fsb

@@ -5,6 +5,7 @@
 //   * BH (preorder, skip links):      32 B FP32 / 64 B FP64 per node
 //   * level order (children contiguous): geo + mass + topo (int4) per node
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <vector>
 #include <cuda_runtime.h>
@@ -46,6 +47,7 @@ struct FsTree {
   float4 *pts32a = nullptr, *pts32b = nullptr;  // permuted points {x,y,z,m0}, {m1,m2,0,0}
   double4 *pts64a = nullptr, *pts64b = nullptr;
   int root_kids = 0;  // child_count[0]
+  std::atomic<int> bh_items_hint{0};  // load-balanced BH: items emitted by the last call
 
   // fast FP32 stochastic / BH path (built by ensure_fast)
   static constexpr int kMaxLevels = 256;

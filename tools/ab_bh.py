@@ -15,7 +15,8 @@ src, qs, kern = bench.workload()
 q = dev.to_device(qs.positions)
 t2 = fs.build_tree(src, 2)
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for beta in (2.0, 6.0, 8.0):
+betas = [float(x) for x in os.environ.get("BETAS", "2,6,8").split(",")]
+for beta in betas:
     cfg = fs.EstimatorConfig("barnes_hut", beta=beta, precision="f32")
     r = evaluate_field_device(cfg, src, kern, q, t2)
     torch.cuda.synchronize()
@@ -24,4 +25,5 @@ for beta in (2.0, 6.0, 8.0):
         r = evaluate_field_device(cfg, src, kern, q, t2)
     b.record()
     torch.cuda.synchronize()
-    print(f"BH beta={beta}: {a.elapsed_time(b) / 3:.3f} ms, checksum {r.values.sum().item():.9e}")
+    print(f"BH beta={beta}: {a.elapsed_time(b) / 3:.3f} ms, checksum {r.values.sum().item():.9e}, "
+          f"visited {r.visited.double().sum().item():.6e}", flush=True)
