@@ -218,7 +218,7 @@ static int bh_split_launch(FsTree* t, const double* q, int64_t n, const int32_t*
   C.n = n;
   C.nn = (uint32_t)t->n;
   C.beta = (float)beta;
-  C.split_after = env_int("FSB_BH_SPLIT_AFTER", 512);
+  C.split_after = env_int("FSB_BH_SPLIT_AFTER", 192);
   C.min_split = env_int("FSB_BH_MIN_SPLIT", 32);
   C.cap = cap;
   Scratch items, ctrs, cnt, atop, stop, aitem, sitem, work;
