@@ -97,3 +97,66 @@ def test_f32_outputs_match_reference_dtype_contract(fs):
     assert r.raw.dtype == np.float64
     assert np.array_equal(r.raw, r.raw.astype(np.float32).astype(np.float64))
     assert r.path_count.min() >= 1 and r.flagged.dtype == bool
+
+
+# scenes that exercise the fast kernel's special paths: multi-point leaves at
+# level 1/2 (manydup, duplicates), deep clusters, lattices on cell boundaries
+FAST_CASES = [
+    (dict(kind="manydup", m=3000, seed=4, posmass=True), "coulomb"),
+    (dict(kind="duplicates", m=5000, seed=5, posmass=True), "smooth_exp"),
+    (dict(kind="cluster", m=4000, seed=6, posmass=True), "coulomb"),
+    (dict(kind="lattice", m=4096, seed=7), "coulomb"),
+    (dict(kind="mesh_sphere_winding", m=6000, seed=8, channels=3), "winding_dipole"),
+    (dict(kind="mesh_torus", m=20000, seed=9), "coulomb"),
+]
+
+
+@pytest.mark.parametrize("case,kind", FAST_CASES, ids=lambda c: c if isinstance(c, str) else c["kind"])
+@pytest.mark.parametrize("rr", ["paper_ratio", "fixed_half", "disabled"])
+def test_fast_kernel_tracks_fp64_parity_kernel(fs, case, kind, rr):
+    """k_sto_fast (FP32) against k_stochastic (FP64, bitwise with the reference) on
+    the same draws: every special path (leaf subdomains, multi-point leaves in
+    the dense part and in walks, chunked drains at large S, all roulette modes)
+    agrees per query to FP32 rounding except where a roulette decision at the
+    FP32/FP64 boundary flips; counters agree exactly when no decision flips."""
+    s = scenes.build_sources(case)
+    kern = fs.KernelSpec(kind)
+    rng = np.random.default_rng(11)
+    q = fs.QuerySet(rng.uniform(-1.2, 1.2, (1500, 3)))
+    t = fs.build_tree(s, 4)
+    for S in (1, 3, 60):
+        a = fs.evaluate_field(fs.EstimatorConfig("stochastic", samples_per_subdomain=S, rr_mode=rr,
+                                                 seed=13, precision="f32"), s, kern, q, tree=t)
+        b = fs.evaluate_field(fs.EstimatorConfig("stochastic", samples_per_subdomain=S, rr_mode=rr,
+                                                 seed=13, precision="f64"), s, kern, q, tree=t)
+        fin = np.isfinite(b.raw)
+        close = _rel(a.raw[fin], b.raw[fin]) <= 1e-4
+        assert close.mean() >= 0.97, (S, close.mean())
+        same = (a.path_steps == b.path_steps) & (a.visited_nodes == b.visited_nodes)
+        assert same.mean() >= 0.97, (S, same.mean())
+        np.testing.assert_array_equal(a.path_count, b.path_count)
+        if rr == "disabled":  # no roulette: no decision can flip
+            assert same.all()
+
+
+def test_load_balanced_bh_matches_warp_coherent_bh(fs, monkeypatch):
+    """The work-splitting FP32 BH sums exactly the warp-coherent kernel's node set
+    (visited counts identical) and agrees to FP64-association rounding, at betas
+    where long union walks do split."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 17, seed=31))
+    rng = np.random.default_rng(12)
+    q = fs.QuerySet(rng.uniform(-0.5, 0.5, (50000, 3)))
+    kern = fs.KernelSpec("coulomb")
+    t = fs.build_tree(s, 2)
+    for beta in (4.0, 10.0):
+        cfg = fs.EstimatorConfig("barnes_hut", beta=beta, precision="f32")
+        monkeypatch.setenv("FSB_BH_SPLIT_AFTER", "64")  # force many splits
+        a = evaluate_field_device(cfg, s, kern, q, t).to_host()
+        monkeypatch.setenv("FSB_BH_SPLIT", "0")
+        b = evaluate_field_device(cfg, s, kern, q, t).to_host()
+        monkeypatch.delenv("FSB_BH_SPLIT")
+        np.testing.assert_array_equal(a.visited_nodes, b.visited_nodes)
+        assert np.max(np.abs(a.raw - b.raw) / np.abs(b.raw)) <= 1e-6
+        c = evaluate_field_device(cfg, s, kern, q, t).to_host()  # deterministic
+        np.testing.assert_array_equal(a.raw, c.raw)
