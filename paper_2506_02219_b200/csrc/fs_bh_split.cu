@@ -19,6 +19,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -321,7 +322,7 @@ int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const doub
   // item queue sized from the last call's count on this tree (a size hint only,
   // so concurrent calls on other streams stay safe); an overflow retries bigger
   const int64_t nchunks = (n + 31) / 32;
-  int64_t cap = std::max<int64_t>(std::max<int64_t>(4096, nchunks / 4),
+  int64_t cap = std::max<int64_t>(std::max<int64_t>(4096, 32 * nchunks),
                                   (int64_t)t->bh_items_hint.load() * 5 / 4);
   if (const char* e = std::getenv("FSB_BH_ITEM_CAP")) cap = std::atoll(e);
   for (int attempt = 0; attempt < 4; ++attempt) {
@@ -333,11 +334,14 @@ int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const doub
       default: rc = bh_split_launch<2>(t, q, n, qperm, beta, kp, out, visited, sms, (int)cap, s, done, &emitted); break;
     }
     if (rc) return rc;
+    if (std::getenv("FSB_BH_DEBUG"))
+      fprintf(stderr, "bh split: cap %lld, emitted %u, %s\n", (long long)cap, emitted,
+              *done ? "ok" : "overflow");
     if (*done) {
       t->bh_items_hint.store((int)std::min<int64_t>(emitted, 1 << 30));
       return 0;
     }
-    cap = std::min<int64_t>(cap * 4, (int64_t)1 << 24);
+    cap = std::min<int64_t>(std::max<int64_t>(cap * 4, (int64_t)emitted * 2), (int64_t)1 << 25);
   }
   return 0;  // not done: the caller falls back to the warp-coherent kernel
 }
