@@ -99,9 +99,13 @@ __device__ __forceinline__ float draw24(uint64_t key, uint64_t ctr) {
   return (float)(uint32_t)(x >> 40) * (1.0f / 16777216.0f);
 }
 
-constexpr int kBlock = 256;  // threads (= queries) per tile
+#ifndef FSB_TILE
+#define FSB_TILE 256
+#endif
+constexpr int kBlock = FSB_TILE;  // threads (= queries) per tile
+constexpr int kOwnerBits = kBlock <= 256 ? 8 : (kBlock <= 512 ? 9 : 10);
 #ifndef FSB_STO_MINB
-#define FSB_STO_MINB 4  // resident blocks per SM the register budget is sized for
+#define FSB_STO_MINB (1024 / FSB_TILE)  // resident blocks per SM the register budget is sized for
 #endif
 #ifndef FSB_QCAP_MAX
 #define FSB_QCAP_MAX 9216  // max queued walk starts per block (one drain per tile on C4)
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
       if (survive<RR>(p, kr, 0)) {  // descends: queue the walk start
         const int pos = atomicAdd(&s_count(0), 1);
         atomicAdd(&s_hist(lo), 1);
-        qa[pos] = make_int4(tid | (steps << 8), a_ord, lo, j);
+        qa[pos] = make_int4(tid | (steps << kOwnerBits), a_ord, lo, j);
         qk[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
         ++steps;
       }
@@ -445,9 +449,9 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
             if (!act && idx < cnt) {
               const int4 wa = sa[idx];  // consecutive lanes, consecutive records
               const uint2 wk = sk[idx];
-              owner = wa.x & 0xff;
+              owner = wa.x & ((1 << kOwnerBits) - 1);
               const int wa_ord = wa.y, k = wa.z;
-              slot = wa.x >> 8;  // creation index among the owner's walks
+              slot = wa.x >> kOwnerBits;  // creation index among the owner's walks
               jj = wa.w;
               path = V.path[jj];
               kr = ((uint64_t)wk.y << 32) | wk.x;
