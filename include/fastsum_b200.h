@@ -158,6 +158,25 @@ int fsb_error_stats(const double *estimates, const double *reference, const uint
                     const uint8_t *flags_b, int64_t n, double *out4, int64_t *count,
                     void *stream);
 
+/* Input generation on the device, byte-identical to the reference generators
+ * fed by numpy default_rng(seed) (PCG64; each thread jumps the stream to its own
+ * draw).  state4 = {state_hi, state_lo, inc_hi, inc_lo} of the generator before
+ * the first draw.  sample_mesh_surface (scene_io.py:112-148): cdf (num_faces,)
+ * = cumsum(areas / total) / last (numpy choice's table), tri (num_faces, 3, 3)
+ * vertex coordinates per face, normals (num_faces, 3) for winding_dipole masses
+ * (else NULL: every mass = `mass`); outputs positions (m,3), masses (m,1|3),
+ * weights (m,).  make_queries (scene_io.py:188-212): kind 0 grid3d (axes ax0,
+ * ax1, ax2; r1 = len(ax1), r2 = len(ax2)), 1 slice plane (su = ax0, sv = ax1,
+ * r1 = len(su); geo = origin, u_axis, v_axis), 2 random uniform (geo = low,
+ * high; state4 of default_rng(spec.seed)); out (n,3).  Stream-ordered. */
+int fsb_sample_mesh_surface(const double *cdf, int64_t num_faces, const double *tri,
+                            const double *normals, int64_t m, const uint64_t *state4,
+                            double w_each, double mass, double *positions, double *masses,
+                            double *weights, void *stream);
+int fsb_make_queries(int kind, int64_t n, const double *ax0, const double *ax1,
+                     const double *ax2, int64_t r1, int64_t r2, const double *geo,
+                     const uint64_t *state4, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,8 @@ import numpy as np
 from .types import QuerySet, SourceSet
 
 __all__ = ["triangle_areas_normals", "icosphere", "torus", "sample_mesh_surface",
-           "GridSpec", "make_queries", "rotate_x"]
+           "GridSpec", "make_queries", "rotate_x", "sample_mesh_surface_device",
+           "make_queries_device"]
 
 
 def triangle_areas_normals(vertices, faces):
@@ -196,3 +197,91 @@ def make_queries(spec: GridSpec) -> QuerySet:
         return QuerySet(pts)
     rng = np.random.default_rng(spec.seed)
     return QuerySet(rng.uniform(lo, hi, size=(spec.count, 3)))
+
+
+# --------------------------------------------------------------------------
+# Device generators (csrc/fs_scene.cu): the same bytes, drawn on the GPU
+# --------------------------------------------------------------------------
+
+def _pcg_state4(seed):
+    """{state_hi, state_lo, inc_hi, inc_lo} of numpy default_rng(seed) before its first draw."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    m64 = (1 << 64) - 1
+    s, inc = int(st["state"]), int(st["inc"])
+    return np.array([s >> 64, s & m64, inc >> 64, inc & m64], dtype=np.uint64)
+
+
+def sample_mesh_surface_device(vertices, faces, num_samples: int, seed: int,
+                               kernel_kind: str = "coulomb", point_mass: float | None = None):
+    """sample_mesh_surface drawn on the GPU: (positions (M,3), masses (M,c), weights (M,))
+    as CUDA tensors, byte-identical to the host generator (scene_io.py:112-148)."""
+    import ctypes as C
+    from . import _device as dev
+    from . import _lib
+    torch = dev.torch()
+    if num_samples < 1:
+        raise ValueError("num_samples must be >= 1")
+    areas, normals = triangle_areas_normals(vertices, faces)
+    total_area = float(areas.sum())
+    if total_area <= 0:
+        raise ValueError("mesh has zero surface area")
+    p = areas / total_area
+    cdf = p.cumsum()  # numpy Generator.choice's table (replace=True, p given)
+    cdf /= cdf[-1]
+    f = np.asarray(faces, dtype=np.int64)
+    tri = np.asarray(vertices, dtype=np.float64)[f]  # (F, 3, 3)
+    w_each = total_area / num_samples
+    wind = kernel_kind == "winding_dipole"
+    mass = (1.0 / num_samples) if point_mass is None else float(point_mass)
+    d_cdf, d_tri = dev.to_device(cdf), dev.to_device(np.ascontiguousarray(tri))
+    d_nrm = dev.to_device(np.ascontiguousarray(normals)) if wind else None
+    pos = dev.empty((num_samples, 3), torch.float64)
+    ms = dev.empty((num_samples, 3) if wind else (num_samples, 1), torch.float64)
+    w = dev.empty(num_samples, torch.float64)
+    st = _pcg_state4(seed)
+    _lib.check(_lib.lib().fsb_sample_mesh_surface(
+        C.c_void_p(dev.ptr(d_cdf)), len(cdf), C.c_void_p(dev.ptr(d_tri)),
+        C.c_void_p(dev.ptr(d_nrm)), num_samples, st.ctypes.data_as(C.c_void_p), w_each, mass,
+        C.c_void_p(dev.ptr(pos)), C.c_void_p(dev.ptr(ms)), C.c_void_p(dev.ptr(w)),
+        C.c_void_p(dev.stream_ptr())))
+    dev.torch().cuda.current_stream().synchronize()  # the host arrays above are freed on return
+    return pos, ms, w
+
+
+def make_queries_device(spec: GridSpec):
+    """make_queries on the GPU: an (N,3) float64 CUDA tensor with the host bytes."""
+    import ctypes as C
+    from . import _device as dev
+    from . import _lib
+    torch = dev.torch()
+    lo, hi = np.asarray(spec.bounds[0], dtype=np.float64), np.asarray(spec.bounds[1], dtype=np.float64)
+    L = _lib.lib()
+    st = None
+    if spec.kind == "grid3d":
+        res = tuple(spec.resolution)
+        rx, ry, rz = (res * 3)[:3] if len(res) == 1 else res[:3]
+        axes = [_axis(lo[0], hi[0], rx), _axis(lo[1], hi[1], ry), _axis(lo[2], hi[2], rz)]
+        kind, n, r1, r2, geo = 0, rx * ry * rz, ry, rz, None
+    elif spec.kind == "slice_plane":
+        res = tuple(spec.resolution)
+        nu, nv = (res * 2)[:2] if len(res) == 1 else res[:2]
+        axes = [_axis(-spec.extent, spec.extent, nu), _axis(-spec.extent, spec.extent, nv),
+                None]
+        kind, n, r1, r2 = 1, nu * nv, nu, 0
+        geo = np.concatenate([np.asarray(spec.origin, dtype=np.float64),
+                              np.asarray(spec.u_axis, dtype=np.float64),
+                              np.asarray(spec.v_axis, dtype=np.float64)])
+    else:
+        axes = [None, None, None]
+        kind, n, r1, r2 = 2, spec.count, 0, 0
+        geo = np.concatenate([lo, hi])
+        st = _pcg_state4(spec.seed)
+    d_axes = [None if a is None else dev.to_device(a) for a in axes]
+    d_geo = None if geo is None else dev.to_device(geo)
+    out = dev.empty((n, 3), torch.float64)
+    _lib.check(L.fsb_make_queries(
+        kind, n, *(C.c_void_p(dev.ptr(a)) for a in d_axes), r1, r2, C.c_void_p(dev.ptr(d_geo)),
+        None if st is None else st.ctypes.data_as(C.c_void_p), C.c_void_p(dev.ptr(out)),
+        C.c_void_p(dev.stream_ptr())))
+    torch.cuda.current_stream().synchronize()
+    return out
