@@ -88,6 +88,19 @@ int fsb_stochastic_batch(fsb_tree *tree, int kid, double alpha, double dfloor, i
                          void *out, int64_t *visited, int64_t *path_steps,
                          int64_t *path_count, void *stream);
 
+/* The paper's GPU recipe, not the reference's: queries are
+ * evaluated in `order` (a permutation; the paper shuffles the grid) and each
+ * group of 2^group_log2 consecutive positions shares one RNG stream keyed on
+ * (seed, (position + query_offset) >> group_log2, subdomain, sample), so a warp
+ * follows one sampled path.  Unbiased per query; group_log2 = 0 is
+ * fsb_stochastic_batch with an evaluation order. */
+int fsb_stochastic_batch_shared(fsb_tree *tree, int kid, double alpha, double dfloor,
+                                int precision, const double *queries, int64_t n,
+                                const int32_t *order, int64_t n_samples, int rr_mode,
+                                uint64_t seed, int64_t query_offset, int group_log2, void *out,
+                                int64_t *visited, int64_t *path_steps, int64_t *path_count,
+                                void *stream);
+
 /* stochastic_moments_batch(*core, kid, alpha, dfloor, queries, n_reps, rr_mode, seed,
  * mean_out, var_out) -- _core.py:270-336.  FP64 only. */
 int fsb_stochastic_moments_batch(fsb_tree *tree, int kid, double alpha, double dfloor,
@@ -103,6 +116,10 @@ int fsb_telescoping_batch(fsb_tree *tree, int kid, double alpha, double dfloor, 
 /* Spatially coherent evaluation order for queries (3-D Morton code over the
  * query bounding box, stable): perm_out (n,) int32.  Result-invariant (F8). */
 int fsb_query_order(const double *queries, int64_t n, int32_t *perm_out, void *stream);
+
+/* Seeded pseudo-random permutation of 0..n-1 (the evaluation order of the
+ * paper's RNG-sharing groups): perm_out (n,) int32. */
+int fsb_shuffle_order(int64_t n, uint64_t seed, int32_t *perm_out, void *stream);
 
 /* post_transform (kernels.py:110-122) applied to raw sums: smooth != 0 gives
  * -ln(raw)/alpha with (+inf, flagged) for raw <= 0; otherwise values = raw.

@@ -49,9 +49,12 @@ SIGNATURES = {
     "fsb_barnes_hut_batch": [_P, _I, _D, _D, _I, _P, _I64, _P, _D, _P, _P, _P],
     "fsb_stochastic_batch": [_P, _I, _D, _D, _I, _P, _I64, _P, _I64, _I, C.c_uint64, _I64, _P,
                              _P, _P, _P, _P],
+    "fsb_stochastic_batch_shared": [_P, _I, _D, _D, _I, _P, _I64, _P, _I64, _I, C.c_uint64, _I64,
+                                    _I, _P, _P, _P, _P, _P],
     "fsb_stochastic_moments_batch": [_P, _I, _D, _D, _P, _I64, _I64, _I, C.c_uint64, _P, _P, _P],
     "fsb_telescoping_batch": [_P, _I, _D, _D, _I, _P, _I64, _P, _P, _P],
     "fsb_query_order": [_P, _I64, _P, _P],
+    "fsb_shuffle_order": [_I64, C.c_uint64, _P, _P],
     "fsb_post_transform": [_P, _I, _I64, _I, _D, _P, _P, _P, _P],
     "fsb_evaluate_field_host": [_P, C.POINTER(EvalArgs), _P, _I64, _P, _P, _P, _P, _P, _P, _I,
                                 _P],

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/fastsum_b200.h"
+#include "fs_common.cuh"
 #include "fs_eval.h"
 #include "fs_internal.h"
 
@@ -115,6 +116,31 @@ int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s) {
   FS_TRY(tmp.alloc(tb, s));
   FS_CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, code.as<uint32_t>(), code2.as<uint32_t>(),
                                         idx.as<int32_t>(), perm, (int)n, 0, 30, s));
+  return 0;
+}
+// seeded pseudo-random evaluation order (the paper shuffles the query grid so that
+// RNG-sharing groups are spatially scattered)
+__global__ void k_shuffle_keys(int64_t n, uint64_t seed, uint64_t* __restrict__ key,
+                               int32_t* __restrict__ idx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  key[i] = key_fold(mix64(seed + kGamma), (uint64_t)i);
+  idx[i] = (int32_t)i;
+}
+
+int shuffle_order(int64_t n, uint64_t seed, int32_t* perm, cudaStream_t s) {
+  if (n <= 0) return 0;
+  Scratch k0, k1, idx, tmp;
+  FS_TRY(k0.alloc(8 * n, s));
+  FS_TRY(k1.alloc(8 * n, s));
+  FS_TRY(idx.alloc(4 * n, s));
+  k_shuffle_keys<<<grid_for(n, 256), 256, 0, s>>>(n, seed, k0.as<uint64_t>(), idx.as<int32_t>());
+  size_t tb = 0;
+  FS_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.as<uint64_t>(), k1.as<uint64_t>(),
+                                        idx.as<int32_t>(), perm, (int)n, 0, 64, s));
+  FS_TRY(tmp.alloc(tb, s));
+  FS_CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k0.as<uint64_t>(), k1.as<uint64_t>(),
+                                        idx.as<int32_t>(), perm, (int)n, 0, 64, s));
   return 0;
 }
 }  // namespace fsb
@@ -284,6 +310,24 @@ int fsb_stochastic_batch(fsb_tree* tree, int kid, double alpha, double dfloor, i
                          path_count, S(stream));
 }
 
+int fsb_stochastic_batch_shared(fsb_tree* tree, int kid, double alpha, double dfloor,
+                                int precision, const double* queries, int64_t n,
+                                const int32_t* order, int64_t n_samples, int rr_mode,
+                                uint64_t seed, int64_t query_offset, int group_log2, void* out,
+                                int64_t* visited, int64_t* path_steps, int64_t* path_count,
+                                void* stream) {
+  ABI_TREE(tree);
+  if (int rc = check_common(kid, precision, n)) return rc;
+  if (n_samples < 1 || n_samples > (1LL << 30) || rr_mode < 0 || rr_mode > 2 || group_log2 < 0 ||
+      group_log2 > 20) {
+    set_error("bad samples_per_subdomain / rr mode / group size");
+    return 1;
+  }
+  return fsb::stochastic(tree->t, kid, alpha, dfloor, precision == 0, queries, n, order,
+                         (int)n_samples, rr_mode, seed, query_offset, out, visited, path_steps,
+                         path_count, S(stream), group_log2);
+}
+
 int fsb_stochastic_moments_batch(fsb_tree* tree, int kid, double alpha, double dfloor,
                                  const double* queries, int64_t n, int64_t n_reps, int rr_mode,
                                  uint64_t seed, double* mean_out, double* var_out, void* stream) {
@@ -312,6 +356,14 @@ int fsb_query_order(const double* queries, int64_t n, int32_t* perm_out, void* s
     return 1;
   }
   return fsb::query_order(queries, n, perm_out, S(stream));
+}
+
+int fsb_shuffle_order(int64_t n, uint64_t seed, int32_t* perm_out, void* stream) {
+  if (n < 0 || (n > 0 && !perm_out)) {
+    set_error("bad shuffle arguments");
+    return 1;
+  }
+  return fsb::shuffle_order(n, seed, perm_out, S(stream));
 }
 
 int fsb_post_transform(const void* raw, int raw_is_f32, int64_t n, int smooth, double alpha,

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(128) k_stochastic(LoTree<KID, F64> T, int root
                                                     const double* __restrict__ q, int64_t n,
                                                     const int32_t* __restrict__ qperm, int S,
                                                     int rr_mode, uint64_t seed, int64_t qoff,
-                                                    KParams kp,
+                                                    int share, KParams kp,
                                                     typename Prec<F64>::Out* __restrict__ out,
                                                     int64_t* __restrict__ visited,
                                                     int64_t* __restrict__ path_steps,
@@ -279,7 +279,8 @@ __global__ void __launch_bounds__(128) k_stochastic(LoTree<KID, F64> T, int root
     acc = T.node_term(0, qx, qy, qz, kp);
     seen = 1;
   } else {
-    uint64_t hq = key_fold(mix64(seed + kGamma), (uint64_t)(qi + qoff));
+    uint64_t hq = key_fold(mix64(seed + kGamma),
+                           share ? (uint64_t)((t + qoff) >> share) : (uint64_t)(qi + qoff));
     for (int a_ord = 0; a_ord < root_kids; ++a_ord) {
       int a = 1 + a_ord;  // level order: the root's children follow the root
       ++seen;
@@ -725,12 +726,13 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
 int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                int64_t query_offset, void* out, int64_t* visited, int64_t* path_steps,
-               int64_t* path_count, cudaStream_t s) {
+               int64_t* path_count, cudaStream_t s, int share) {
   if (n <= 0) return 0;
   if (!f64 && !std::getenv("FSB_DISABLE_FAST")) {
     bool used = false;
     FS_TRY(stochastic_fast(t, kid, alpha, dfloor, q, n, qperm, n_samples, rr_mode, seed,
-                           query_offset, (float*)out, visited, path_steps, path_count, s, &used));
+                           query_offset, share, (float*)out, visited, path_steps, path_count, s,
+                           &used));
     if (used) return 0;
   }
   FS_TRY(ensure_lo(t, f64, s));
@@ -740,7 +742,7 @@ int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
     constexpr bool F64 = decltype(P)::value;
     k_stochastic<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(
         lo_view<KID, F64>(t), t->root_kids, q, n, qperm, n_samples, rr_mode, seed, query_offset,
-        kp, (typename Prec<F64>::Out*)out, visited, path_steps, path_count);
+        share, kp, (typename Prec<F64>::Out*)out, visited, path_steps, path_count);
   });
 }
 

@@ -15,10 +15,12 @@ int brute_force_f32_acc64(int kid, double alpha, double dfloor, const double* pt
 int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, double beta, void* out, int64_t* visited,
                cudaStream_t s);
+// share = 0: per-query RNG streams (reference); share = k > 0: the 2^k consecutive
+// positions of the processing order (qperm) share one stream (paper recipe)
 int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                int64_t query_offset, void* out, int64_t* visited, int64_t* path_steps,
-               int64_t* path_count, cudaStream_t s);
+               int64_t* path_count, cudaStream_t s, int share = 0);
 int stochastic_moments(FsTree* t, int kid, double alpha, double dfloor, const double* q,
                        int64_t n, int64_t n_reps, int rr_mode, uint64_t seed, double* mean_out,
                        double* var_out, cudaStream_t s);
@@ -26,7 +28,7 @@ int telescoping(FsTree* t, int kid, double alpha, double dfloor, bool f64, const
                 int64_t n, void* out, int64_t* visited, cudaStream_t s);
 int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                     const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
-                    int64_t qoff, float* out, int64_t* visited, int64_t* path_steps,
+                    int64_t qoff, int share, float* out, int64_t* visited, int64_t* path_steps,
                     int64_t* path_count, cudaStream_t s, bool* used);
 int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                      const int32_t* qperm, double beta, float* out, int64_t* visited,

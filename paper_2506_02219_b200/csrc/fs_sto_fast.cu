@@ -158,7 +158,7 @@ constexpr int kLutBits = FSB_LUT_BITS, kLut = 1 << kLutBits;
 template <int KID, int RR>
 __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     k_sto_fast(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
-               const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff,
+               const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff, int share,
                KParams kp, float* __restrict__ res_g, unsigned char* __restrict__ queues,
                unsigned int* __restrict__ tile_ctr, float* __restrict__ out, int64_t* __restrict__ visited,
                int64_t* __restrict__ path_steps, int64_t* __restrict__ path_count) {
@@ -275,7 +275,10 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
       qy = live ? (float)q[3 * qi + 1] : 0.f;
       qz = live ? (float)q[3 * qi + 2] : 0.f;
       s_q(tid) = make_float4(qx, qy, qz, 0.f);
-      const uint64_t hq = key_fold(hseed, (uint64_t)(qi + qoff));
+      // stream key: the query's global index (reference), or with warp sharing
+      // the index of its group of 2^share consecutive positions (paper recipe)
+      const uint64_t hq = key_fold(
+          hseed, share ? (uint64_t)((t + qoff) >> share) : (uint64_t)(qi + qoff));
       s_hq(tid) = make_uint2((uint32_t)hq, (uint32_t)(hq >> 32));
     }
 
@@ -606,7 +609,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 // returns 1 if the fast path does not apply (caller falls back), 0 on launch
 int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                     const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
-                    int64_t qoff, float* out, int64_t* visited, int64_t* path_steps,
+                    int64_t qoff, int share, float* out, int64_t* visited, int64_t* path_steps,
                     int64_t* path_count, cudaStream_t s, bool* used) {
   *used = false;
   if (t->root_kids <= 0 || t->num_levels > kFastMaxLevels) return 0;
@@ -668,7 +671,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     FS_TRY(queues.alloc((size_t)grid * 2 * V.qcap * kWalkBytes, s));
     FS_TRY(ctr.alloc(sizeof(unsigned int), s));
     FS_CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned int), s));
-    kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, seed, qoff, kp,
+    kern<<<(unsigned)grid, B, smem, s>>>(V, q, n, qperm, n_samples, seed, qoff, share, kp,
                                          res.as<float>(), queues.as<unsigned char>(),
                                          ctr.as<unsigned int>(), out, visited, path_steps,
                                          path_count);

@@ -170,6 +170,17 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
         elif config.method == "telescoping_exhaustive":
             _lib.check(L.fsb_telescoping_batch(h, kid, alpha, dfloor, prec, _vp(q), n, _vp(raw),
                                                _vp(visited), _sp()))
+        elif getattr(config, "rng_sharing", "query") == "warp":
+            # the paper's recipe: shuffled evaluation order, 32 consecutive
+            # positions share one stream (fsb_stochastic_batch_shared)
+            order = dev.empty(n, torch.int32)
+            _lib.check(L.fsb_shuffle_order(n, int(config.seed) & ((1 << 64) - 1), _vp(order),
+                                           _sp()))
+            _lib.check(L.fsb_stochastic_batch_shared(
+                h, kid, alpha, dfloor, prec, _vp(q), n, _vp(order),
+                int(config.samples_per_subdomain), _RR_CODES[config.rr_mode],
+                int(config.seed) & ((1 << 64) - 1), int(query_offset), 5, _vp(raw),
+                _vp(visited), _vp(steps), _vp(count), _sp()))
         else:
             _lib.check(L.fsb_stochastic_batch(
                 h, kid, alpha, dfloor, prec, _vp(q), n, _vp(perm),
@@ -229,6 +240,9 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
     a slab of a larger query set evaluates exactly as inside the whole set.
     """
     _check_channels(sources, kernel)
+    if config.method == "stochastic" and getattr(config, "rng_sharing", "query") == "warp":
+        return evaluate_field_device(config, sources, kernel, queries, tree,
+                                     query_offset=query_offset).to_host()
     L = _lib.lib()
     torch = dev.torch()
     q = np.ascontiguousarray(queries.positions, dtype=np.float64)

@@ -201,3 +201,32 @@ def test_fast_fp32_estimator_unbiased_over_seeds(fs):
     e1 = np.median(np.abs(runs[0] - truth))
     e128 = np.median(np.abs(mean - truth))
     assert e128 < e1 / 4  # ~sqrt(128) = 11x in expectation
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_paper_warp_shared_rng_is_unbiased_and_deterministic(fs, prec):
+    """rng_sharing="warp" (the paper's GPU recipe): shuffled order,
+    32 queries per stream.  Deterministic for a seed, unbiased over seeds, and its
+    median error matches the reference-stream estimator's."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 15, seed=29))
+    rng = np.random.default_rng(8)
+    q = rng.uniform(-0.6, 0.6, (4096, 3))
+    kern = fs.KernelSpec("coulomb")
+    truth = fs.evaluate_field(fs.EstimatorConfig("brute_force"), s, kern, fs.QuerySet(q)).values
+    t = fs.build_tree(s, 4)
+    qd = dev.to_device(q)
+
+    def run(seed, sharing):
+        cfg = fs.EstimatorConfig("stochastic", seed=seed, precision=prec, rng_sharing=sharing)
+        return evaluate_field_device(cfg, s, kern, qd, t).values.cpu().numpy()
+
+    np.testing.assert_array_equal(run(3, "warp"), run(3, "warp"))
+    runs = np.stack([run(k, "warp") for k in range(64)])
+    se = runs.std(axis=0, ddof=1) / np.sqrt(len(runs))
+    ok = np.abs(runs.mean(axis=0) - truth) <= 4 * se + 1e-6 * np.abs(truth)
+    assert ok.mean() >= 0.95, ok.mean()
+    e_warp = np.median([np.median(np.abs(r - truth)) for r in runs[:16]])
+    e_ref = np.median([np.median(np.abs(run(k, "query") - truth)) for k in range(16)])
+    assert abs(e_warp - e_ref) <= 0.1 * e_ref
