@@ -19,11 +19,13 @@
 //    are uniform splits, octree.py:225), the roulette.
 //  * Deeper steps (~1/3 of samples descend below level 2) would leave most
 //    lanes idle if walked in place.  Descending samples are queued (24 B walk
-//    starts per block in global memory, L2-resident) and served after the
-//    sampling loop by lanes that refill independently from the queue and
-//    carry each walk to completion.  A finished walk stores its residual in
-//    its (a, s) slot and owners fold their slots in (a, s) order, so a query's
-//    value never depends on which lane served its walks or when.
+//    starts per block in global memory, L2-resident), counting-sorted by
+//    level-2 node, and served after the sampling loop by lanes that refill
+//    independently from the queue and carry each walk to completion (the
+//    child holding the sampled point comes from its per-point path of
+//    sibling ranks).  A finished walk stores its residual in its owner's
+//    creation-ordered slot and owners fold their slots in that ((a, s))
+//    order, so a query's value never depends on which lane served its walks.
 //  * FP32 terms and residuals, FP64 accumulation across chunks/subdomains.
 #include <algorithm>
 
@@ -85,12 +87,6 @@ __device__ __forceinline__ float fdist(float4 c, float qx, float qy, float qz) {
   float dx = qx - c.x, dy = qy - c.y, dz = qz - c.z;
   float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
   return d2 * rsqrt_ftz(fmaxf(d2, 1e-30f));
-}
-
-__device__ __forceinline__ float rr_fast(float rp, float rc, int mode) {
-  if (mode == 1) return 0.5f;
-  if (mode == 2) return 1.0f;
-  return fminf(fmaxf(rp, 1.0f) * rcp_ftz(fmaxf(rc, 1e-12f)), 1.0f);
 }
 
 // roulette uniform from the top 24 bits of the same splitmix draw
