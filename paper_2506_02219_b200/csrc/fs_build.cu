@@ -379,9 +379,13 @@ __global__ void k_aggregate(int64_t r0, int64_t r1, const int32_t* __restrict__ 
 
 // ------------------------------------------------------------ host helpers
 template <class T>
-static int dalloc(T** p, int64_t count) {
+// tree arrays come from the stream-ordered pool (retained across builds, see
+// retain_pool_memory): a C4 tree is ~1 GB in ~40 arrays, and cudaMalloc would
+// map (and cudaFree synchronise) every one of them on every build
+static int dalloc(T** p, int64_t count, cudaStream_t s) {
   size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(count, 1);
-  FS_CK(cudaMalloc((void**)p, bytes));
+  retain_pool_memory();
+  FS_CK(cudaMallocAsync((void**)p, bytes, s));
   return 0;
 }
 
@@ -442,7 +446,8 @@ int level_order(FsTree* t, const int32_t* nb, const int32_t* nd, int max_dep,
   FS_CK(cudaMemcpyAsync(&lastkey, lkey_s.as<uint64_t>() + (n - 1), 8, cudaMemcpyDeviceToHost, s));
   FS_CK(cudaStreamSynchronize(s));
   int nl = (int)(lastkey >> 32) + 1;
-  FS_CK(cudaMalloc((void**)lstart_dev, sizeof(int64_t) * (nl + 1)));
+  retain_pool_memory();
+  FS_CK(cudaMallocAsync((void**)lstart_dev, sizeof(int64_t) * (nl + 1), s));
   k_level_starts<<<grid_for(n, B), B, 0, s>>>(lkey_s.as<uint64_t>(), n, *lstart_dev);
   k_invert<<<grid_for(n, B), B, 0, s>>>(t->lo2pre, n, t->pre2lo);
   t->level_off.assign(nl + 1, n);
@@ -457,29 +462,29 @@ int level_order(FsTree* t, const int32_t* nb, const int32_t* nd, int max_dep,
   return 0;
 }
 
-static int alloc_export(FsTree* t) {
+static int alloc_export(FsTree* t, cudaStream_t s) {
   int64_t n = t->n, m = t->m;
   int c = t->c;
-  FS_TRY(dalloc(&t->bbox_min, 3 * n));
-  FS_TRY(dalloc(&t->bbox_max, 3 * n));
-  FS_TRY(dalloc(&t->diameter, n));
-  FS_TRY(dalloc(&t->agg_mass, (int64_t)c * n));
-  FS_TRY(dalloc(&t->agg_weight, n));
-  FS_TRY(dalloc(&t->com, 3 * n));
-  FS_TRY(dalloc(&t->child_start, n));
-  FS_TRY(dalloc(&t->child_count, n));
-  FS_TRY(dalloc(&t->child_index, n - 1));
-  FS_TRY(dalloc(&t->begin, n));
-  FS_TRY(dalloc(&t->end, n));
-  FS_TRY(dalloc(&t->depth, n));
-  FS_TRY(dalloc(&t->perm, m));
-  FS_TRY(dalloc(&t->points, 3 * m));
-  FS_TRY(dalloc(&t->masses, (int64_t)c * m));
-  FS_TRY(dalloc(&t->weights, m));
-  FS_TRY(dalloc(&t->lo2pre, n));
-  FS_TRY(dalloc(&t->pre2lo, n));
-  FS_TRY(dalloc(&t->skip, n));
-  FS_TRY(dalloc(&t->fc_lo, n));
+  FS_TRY(dalloc(&t->bbox_min, 3 * n, s));
+  FS_TRY(dalloc(&t->bbox_max, 3 * n, s));
+  FS_TRY(dalloc(&t->diameter, n, s));
+  FS_TRY(dalloc(&t->agg_mass, (int64_t)c * n, s));
+  FS_TRY(dalloc(&t->agg_weight, n, s));
+  FS_TRY(dalloc(&t->com, 3 * n, s));
+  FS_TRY(dalloc(&t->child_start, n, s));
+  FS_TRY(dalloc(&t->child_count, n, s));
+  FS_TRY(dalloc(&t->child_index, n - 1, s));
+  FS_TRY(dalloc(&t->begin, n, s));
+  FS_TRY(dalloc(&t->end, n, s));
+  FS_TRY(dalloc(&t->depth, n, s));
+  FS_TRY(dalloc(&t->perm, m, s));
+  FS_TRY(dalloc(&t->points, 3 * m, s));
+  FS_TRY(dalloc(&t->masses, (int64_t)c * m, s));
+  FS_TRY(dalloc(&t->weights, m, s));
+  FS_TRY(dalloc(&t->lo2pre, n, s));
+  FS_TRY(dalloc(&t->pre2lo, n, s));
+  FS_TRY(dalloc(&t->skip, n, s));
+  FS_TRY(dalloc(&t->fc_lo, n, s));
   t->owns_export = true;
   return 0;
 }
@@ -592,7 +597,7 @@ int build_tree(FsTree** out, const double* pos, const double* masses, const doub
   int64_t n = (int64_t)last_off + last_cnt;
   t->n = n;
   {
-    int rc = alloc_export(t);
+    int rc = alloc_export(t, s);
     if (rc) {
       free_tree(t);
       return rc;
@@ -640,7 +645,7 @@ int build_tree(FsTree** out, const double* pos, const double* masses, const doub
   int64_t rk = 0;
   FS_CK(cudaMemcpyAsync(&rk, t->child_count, 8, cudaMemcpyDeviceToHost, s));
   FS_CK(cudaStreamSynchronize(s));
-  FS_CK(cudaFree(lstart));
+  FS_CK(cudaFreeAsync(lstart, s));
   t->root_kids = (int)rk;
   *out = t;
   return 0;

@@ -9,8 +9,9 @@
 namespace fsb {
 
 template <class T>
-static int dalloc(T** p, int64_t count) {
-  FS_CK(cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<int64_t>(count, 1)));
+static int dalloc(T** p, int64_t count, cudaStream_t s) {  // stream-ordered pool (fs_build.cu)
+  retain_pool_memory();
+  FS_CK(cudaMallocAsync((void**)p, sizeof(T) * (size_t)std::max<int64_t>(count, 1), s));
   return 0;
 }
 
@@ -22,8 +23,11 @@ void free_tree(FsTree* t) {
                   t->fc_lo, t->bh32, t->bh64, t->lo_geo32, t->lo_mass32, t->lo_geo64,
                   t->lo_mass64, t->lo_topo, t->pts32a, t->pts32b, t->pts64a, t->pts64b,
                   t->lo_cm32, t->lo_m12_32, t->lo_begin, t->pt_path};
+  // the handle's owner may still have work queued on any stream: wait for the
+  // device once, then return every array to the pool
+  cudaDeviceSynchronize();
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
   delete t;
 }
 
@@ -87,7 +91,7 @@ int tree_from_arrays(FsTree** out, const double* diameter, const double* agg_mas
   int rc = 0;
   auto cp = [&](auto** dst, const auto* src, int64_t count) -> int {
     using T = std::remove_pointer_t<std::remove_reference_t<decltype(*dst)>>;
-    FS_TRY(dalloc(dst, count));
+    FS_TRY(dalloc(dst, count, s));
     if (count > 0)
       FS_CK(cudaMemcpyAsync(*dst, src, sizeof(T) * count, cudaMemcpyDeviceToDevice, s));
     return 0;
@@ -97,8 +101,8 @@ int tree_from_arrays(FsTree** out, const double* diameter, const double* agg_mas
       (rc = cp(&t->child_count, child_count, n)) ||
       (rc = cp(&t->child_index, child_index, n - 1)) || (rc = cp(&t->begin, begin, n)) ||
       (rc = cp(&t->end, end, n)) || (rc = cp(&t->points, points, 3 * m)) ||
-      (rc = cp(&t->masses, masses, m * c)) || (rc = dalloc(&t->lo2pre, n)) ||
-      (rc = dalloc(&t->pre2lo, n)) || (rc = dalloc(&t->skip, n)) || (rc = dalloc(&t->fc_lo, n))) {
+      (rc = cp(&t->masses, masses, m * c)) || (rc = dalloc(&t->lo2pre, n, s)) ||
+      (rc = dalloc(&t->pre2lo, n, s)) || (rc = dalloc(&t->skip, n, s)) || (rc = dalloc(&t->fc_lo, n, s))) {
     free_tree(t);
     return rc;
   }
@@ -125,7 +129,7 @@ int tree_from_arrays(FsTree** out, const double* diameter, const double* agg_mas
     free_tree(t);
     return rc;
   }
-  cudaFree(lstart);
+  cudaFreeAsync(lstart, s);
   k_fc_skip<<<grid_for(n, B), B, 0, s>>>(t->child_start, t->child_count, t->child_index, t->end,
                                          t->pre2lo, first_at.as<int32_t>(), n, m, t->fc_lo,
                                          t->skip);
@@ -176,12 +180,12 @@ __global__ void k_pack_bh(const double* __restrict__ com, const double* __restri
 int ensure_bh(FsTree* t, bool f64, cudaStream_t s) {
   const int B = 256;
   if (f64 && !t->bh64) {
-    FS_TRY(dalloc(&t->bh64, t->n));
+    FS_TRY(dalloc(&t->bh64, t->n, s));
     k_pack_bh<double, double4><<<grid_for(t->n, B), B, 0, s>>>(
         t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->skip, t->n, t->c,
         reinterpret_cast<double4*>(t->bh64), nullptr);
   } else if (!f64 && !t->bh32) {
-    FS_TRY(dalloc(&t->bh32, t->n));
+    FS_TRY(dalloc(&t->bh32, t->n, s));
     k_pack_bh<float, float4><<<grid_for(t->n, B), B, 0, s>>>(
         t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->skip, t->n, t->c,
         reinterpret_cast<float4*>(t->bh32), nullptr);
@@ -235,22 +239,22 @@ __global__ void k_pack_pts(const double* __restrict__ pts, const double* __restr
 
 int ensure_lo(FsTree* t, bool f64, cudaStream_t s) {
   const int B = 256;
-  if (!t->lo_topo) FS_TRY(dalloc(&t->lo_topo, t->n));
+  if (!t->lo_topo) FS_TRY(dalloc(&t->lo_topo, t->n, s));
   if (f64 && !t->lo_geo64) {
-    FS_TRY(dalloc(&t->lo_geo64, t->n));
-    FS_TRY(dalloc(&t->lo_mass64, t->n));
-    FS_TRY(dalloc(&t->pts64a, t->m));
-    FS_TRY(dalloc(&t->pts64b, t->m));
+    FS_TRY(dalloc(&t->lo_geo64, t->n, s));
+    FS_TRY(dalloc(&t->lo_mass64, t->n, s));
+    FS_TRY(dalloc(&t->pts64a, t->m, s));
+    FS_TRY(dalloc(&t->pts64b, t->m, s));
     k_pack_lo<double, double4><<<grid_for(t->n, B), B, 0, s>>>(
         t->lo2pre, t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->fc_lo,
         t->n, t->c, t->lo_geo64, t->lo_mass64, t->lo_topo);
     k_pack_pts<double, double4><<<grid_for(t->m, B), B, 0, s>>>(t->points, t->masses, t->m, t->c,
                                                                 t->pts64a, t->pts64b);
   } else if (!f64 && !t->lo_geo32) {
-    FS_TRY(dalloc(&t->lo_geo32, t->n));
-    FS_TRY(dalloc(&t->lo_mass32, t->n));
-    FS_TRY(dalloc(&t->pts32a, t->m));
-    FS_TRY(dalloc(&t->pts32b, t->m));
+    FS_TRY(dalloc(&t->lo_geo32, t->n, s));
+    FS_TRY(dalloc(&t->lo_mass32, t->n, s));
+    FS_TRY(dalloc(&t->pts32a, t->m, s));
+    FS_TRY(dalloc(&t->pts32b, t->m, s));
     k_pack_lo<float, float4><<<grid_for(t->n, B), B, 0, s>>>(
         t->lo2pre, t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->fc_lo,
         t->n, t->c, t->lo_geo32, t->lo_mass32, t->lo_topo);
@@ -330,7 +334,7 @@ int ensure_path(FsTree* t, cudaStream_t s) {
   FS_CK(cudaStreamSynchronize(s));
   int bits = 1;
   while ((1ll << bits) < kids) ++bits;
-  FS_TRY(dalloc(&t->pt_path, t->m));
+  FS_TRY(dalloc(&t->pt_path, t->m, s));
   t->path_bits = bits;
   t->path_levels = bits <= 16 ? 64 / bits : 0;
   k_point_path<<<grid_for(t->m, 256), 256, 0, s>>>(t->lo_topo, t->m, bits, t->path_levels,
@@ -342,9 +346,9 @@ int ensure_path(FsTree* t, cudaStream_t s) {
 int ensure_fast(FsTree* t, cudaStream_t s) {
   if (t->fast_ready) return 0;
   const int B = 256;
-  FS_TRY(dalloc(&t->lo_cm32, t->n));
-  FS_TRY(dalloc(&t->lo_begin, t->n));
-  if (t->c >= 3) FS_TRY(dalloc(&t->lo_m12_32, t->n));
+  FS_TRY(dalloc(&t->lo_cm32, t->n, s));
+  FS_TRY(dalloc(&t->lo_begin, t->n, s));
+  if (t->c >= 3) FS_TRY(dalloc(&t->lo_m12_32, t->n, s));
   k_pack_fast<<<grid_for(t->n, B), B, 0, s>>>(t->lo2pre, t->com, t->agg_mass, t->begin, t->n, t->c,
                                               t->lo_cm32, t->c >= 3 ? t->lo_m12_32 : nullptr,
                                               t->lo_begin);
