@@ -343,6 +343,13 @@ int ensure_path(FsTree* t, cudaStream_t s) {
   return 0;
 }
 
+__global__ void k_level_diam(const int64_t* __restrict__ start, int nl,
+                             const int32_t* __restrict__ lo2pre, const double* __restrict__ diam,
+                             double* __restrict__ out) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < nl) out[l] = diam[lo2pre[start[l]]];
+}
+
 int ensure_fast(FsTree* t, cudaStream_t s) {
   if (t->fast_ready) return 0;
   const int B = 256;
@@ -365,17 +372,22 @@ int ensure_fast(FsTree* t, cudaStream_t s) {
   }
   int res[2];
   FS_CK(cudaMemcpyAsync(res, fl.p, sizeof(res), cudaMemcpyDeviceToHost, s));
-  std::vector<int64_t> firsts(t->num_levels);
-  for (int l = 0; l < t->num_levels && l < FsTree::kMaxLevels; ++l) {
-    double dd = 0;
-    int32_t pre = 0;
-    FS_CK(cudaMemcpyAsync(&pre, t->lo2pre + t->level_off[l], 4, cudaMemcpyDeviceToHost, s));
-    FS_CK(cudaStreamSynchronize(s));
-    FS_CK(cudaMemcpyAsync(&dd, t->diameter + pre, 8, cudaMemcpyDeviceToHost, s));
-    FS_CK(cudaStreamSynchronize(s));
-    t->level_diam[l] = (float)dd;
+  // one diameter per level (the level's first node), gathered on the device
+  const int nl = std::min(t->num_levels, FsTree::kMaxLevels);
+  std::vector<int64_t> starts(t->level_off.begin(), t->level_off.begin() + nl);
+  std::vector<double> ldiam(std::max(nl, 1));
+  Scratch dstart, ddiam;
+  FS_TRY(dstart.alloc(sizeof(int64_t) * std::max(nl, 1), s));
+  FS_TRY(ddiam.alloc(sizeof(double) * std::max(nl, 1), s));
+  if (nl > 0) {
+    FS_CK(cudaMemcpyAsync(dstart.p, starts.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice,
+                          s));
+    k_level_diam<<<grid_for(nl, 64), 64, 0, s>>>(dstart.as<int64_t>(), nl, t->lo2pre,
+                                                 t->diameter, ddiam.as<double>());
+    FS_CK(cudaMemcpyAsync(ldiam.data(), ddiam.p, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
   }
   FS_CK(cudaStreamSynchronize(s));
+  for (int l = 0; l < nl; ++l) t->level_diam[l] = (float)ldiam[l];
   t->uniform_diam = res[0] == 0 && t->num_levels <= FsTree::kMaxLevels;
   t->first_multi_level = res[1];
   t->fast_ready = true;
