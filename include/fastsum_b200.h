@@ -93,7 +93,9 @@ int fsb_stochastic_batch(fsb_tree *tree, int kid, double alpha, double dfloor, i
  * group of 2^group_log2 consecutive positions shares one RNG stream keyed on
  * (seed, (position + query_offset) >> group_log2, subdomain, sample), so a warp
  * follows one sampled path.  Unbiased per query; group_log2 = 0 is
- * fsb_stochastic_batch with an evaluation order. */
+ * fsb_stochastic_batch with an evaluation order.  FP32 with group_log2 = 5 and
+ * query_offset % 32 == 0 runs the warp-uniform kernel (k_sto_warp); other
+ * cases run the per-query kernels with the group keys. */
 int fsb_stochastic_batch_shared(fsb_tree *tree, int kid, double alpha, double dfloor,
                                 int precision, const double *queries, int64_t n,
                                 const int32_t *order, int64_t n_samples, int rr_mode,
@@ -118,7 +120,8 @@ int fsb_telescoping_batch(fsb_tree *tree, int kid, double alpha, double dfloor, 
 int fsb_query_order(const double *queries, int64_t n, int32_t *perm_out, void *stream);
 
 /* Seeded pseudo-random permutation of 0..n-1 (the evaluation order of the
- * paper's RNG-sharing groups): perm_out (n,) int32. */
+ * paper's RNG-sharing groups): perm_out (n,) int32.  A 4-round Feistel network
+ * keyed on the seed, cycle-walked into [0, n); one kernel, no sort. */
 int fsb_shuffle_order(int64_t n, uint64_t seed, int32_t *perm_out, void *stream);
 
 /* post_transform (kernels.py:110-122) applied to raw sums: smooth != 0 gives

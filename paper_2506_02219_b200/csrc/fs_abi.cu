@@ -120,27 +120,41 @@ int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s) {
 }
 // seeded pseudo-random evaluation order (the paper shuffles the query grid so that
 // RNG-sharing groups are spatially scattered)
-__global__ void k_shuffle_keys(int64_t n, uint64_t seed, uint64_t* __restrict__ key,
-                               int32_t* __restrict__ idx) {
+// seeded permutation of [0, n): a 4-round balanced Feistel network on the
+// smallest 2^(2h) >= n domain, cycle-walked back into [0, n) (a bijection; on
+// average < 4 rounds of walking).  One pass, no sort.
+__device__ __forceinline__ uint64_t feistel4(uint64_t x, int hb, uint64_t k0, uint64_t k1,
+                                             uint64_t k2, uint64_t k3) {
+  const uint64_t mask = (1ull << hb) - 1ull;
+  uint64_t l = x >> hb, r = x & mask;
+  const uint64_t ks[4] = {k0, k1, k2, k3};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t f = mix64(ks[i] ^ r) & mask;
+    const uint64_t nl = r;
+    r = l ^ f;
+    l = nl;
+  }
+  return (l << hb) | r;
+}
+
+__global__ void k_shuffle(int64_t n, int hb, uint64_t k0, uint64_t k1, uint64_t k2, uint64_t k3,
+                          int32_t* __restrict__ perm) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  key[i] = key_fold(mix64(seed + kGamma), (uint64_t)i);
-  idx[i] = (int32_t)i;
+  uint64_t y = feistel4((uint64_t)i, hb, k0, k1, k2, k3);
+  while (y >= (uint64_t)n) y = feistel4(y, hb, k0, k1, k2, k3);
+  perm[i] = (int32_t)y;
 }
 
 int shuffle_order(int64_t n, uint64_t seed, int32_t* perm, cudaStream_t s) {
   if (n <= 0) return 0;
-  Scratch k0, k1, idx, tmp;
-  FS_TRY(k0.alloc(8 * n, s));
-  FS_TRY(k1.alloc(8 * n, s));
-  FS_TRY(idx.alloc(4 * n, s));
-  k_shuffle_keys<<<grid_for(n, 256), 256, 0, s>>>(n, seed, k0.as<uint64_t>(), idx.as<int32_t>());
-  size_t tb = 0;
-  FS_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.as<uint64_t>(), k1.as<uint64_t>(),
-                                        idx.as<int32_t>(), perm, (int)n, 0, 64, s));
-  FS_TRY(tmp.alloc(tb, s));
-  FS_CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k0.as<uint64_t>(), k1.as<uint64_t>(),
-                                        idx.as<int32_t>(), perm, (int)n, 0, 64, s));
+  int hb = 1;
+  while ((1ll << (2 * hb)) < n) ++hb;
+  const uint64_t h = key_fold(mix64(seed + kGamma), 0x73687566ull);  // "shuf"
+  k_shuffle<<<grid_for(n, 256), 256, 0, s>>>(n, hb, key_fold(h, 0), key_fold(h, 1),
+                                             key_fold(h, 2), key_fold(h, 3), perm);
+  FS_CK(cudaGetLastError());
   return 0;
 }
 }  // namespace fsb

@@ -28,6 +28,7 @@
 //    order, so a query's value never depends on which lane served its walks.
 //  * FP32 terms and residuals, FP64 accumulation across chunks/subdomains.
 #include <algorithm>
+#include <cstdlib>
 
 #include "fs_common.cuh"
 #include "fs_eval.h"
@@ -602,6 +603,349 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 #undef s_t2
 }
 
+// ================================================ warp-shared streams (paper)
+// The paper's GPU recipe: the 32 queries of a warp, taken
+// in a seeded shuffled order, share the index and roulette streams (key = the
+// group index (t + qoff) >> 5).  Same estimator per query as k_sto_fast with
+// share = 5, but the shared draws turn the walk into warp-uniform work:
+//  * sampling: lane L computes the (a, s) pair f0 + L (6 mixes once per warp
+//    instead of once per lane), and the per-level roulette uniforms of a walk
+//    in parallel (lane L holds the draw with counter L);
+//  * walks: every lane descends the same path (same sampled point), so child
+//    records are warp-broadcast loads and the control flow is uniform; each
+//    lane keeps its own roulette state (p depends on the query) and stops
+//    committing once its roulette fails; the walk ends when no lane is alive.
+//    No queue, no sort, no result slots: residuals accumulate in (a, s) order.
+constexpr int kWarpBlock = 256;
+#ifndef FSB_WARP_MINB
+#define FSB_WARP_MINB 4
+#endif
+#ifndef FSB_WARP_DENSE2
+#define FSB_WARP_DENSE2 1
+#endif
+#ifndef FSB_WARP_SERIAL
+#define FSB_WARP_SERIAL 1
+#endif
+
+template <int KID, int RR>
+__global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
+    k_sto_warp(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
+               const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff, KParams kp,
+               unsigned int* __restrict__ chunk_ctr, float* __restrict__ out,
+               int64_t* __restrict__ visited, int64_t* __restrict__ path_steps,
+               int64_t* __restrict__ path_count) {
+  // shared layout: 16 B s_cm1[n1] {com, m0}, s_tp1[n1] topology, s_cm2[n2];
+  // 8 B s_w1[n1], s_w2[n2] (winding), s_t2[n2] {first child | count << 25, points};
+  // 4 B s_b2[n2] begins; 2 B s_lut[n1][kLut + 1]
+  const int n1 = V.n1, n2 = V.n2;
+  // Coulomb: level-2 records also as packed pairs {x0,x1,y0,y1}, {z0,z1,-m0,-m1}
+  constexpr bool kPack = KID == KID_COULOMB && FSB_WARP_DENSE2;
+  const int np2 = kPack ? (n2 + 1) / 2 : 0;
+  const int o_cm1 = 0, o_tp1 = n1, o_cm2 = 2 * n1, o_p2 = 2 * n1 + n2;
+  const int o_w1 = 2 * (2 * n1 + n2 + 2 * np2), o_w2 = o_w1 + (KID == KID_WINDING ? n1 : 0);
+  const int o_t2 = o_w2 + (KID == KID_WINDING ? n2 : 0);
+  const int o_b2 = 2 * (o_t2 + n2);
+  const int o_lut = 2 * (o_b2 + n2);
+#define s_cm1(i) sh_f4[o_cm1 + (i)]
+#define s_tp1(i) sh_i4[o_tp1 + (i)]
+#define s_cm2(i) sh_f4[o_cm2 + (i)]
+#define s_w1(i) sh_f2[o_w1 + (i)]
+#define s_w2(i) sh_f2[o_w2 + (i)]
+#define s_t2(i) sh_i2[o_t2 + (i)]
+#define s_b2(i) sh_i[o_b2 + (i)]
+#define s_lut(i) sh_u16[o_lut + (i)]
+#define s_p2(i) sh_f4[o_p2 + (i)]
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < n1; i += kWarpBlock) {
+    s_cm1(i) = V.cm[1 + i];
+    s_tp1(i) = V.topo[1 + i];
+    if (KID == KID_WINDING) s_w1(i) = V.m12[1 + i];
+  }
+  const bool l2_multi = V.first_multi <= 2;
+  for (int i = tid; i < n2; i += kWarpBlock) {
+    s_cm2(i) = V.cm[V.base2 + i];
+    if (KID == KID_WINDING) s_w2(i) = V.m12[V.base2 + i];
+    int b = V.lb[V.base2 + i];
+    const int4 tp = V.topo[V.base2 + i];
+    if (l2_multi && tp.y == 0 && tp.w - tp.z > 1) b |= 0x80000000;
+    s_b2(i) = b;
+    s_t2(i) = make_int2(tp.y > 0 ? (tp.x | (tp.y << 25)) : 0, tp.w - tp.z);
+  }
+  for (int i = tid; i < np2; i += kWarpBlock) {  // odd tail: a massless copy
+    const float4 u = V.cm[V.base2 + 2 * i];
+    const float4 v = 2 * i + 1 < n2 ? V.cm[V.base2 + 2 * i + 1] : make_float4(u.x, u.y, u.z, 0.f);
+    s_p2(2 * i) = make_float4(u.x, v.x, u.y, v.y);
+    s_p2(2 * i + 1) = make_float4(u.z, v.z, -u.w, -v.w);
+  }
+  __syncthreads();
+  for (int i = tid; i < n1 * (kLut + 1); i += kWarpBlock) {
+    const int a = i / (kLut + 1), b = i - a * (kLut + 1);
+    const int4 tpa = s_tp1(a);
+    int c = 0;
+    if (tpa.y > 0) {
+      int jb = tpa.z + (int)(((int64_t)b * (tpa.w - tpa.z)) >> kLutBits);
+      if (jb > tpa.w - 1) jb = tpa.w - 1;
+      const int k0 = tpa.x - V.base2;
+      c = child_search(o_b2, k0, tpa.y, jb) - k0;
+    }
+    s_lut(i) = (unsigned short)c;
+  }
+  int seen_base = n1, n_int = 0;
+  for (int a = 0; a < n1; ++a) {
+    const int4 tpa = s_tp1(a);
+    if (tpa.y > 0) {
+      seen_base += S * (tpa.y + 1);
+      ++n_int;
+    }
+  }
+  __syncthreads();
+
+  const uint64_t hseed = mix64(seed + kGamma);
+  const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
+  const float2 w0 = make_float2(0.f, 0.f);
+  const int nslot = n1 * S;
+  const int64_t nchunks = (n + 31) / 32;
+  while (true) {
+    unsigned int ch = 0;
+    if (lane == 0) ch = atomicAdd(chunk_ctr, 1u);
+    ch = __shfl_sync(0xffffffffu, ch, 0);
+    if ((int64_t)ch >= nchunks) break;
+    const int64_t t = (int64_t)ch * 32 + lane;
+    const bool live = t < n;
+    const int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
+    const float qx = live ? (float)q[3 * qi] : 0.f, qy = live ? (float)q[3 * qi + 1] : 0.f,
+                qz = live ? (float)q[3 * qi + 2] : 0.f;
+    const uint64_t hq = key_fold(hseed, (uint64_t)(((int64_t)ch * 32 + qoff) >> 5));
+
+    // ---- dense part: every level-2 record (as k_sto_fast) + leaf subdomains
+    double acc = 0.0;
+    if (kPack && !l2_multi) {
+      // packed FP32 (FADD2/FFMA2): two records per instruction; the distance
+      // floor enters as r2 + floor^2 (as k_brute32_coulomb2)
+      const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy),
+                   nz = make_float2(-qz, -qz);
+      const float f2 = kp.dfloor_f * kp.dfloor_f;
+      const float2 fl2 = make_float2(f2, f2);
+      int k = 0;
+      for (; k < np2; k += 8) {
+        const int e = min(k + 8, np2);
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+#pragma unroll 4
+        for (int i = k; i < e; ++i) {
+          const float4 A = s_p2(2 * i), B = s_p2(2 * i + 1);
+          const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
+          const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
+          const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
+          const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
+          const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+          if (i & 1)
+            a1 = __ffma2_rn(make_float2(B.z, B.w), ri, a1);
+          else
+            a0 = __ffma2_rn(make_float2(B.z, B.w), ri, a0);
+        }
+        acc += (double)((a0.x + a0.y) + (a1.x + a1.y));
+      }
+    } else if (!l2_multi) {
+      int k = 0;
+      for (; k + 16 <= n2; k += 16) {
+        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; u += 4) {
+          p0 += fterm<KID>(s_cm2(k + u), KID == KID_WINDING ? s_w2(k + u) : w0, qx, qy, qz, kp);
+          p1 += fterm<KID>(s_cm2(k + u + 1), KID == KID_WINDING ? s_w2(k + u + 1) : w0, qx, qy,
+                           qz, kp);
+          p2 += fterm<KID>(s_cm2(k + u + 2), KID == KID_WINDING ? s_w2(k + u + 2) : w0, qx, qy,
+                           qz, kp);
+          p3 += fterm<KID>(s_cm2(k + u + 3), KID == KID_WINDING ? s_w2(k + u + 3) : w0, qx, qy,
+                           qz, kp);
+        }
+        acc += (double)((p0 + p1) + (p2 + p3));
+      }
+      float p0 = 0.f;
+      for (; k < n2; ++k)
+        p0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
+      acc += (double)p0;
+    } else {
+      for (int k = 0; k < n2; ++k) {
+        float v;
+        if (s_b2(k) < 0) {
+          const int4 tp = V.topo[V.base2 + k];
+          v = leaf_exact<KID>(V, tp.z, tp.w, qx, qy, qz, kp);
+        } else {
+          v = fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
+        }
+        acc += (double)v;
+      }
+    }
+    for (int a_ord = 0; a_ord < n1; ++a_ord) {  // leaf subdomains: exact, never sampled
+      const int4 tpa = s_tp1(a_ord);
+      if (tpa.y == 0)
+        acc += (double)((tpa.w - tpa.z > 1)
+                            ? leaf_exact<KID>(V, tpa.z, tpa.w, qx, qy, qz, kp)
+                            : fterm<KID>(s_cm1(a_ord), KID == KID_WINDING ? s_w1(a_ord) : w0, qx,
+                                         qy, qz, kp));
+    }
+
+    int seen = seen_base, steps = 0;
+    double acc_deep = 0.0;
+    for (int f0 = 0; f0 < nslot; f0 += 32) {
+      // lane L draws sample f0 + L for the whole warp: index draw exactly as
+      // _core.py:166-169, level-1 step from shared memory
+      int my_a = -1, my_lo = 0, my_j = 0;
+      uint64_t my_kr = 0;
+      {
+        const int f = f0 + lane;
+        if (f < nslot) {
+          const int a_ord = f / S, sm = f - a_ord * S;
+          const int4 tpa = s_tp1(a_ord);
+          if (tpa.y > 0) {
+            const uint64_t hs = key_fold(key_fold(hq, (uint64_t)a_ord), (uint64_t)sm);
+            const uint64_t ki = key_fold(hs, 0);
+            my_kr = key_fold(hs, 1);
+            const uint64_t x = mix64(ki + kGamma);
+            const double u0 = __ull2double_rn(x >> 11) * (1.0 / 9007199254740992.0);
+            int j = tpa.z + (int)__dmul_rn(u0, (double)(tpa.w - tpa.z));
+            if (j >= tpa.w) j = tpa.w - 1;
+            const int k0 = tpa.x - V.base2, lut0 = a_ord * (kLut + 1);
+            const int bkt = (int)(x >> (64 - kLutBits));
+            int c = s_lut(lut0 + bkt);
+            const int ce = s_lut(lut0 + bkt + 1);
+            while (c < ce && (s_b2(k0 + c + 1) & 0x7fffffff) <= j) ++c;
+            my_a = a_ord;
+            my_lo = k0 + c;
+            my_j = j;
+          }
+        }
+      }
+      const int cnt = min(32, nslot - f0);
+      for (int i = 0; i < cnt; ++i) {
+        const int a_ord = __shfl_sync(0xffffffffu, my_a, i);
+        if (a_ord < 0) continue;  // warp-uniform
+        const int lo = __shfl_sync(0xffffffffu, my_lo, i);
+        const int jj = __shfl_sync(0xffffffffu, my_j, i);
+        const uint64_t kr = ((uint64_t)__shfl_sync(0xffffffffu, (unsigned)(my_kr >> 32), i) << 32) |
+                            __shfl_sync(0xffffffffu, (unsigned)my_kr, i);
+        // roulette uniforms of this walk: lane L holds the draw with counter L
+        const float u_l = RR == 2 ? 0.f : draw24(kr, (uint64_t)lane);
+        const int4 tpa = s_tp1(a_ord);
+        const int count_a = tpa.w - tpa.z;
+        const float4 c2 = s_cm2(lo);
+        float rp = fdist(c2, qx, qy, qz) * id2;
+        float prr = rr_fast_t<RR>(fdist(s_cm1(a_ord), qx, qy, qz) * id1, rp);
+        const float ua = __shfl_sync(0xffffffffu, u_l, 0);
+        bool alive = live && (RR == 2 || prr >= 1.f || ua < prr);
+        if (!__any_sync(0xffffffffu, alive)) continue;
+        if (alive) ++steps;
+        float cvn = fterm<KID>(c2, KID == KID_WINDING ? s_w2(lo) : w0, qx, qy, qz, kp);
+        const int2 t2 = s_t2(lo);
+        int4 tp = make_int4(t2.x & 0x1ffffff, (int)((unsigned)t2.x >> 25), 0, t2.y);
+        const uint64_t path = V.path[jj];
+        int lvl = 2;
+        float resid = 0.f;
+        while (tp.y > 0) {  // warp-uniform: every lane walks the same node
+          const bool cmulti = lvl + 1 >= V.first_multi;
+          float ks0 = 0.f, ks1 = 0.f;
+          int le = 0, c = 0;
+          const unsigned am = __ballot_sync(0xffffffffu, alive);
+          if (FSB_WARP_SERIAL && !cmulti && lvl < V.path_levels &&
+              __popc(am) * (((tp.y + 31) >> 5) * 11 + 14) < tp.y * 10) {
+            // few live queries: one at a time, lanes over the children, then a
+            // butterfly sum (work ~ live queries x children, not 32 x children)
+            le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
+            for (unsigned mm = am; mm; mm &= mm - 1) {
+              const int src = __ffs(mm) - 1;
+              const float sx = __shfl_sync(0xffffffffu, qx, src),
+                          sy = __shfl_sync(0xffffffffu, qy, src),
+                          sz = __shfl_sync(0xffffffffu, qz, src);
+              float part = 0.f;
+              for (int k = lane; k < tp.y; k += 32)
+                part += fterm<KID>(V.cm[tp.x + k], KID == KID_WINDING ? V.m12[tp.x + k] : w0, sx,
+                                   sy, sz, kp);
+#pragma unroll
+              for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+              if (lane == src) ks0 = part;
+            }
+          } else if (!cmulti && lvl < V.path_levels) {
+            le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
+            if (tp.x & 1) {
+              ks0 += fterm<KID>(V.cm[tp.x], KID == KID_WINDING ? V.m12[tp.x] : w0, qx, qy, qz, kp);
+              c = 1;
+            }
+            for (; c + 3 < tp.y; c += 4) {
+              const int r = tp.x + c;
+              float4 c0, c1, c2_, c3;
+              ld_pair(V.cm + r, c0, c1);
+              ld_pair(V.cm + r + 2, c2_, c3);
+              ks0 += fterm<KID>(c0, KID == KID_WINDING ? V.m12[r] : w0, qx, qy, qz, kp);
+              ks1 += fterm<KID>(c1, KID == KID_WINDING ? V.m12[r + 1] : w0, qx, qy, qz, kp);
+              ks0 += fterm<KID>(c2_, KID == KID_WINDING ? V.m12[r + 2] : w0, qx, qy, qz, kp);
+              ks1 += fterm<KID>(c3, KID == KID_WINDING ? V.m12[r + 3] : w0, qx, qy, qz, kp);
+            }
+            for (; c < tp.y; ++c)
+              ks0 += fterm<KID>(V.cm[tp.x + c], KID == KID_WINDING ? V.m12[tp.x + c] : w0, qx, qy,
+                                qz, kp);
+          } else {
+            for (; c < tp.y; ++c) {
+              const int r = tp.x + c;
+              const float4 cr = V.cm[r];
+              const float2 wr = KID == KID_WINDING ? V.m12[r] : w0;
+              float v;
+              if (cmulti) {
+                const int4 tc = V.topo[r];
+                v = (tc.y == 0 && tc.w - tc.z > 1)
+                        ? leaf_exact<KID>(V, tc.z, tc.w, qx, qy, qz, kp)
+                        : fterm<KID>(cr, wr, qx, qy, qz, kp);
+              } else {
+                v = fterm<KID>(cr, wr, qx, qy, qz, kp);
+              }
+              ks0 += v;
+              le += V.lb[r] <= jj;
+            }
+          }
+          const int cidx = tp.x + le - 1;
+          const float4 cch = V.cm[cidx];
+          if (alive) {
+            seen += tp.y + 1;
+            const float pagg = (float)(tp.w - tp.z) / (float)count_a;
+            resid += ((ks0 + ks1) - cvn) * rcp_ftz(pagg * prr);
+          }
+          const float rc = fdist(cch, qx, qy, qz) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
+          const float p = rr_fast_t<RR>(rp, rc);
+          const int ctr = lvl - 1;  // levels descended so far
+          const float u = ctr < 32 ? __shfl_sync(0xffffffffu, u_l, ctr & 31)
+                                   : (RR == 2 ? 0.f : draw24(kr, (uint64_t)ctr));
+          alive = alive && (RR == 2 || p >= 1.f || u < p);
+          if (!__any_sync(0xffffffffu, alive)) break;
+          if (alive) {
+            ++steps;
+            cvn = fterm<KID>(cch, KID == KID_WINDING ? V.m12[cidx] : w0, qx, qy, qz, kp);
+            prr *= p;
+            rp = rc;
+          }
+          tp = V.topo[cidx];
+          ++lvl;
+        }
+        acc_deep += (double)resid;
+      }
+    }
+    if (live) {
+      out[qi] = (float)(acc + acc_deep / (double)S);
+      if (visited) visited[qi] = seen;
+      if (path_steps) path_steps[qi] = steps;
+      if (path_count) path_count[qi] = (int64_t)S * n_int;
+    }
+  }
+#undef s_cm1
+#undef s_tp1
+#undef s_cm2
+#undef s_w1
+#undef s_w2
+#undef s_t2
+#undef s_b2
+#undef s_lut
+#undef s_p2
+}
+
 // returns 1 if the fast path does not apply (caller falls back), 0 on launch
 int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                     const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
@@ -678,6 +1022,42 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   if (rr_mode < 0 || rr_mode > 2) {
     set_error("unknown rr mode %d", rr_mode);
     return 1;
+  }
+  if (share == 5 && (qoff & 31) == 0 && !std::getenv("FSB_STO_WARP_OFF")) {
+    // warp-shared streams on warp-aligned groups: the warp-uniform kernel
+    const size_t wsmem =
+        ((16 * (2 * n1 + n2 + (kid == KID_COULOMB && FSB_WARP_DENSE2 ? 2 * ((n2 + 1) / 2) : 0)) +
+          8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 1)) +
+         15) & ~(size_t)15;
+    auto launch_w = [&](auto kern) -> int {
+      if (wsmem > 48 * 1024)
+        FS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+      FS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpBlock, wsmem));
+      const int64_t blocks = (n + kWarpBlock - 1) / kWarpBlock;
+      const int64_t grid = std::min<int64_t>(blocks, (int64_t)sms * std::max(per_sm, 1));
+      Scratch ctr;
+      FS_TRY(ctr.alloc(sizeof(unsigned int), s));
+      FS_CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned int), s));
+      kern<<<(unsigned)grid, kWarpBlock, wsmem, s>>>(V, q, n, qperm, n_samples, seed, qoff, kp,
+                                                     ctr.as<unsigned int>(), out, visited,
+                                                     path_steps, path_count);
+      FS_CK(cudaGetLastError());
+      return 0;
+    };
+    switch (kid * 3 + rr_mode) {
+      case 0: rc = launch_w(k_sto_warp<0, 0>); break;
+      case 1: rc = launch_w(k_sto_warp<0, 1>); break;
+      case 2: rc = launch_w(k_sto_warp<0, 2>); break;
+      case 3: rc = launch_w(k_sto_warp<1, 0>); break;
+      case 4: rc = launch_w(k_sto_warp<1, 1>); break;
+      case 5: rc = launch_w(k_sto_warp<1, 2>); break;
+      case 6: rc = launch_w(k_sto_warp<2, 0>); break;
+      case 7: rc = launch_w(k_sto_warp<2, 1>); break;
+      case 8: rc = launch_w(k_sto_warp<2, 2>); break;
+      default: set_error("unknown kernel id"); return 1;
+    }
+    if (rc == 0) *used = true;
+    return rc;
   }
   switch (kid * 3 + rr_mode) {
     case 0: rc = launch(k_sto_fast<0, 0>); break;

@@ -160,3 +160,57 @@ def test_load_balanced_bh_matches_warp_coherent_bh(fs, monkeypatch):
         assert np.max(np.abs(a.raw - b.raw) / np.abs(b.raw)) <= 1e-6
         c = evaluate_field_device(cfg, s, kern, q, t).to_host()  # deterministic
         np.testing.assert_array_equal(a.raw, c.raw)
+
+
+@pytest.mark.parametrize("case,kind", FAST_CASES, ids=lambda c: c if isinstance(c, str) else c["kind"])
+@pytest.mark.parametrize("rr", ["paper_ratio", "fixed_half", "disabled"])
+def test_warp_kernel_tracks_fp64_shared_kernel(fs, case, kind, rr):
+    """rng_sharing="warp": k_sto_warp (FP32, warp-uniform walks; query_offset % 32
+    == 0) and k_sto_fast with group keys (offset 7) against k_stochastic in the
+    same mode (FP64, group keys): same order, same draws, so per-query values
+    agree to FP32 rounding and the walk counters agree except where a roulette
+    decision at the FP32/FP64 boundary flips."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    s = scenes.build_sources(case)
+    kern = fs.KernelSpec(kind)
+    rng = np.random.default_rng(12)
+    qd = dev.to_device(rng.uniform(-1.2, 1.2, (1500, 3)))
+    t = fs.build_tree(s, 4)
+    for S in (1, 3, 60):
+        for off in (0, 64, 7):
+            res = {}
+            for prec in ("f32", "f64"):
+                cfg = fs.EstimatorConfig("stochastic", samples_per_subdomain=S, rr_mode=rr,
+                                         seed=17, precision=prec, rng_sharing="warp")
+                r = evaluate_field_device(cfg, s, kern, qd, t, query_offset=off)
+                res[prec] = (r.raw.cpu().numpy(), r.path_steps.cpu().numpy(),
+                             r.visited.cpu().numpy(), r.path_count.cpu().numpy())
+            a, b = res["f32"], res["f64"]
+            fin = np.isfinite(b[0])
+            close = _rel(a[0][fin], b[0][fin]) <= 1e-4
+            assert close.mean() >= 0.97, (S, off, close.mean())
+            same = (a[1] == b[1]) & (a[2] == b[2])
+            assert same.mean() >= 0.97, (S, off, same.mean())
+            np.testing.assert_array_equal(a[3], b[3])
+            if rr == "disabled":
+                assert same.all()
+
+
+def test_shuffle_order_is_a_seeded_permutation(fs):
+    from paper_2506_02219_b200 import _device as dev, _lib
+    import ctypes as C
+    L = _lib.lib()
+    import torch
+    for n in (1, 2, 31, 1000, 65537):
+        outs = []
+        for seed in (5, 5, 6):
+            p = dev.empty(n, torch.int32)
+            _lib.check(L.fsb_shuffle_order(n, seed, C.c_void_p(dev.ptr(p)),
+                                           C.c_void_p(dev.stream_ptr())))
+            outs.append(p.cpu().numpy())
+        np.testing.assert_array_equal(np.sort(outs[0]), np.arange(n))
+        np.testing.assert_array_equal(outs[0], outs[1])
+        if n > 31:
+            assert (outs[0] != outs[2]).mean() > 0.9
+            assert (outs[0] != np.arange(n)).mean() > 0.9
