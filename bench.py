@@ -5,7 +5,11 @@ potential of 2^22 area-uniform samples of one compact tilted torus
 (torus(0.25, 0.06) rotated 0.7 rad about x, shifted (0.1, 0.05, -0.1); masses
 1/M, seed 7) on a 1000 x 1000 slice plane at z = 0.03.  A step is one
 stochastic S=1 evaluation of all 10^6 queries (FP32 terms / FP64
-accumulation, tree prebuilt and resident).  Reported beside it:
+accumulation, tree prebuilt and resident) with the paper's GPU recipe for
+the RNG streams (``--streams warp``, default: 32 shuffled queries share one
+stream); the reference's per-query streams
+(``--streams query``, draw-for-draw parity) are timed and error-matched beside
+it under ``other_streams``.  Reported beside the step:
 
 * median relative error of S=1 vs brute force (GPU brute force, FP64 accum.)
 * the GPU deterministic BH (same API, f32) beta sweep, log-log interpolated
@@ -56,9 +60,18 @@ def workload(m=M_SOURCES, side=N_SIDE):
     return src, qs, KernelSpec("coulomb")
 
 
-def config_block():
+STREAM_NOTES = {
+    "warp": ("warp-shared RNG streams, the paper's GPU recipe (PAPER.md:323, 392): 32 queries in a "
+             "seeded shuffled order share the index and roulette streams (rng_sharing='warp')"),
+    "query": ("per-query RNG streams, the reference's (rng.py:39-47, _core.py:219; "
+              "rng_sharing='query', draw-for-draw parity)"),
+}
+
+
+def config_block(streams="warp"):
     return {"workload": "C4: coulomb, 2^22 tilted-torus surface samples, 1000^2 slice plane z=0.03",
             "sources": M_SOURCES, "queries": N_SIDE * N_SIDE, "method": "stochastic S=1 paper_ratio",
+            "rng_streams": STREAM_NOTES[streams],
             "branching": {"stochastic": 4, "barnes_hut": 2}, "precision": "f32 terms, f64 accumulation",
             "l2": "no flush; inputs larger than L2 (tree records ~0.3 GB, queries 24 MB)",
             "parallelism": "query slabs (replica tree per rank)"}
@@ -237,10 +250,13 @@ def run_ours(args):
 
     q_dev = dev.to_device(qs.positions)
     qoff = rank * n  # slab `rank` of a world*n query set: distinct RNG streams per rank
-    cfg_s1 = fs.EstimatorConfig("stochastic", samples_per_subdomain=1, seed=1, precision="f32")
+    other = "query" if args.streams == "warp" else "warp"
+    cfgs = {m: fs.EstimatorConfig("stochastic", samples_per_subdomain=1, seed=1, precision="f32",
+                                  rng_sharing=m) for m in ("warp", "query")}
+    cfg_s1 = cfgs[args.streams]
 
-    def step():
-        return evaluate_field_device(cfg_s1, src, kern, q_dev, tree4, query_offset=qoff)
+    def step(mode=args.streams):
+        return evaluate_field_device(cfgs[mode], src, kern, q_dev, tree4, query_offset=qoff)
 
     for _ in range(args.warmup):
         step()
@@ -286,11 +302,20 @@ def run_ours(args):
     vis = dev.empty(n, torch.int64)
     h = C.c_void_p(tree4._device_tree().handle)
 
+    order = dev.empty(n, torch.int32)
+    _lib.check(L.fsb_shuffle_order(n, 1, qoff, C.c_void_p(dev.ptr(order)), sp))
+
     def kernel_only():
-        _lib.check(L.fsb_stochastic_batch(h, 0, kern.alpha, kern.distance_floor, 1,
-                                          C.c_void_p(dev.ptr(q_dev)), n, None, 1, 0, 1, qoff,
-                                          C.c_void_p(dev.ptr(raw)), C.c_void_p(dev.ptr(vis)),
-                                          None, None, sp))
+        if args.streams == "warp":  # k_sto_warp (the order is computed once, outside)
+            _lib.check(L.fsb_stochastic_batch_shared(
+                h, 0, kern.alpha, kern.distance_floor, 1, C.c_void_p(dev.ptr(q_dev)), n,
+                C.c_void_p(dev.ptr(order)), 1, 0, 1, qoff, 5, C.c_void_p(dev.ptr(raw)),
+                C.c_void_p(dev.ptr(vis)), None, None, sp))
+        else:  # k_sto_fast
+            _lib.check(L.fsb_stochastic_batch(h, 0, kern.alpha, kern.distance_floor, 1,
+                                              C.c_void_p(dev.ptr(q_dev)), n, None, 1, 0, 1, qoff,
+                                              C.c_void_p(dev.ptr(raw)), C.c_void_p(dev.ptr(vis)),
+                                              None, None, sp))
     kernel_only()
     torch.cuda.synchronize()
     reps = max(3, args.steps)
@@ -308,8 +333,8 @@ def run_ours(args):
     out = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-           "data": "synthetic (reference mesh generators, fixed seeds)", "config": config_block(),
-           "clocks": clk.summary(), "e2e": e2e}
+           "data": "synthetic (reference mesh generators, fixed seeds)",
+           "config": config_block(args.streams), "clocks": clk.summary(), "e2e": e2e}
     if launches_per_step is not None:
         out["gpu_launches"] = launches_per_step * args.steps
 
@@ -327,6 +352,17 @@ def run_ours(args):
         truth_h = truth.cpu().numpy()
         s1 = res.values.cpu().numpy()
         err_s1 = median_rel(s1, truth_h)
+        # the other stream mode, timed the same way (device-resident steps)
+        for _ in range(args.warmup):
+            r_o = step(other)
+        torch.cuda.synchronize()
+        ev_a.record()
+        for _ in range(args.steps):
+            r_o = step(other)
+        ev_b.record()
+        torch.cuda.synchronize()
+        other_ms = ev_a.elapsed_time(ev_b) / args.steps
+        err_other = median_rel(r_o.values.cpu().numpy(), truth_h)
         sweep = []
         for beta in BETAS:
             cfg = fs.EstimatorConfig("barnes_hut", beta=beta, precision="f32")
@@ -346,9 +382,10 @@ def run_ours(args):
             sweep.append({"beta": beta, "ms": ms, "median_rel_err": err,
                           "visited_mean": float(r.visited.double().mean().item())})
             log(f"BH beta={beta}: {ms:.2f} ms, median rel err {err:.3e}")
-            if err < 0.5 * err_s1 or ms > 2000:
+            if err < 0.5 * min(err_s1, err_other) or ms > 2000:
                 break
         matched_ms = loglog_interp([(p["median_rel_err"], p["ms"]) for p in sweep], err_s1)
+        matched_other = loglog_interp([(p["median_rel_err"], p["ms"]) for p in sweep], err_other)
         # the north star's warp-coherent BH (one query per lane, no work splitting),
         # bracketing the matched point: reported beside the load-balanced headline
         wc = []
@@ -377,6 +414,11 @@ def run_ours(args):
         out["speedup_vs_bh_at_matched_error"] = (matched_ms / step_ms) if matched_ms else None
         out["bh_note"] = ("headline BH = load-balanced FP32 BH (warps hand large subtrees of long "
                           "union walks to other warps, csrc/fs_bh_split.cu)")
+        out["other_streams"] = {
+            "rng_streams": STREAM_NOTES[other], "ms_per_step": other_ms,
+            "value": world * n / (other_ms * 1e-3), "s1_median_rel_err": err_other,
+            "matched_bh_ms": matched_other,
+            "speedup_vs_bh_at_matched_error": (matched_other / other_ms) if matched_other else None}
         out["warp_coherent_bh"] = {"sweep": wc, "matched_ms": wc_ms,
                                    "speedup_at_matched_error": (wc_ms / step_ms) if wc_ms else None,
                                    "note": "one query per lane, warp-union preorder walk, no "
@@ -401,16 +443,19 @@ def run_ours(args):
         ach = inter_q * n / (kern_ms * 1e-3)
         limit = min(128 * sms * f_mhz * 1e6 / 8, 16 * sms * f_mhz * 1e6 / 1)  # coulomb I=8, U=1
         # pipe floor with the integer RNG work (6 splitmix64 per sample: 6 IMAD on
-        # the FMA-heavy pipe + 14 ALU ops each): max over FMA / ALU / MUFU pipes
-        fma_cyc = (7 * inter_q + 2 * 36 * samples_q) / 128.0
-        alu_cyc = (1 * inter_q + 84 * samples_q) / 64.0
-        mufu_cyc = (inter_q + samples_q) / 16.0
+        # the FMA-heavy pipe + 14 ALU ops each; once per warp with shared streams):
+        # max over FMA / ALU / MUFU pipes
+        share = 32.0 if args.streams == "warp" else 1.0
+        fma_cyc = (7 * inter_q + 2 * 36 * samples_q / share) / 128.0
+        alu_cyc = (1 * inter_q + 84 * samples_q / share) / 64.0
+        mufu_cyc = (inter_q + samples_q / share) / 16.0
         floor_ms = max(fma_cyc, alu_cyc, mufu_cyc) * n / (sms * f_mhz * 1e6) * 1e3
+        kname = "k_sto_warp" if args.streams == "warp" else "k_sto_fast"
         out["roofline"] = {
             "bound": "fp32+mufu", "achieved": ach * 10 / 1e12, "peak": limit * 10 / 1e12,
             "unit": "TFLOP/s", "frac": ach / limit,
-            "traffic": _profiled_traffic("k_sto_fast<0"),
-            "kernel": "k_sto_fast<coulomb, paper_ratio> (FP32)", "kernel_ms": kern_ms,
+            "traffic": _profiled_traffic(kname + "<0"),
+            "kernel": f"{kname}<coulomb, paper_ratio> (FP32)", "kernel_ms": kern_ms,
             "work": (f"{inter_q:.1f} interactions/query = {n2} dense level-2 records + "
                      f"{walk_inter:.1f} walk children; 10 flops each"),
             "peak_source": (f"FP32 128/clk/SM over 8 ops, MUFU 16/clk/SM over 1 op, {sms} SMs "
@@ -543,8 +588,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference mesh generators, fixed seeds)", "config": config_block(),
-            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
+            "data": "synthetic (reference mesh generators, fixed seeds)",
+            "config": config_block("query"), "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
                              "sample": f"{n_sample} random queries of the C4 plane per step, "
                                        f"stochastic S=1 f64, oracle/fastsum_oracle.c (OpenMP)"},
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -560,6 +605,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-sample", type=int, default=N_SIDE * N_SIDE)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--streams", choices=("warp", "query"), default="warp",
+                    help="RNG streams of the headline step (the other mode is reported beside)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -119,10 +119,13 @@ int fsb_telescoping_batch(fsb_tree *tree, int kid, double alpha, double dfloor, 
  * query bounding box, stable): perm_out (n,) int32.  Result-invariant (F8). */
 int fsb_query_order(const double *queries, int64_t n, int32_t *perm_out, void *stream);
 
-/* Seeded pseudo-random permutation of 0..n-1 (the evaluation order of the
- * paper's RNG-sharing groups): perm_out (n,) int32.  A 4-round Feistel network
- * keyed on the seed, cycle-walked into [0, n); one kernel, no sort. */
-int fsb_shuffle_order(int64_t n, uint64_t seed, int32_t *perm_out, void *stream);
+/* Seeded evaluation order of the paper's RNG-sharing groups: perm_out (n,) int32,
+ * a permutation of 0..n-1 that maps every window of 2^15 consecutive positions
+ * onto itself (window w: a 4-round Feistel network keyed on (seed,
+ * query_offset + w * 2^15), cycle-walked into the window; one kernel, no sort).
+ * Window-local order lets evaluate_field_host pipeline window-aligned slabs. */
+int fsb_shuffle_order(int64_t n, uint64_t seed, int64_t query_offset, int32_t *perm_out,
+                      void *stream);
 
 /* post_transform (kernels.py:110-122) applied to raw sums: smooth != 0 gives
  * -ln(raw)/alpha with (+inf, flagged) for raw <= 0; otherwise values = raw.
@@ -162,6 +165,8 @@ typedef struct fsb_eval_args {
   const double *src_ms;   /* brute force: device masses (m,c) */
   int64_t m;
   int c;
+  int rng_group_log2;     /* stochastic: 0 = per-query streams (reference); 5 = the
+                             paper's warp-shared streams over fsb_shuffle_order */
 } fsb_eval_args;
 
 int fsb_evaluate_field_host(fsb_tree *tree, const fsb_eval_args *args, const double *queries,

@@ -29,7 +29,8 @@ class EvalArgs(C.Structure):
     _fields_ = [("method", _I), ("kid", _I), ("alpha", _D), ("dfloor", _D), ("precision", _I),
                 ("beta", _D), ("n_samples", _I64), ("rr_mode", _I), ("seed", C.c_uint64),
                 ("query_offset", _I64), ("smooth", _I), ("query_order", _I),
-                ("src_pts", _P), ("src_ms", _P), ("m", _I64), ("c", _I)]
+                ("src_pts", _P), ("src_ms", _P), ("m", _I64), ("c", _I),
+                ("rng_group_log2", _I)]
 
 
 METHOD_CODES = {"brute_force": 0, "barnes_hut": 1, "telescoping_exhaustive": 2, "stochastic": 3}
@@ -54,7 +55,7 @@ SIGNATURES = {
     "fsb_stochastic_moments_batch": [_P, _I, _D, _D, _P, _I64, _I64, _I, C.c_uint64, _P, _P, _P],
     "fsb_telescoping_batch": [_P, _I, _D, _D, _I, _P, _I64, _P, _P, _P],
     "fsb_query_order": [_P, _I64, _P, _P],
-    "fsb_shuffle_order": [_I64, C.c_uint64, _P, _P],
+    "fsb_shuffle_order": [_I64, C.c_uint64, _I64, _P, _P],
     "fsb_post_transform": [_P, _I, _I64, _I, _D, _P, _P, _P, _P],
     "fsb_evaluate_field_host": [_P, C.POINTER(EvalArgs), _P, _I64, _P, _P, _P, _P, _P, _P, _I,
                                 _P],

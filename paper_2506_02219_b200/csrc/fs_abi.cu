@@ -120,14 +120,16 @@ int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s) {
 }
 // seeded pseudo-random evaluation order (the paper shuffles the query grid so that
 // RNG-sharing groups are spatially scattered)
-// seeded permutation of [0, n): a 4-round balanced Feistel network on the
-// smallest 2^(2h) >= n domain, cycle-walked back into [0, n) (a bijection; on
-// average < 4 rounds of walking).  One pass, no sort.
-__device__ __forceinline__ uint64_t feistel4(uint64_t x, int hb, uint64_t k0, uint64_t k1,
-                                             uint64_t k2, uint64_t k3) {
+// Seeded evaluation order of the warp-shared mode: positions are cut into
+// windows of kShuffleWindow, and window w (positions [wW, min((w+1)W, n)))
+// is permuted by a 4-round balanced Feistel network keyed on (seed,
+// query_offset + wW) over the smallest 2^(2h) >= its size, cycle-walked back
+// into range (a bijection; < 4 walking rounds on average).  One pass, no sort.
+// Windows keep the order slab-local, so the host pipeline can copy, evaluate
+// and return window-aligned slabs independently (same result as one launch).
+__device__ __forceinline__ uint64_t feistel4(uint64_t x, int hb, const uint64_t (&ks)[4]) {
   const uint64_t mask = (1ull << hb) - 1ull;
   uint64_t l = x >> hb, r = x & mask;
-  const uint64_t ks[4] = {k0, k1, k2, k3};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint64_t f = mix64(ks[i] ^ r) & mask;
@@ -138,22 +140,24 @@ __device__ __forceinline__ uint64_t feistel4(uint64_t x, int hb, uint64_t k0, ui
   return (l << hb) | r;
 }
 
-__global__ void k_shuffle(int64_t n, int hb, uint64_t k0, uint64_t k1, uint64_t k2, uint64_t k3,
-                          int32_t* __restrict__ perm) {
+__global__ void k_shuffle(int64_t n, uint64_t h, int64_t qoff, int32_t* __restrict__ perm) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint64_t y = feistel4((uint64_t)i, hb, k0, k1, k2, k3);
-  while (y >= (uint64_t)n) y = feistel4(y, hb, k0, k1, k2, k3);
-  perm[i] = (int32_t)y;
+  const int64_t base = i & ~(int64_t)(kShuffleWindow - 1);
+  const int64_t size = min((int64_t)kShuffleWindow, n - base);
+  int hb = 1;
+  while ((1ll << (2 * hb)) < size) ++hb;
+  const uint64_t hw = key_fold(h, (uint64_t)(qoff + base));
+  const uint64_t ks[4] = {key_fold(hw, 0), key_fold(hw, 1), key_fold(hw, 2), key_fold(hw, 3)};
+  uint64_t y = feistel4((uint64_t)(i - base), hb, ks);
+  while (y >= (uint64_t)size) y = feistel4(y, hb, ks);
+  perm[i] = (int32_t)(base + (int64_t)y);
 }
 
-int shuffle_order(int64_t n, uint64_t seed, int32_t* perm, cudaStream_t s) {
+int shuffle_order(int64_t n, uint64_t seed, int64_t qoff, int32_t* perm, cudaStream_t s) {
   if (n <= 0) return 0;
-  int hb = 1;
-  while ((1ll << (2 * hb)) < n) ++hb;
   const uint64_t h = key_fold(mix64(seed + kGamma), 0x73687566ull);  // "shuf"
-  k_shuffle<<<grid_for(n, 256), 256, 0, s>>>(n, hb, key_fold(h, 0), key_fold(h, 1),
-                                             key_fold(h, 2), key_fold(h, 3), perm);
+  k_shuffle<<<grid_for(n, 256), 256, 0, s>>>(n, h, qoff, perm);
   FS_CK(cudaGetLastError());
   return 0;
 }
@@ -187,7 +191,7 @@ static int check_common(int kid, int precision, int64_t n) {
 
 extern "C" {
 
-int fsb_abi_version(void) { return 1; }
+int fsb_abi_version(void) { return 2; }
 
 const char* fsb_last_error(void) { return fsb::g_last_error.c_str(); }
 
@@ -372,12 +376,13 @@ int fsb_query_order(const double* queries, int64_t n, int32_t* perm_out, void* s
   return fsb::query_order(queries, n, perm_out, S(stream));
 }
 
-int fsb_shuffle_order(int64_t n, uint64_t seed, int32_t* perm_out, void* stream) {
+int fsb_shuffle_order(int64_t n, uint64_t seed, int64_t query_offset, int32_t* perm_out,
+                      void* stream) {
   if (n < 0 || (n > 0 && !perm_out)) {
     set_error("bad shuffle arguments");
     return 1;
   }
-  return fsb::shuffle_order(n, seed, perm_out, S(stream));
+  return fsb::shuffle_order(n, seed, query_offset, perm_out, S(stream));
 }
 
 int fsb_post_transform(const void* raw, int raw_is_f32, int64_t n, int smooth, double alpha,

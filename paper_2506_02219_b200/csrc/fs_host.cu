@@ -81,7 +81,8 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   FS_TRY(vis.alloc(sizeof(int64_t) * (size_t)n, s));
   FS_TRY(stp.alloc(sizeof(int64_t) * (size_t)n, s));
   FS_TRY(cnt.alloc(sizeof(int64_t) * (size_t)n, s));
-  if (a->method == FSB_METHOD_BARNES_HUT && a->query_order)
+  const bool shared = a->method == FSB_METHOD_STOCHASTIC && a->rng_group_log2 > 0;
+  if ((a->method == FSB_METHOD_BARNES_HUT && a->query_order) || shared)
     FS_TRY(perm.alloc(sizeof(int32_t) * (size_t)n, s));
 
   Streams& st = streams_for_device();
@@ -107,8 +108,11 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   // H2D and the last D2H copies cannot overlap any evaluation
   chunks = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, n));
   std::vector<int64_t> cut(chunks + 1, 0);
-  for (int k = 1; k < chunks; ++k)
+  for (int k = 1; k < chunks; ++k) {
     cut[k] = (int64_t)((double)n * (k - 0.5) / (chunks - 1.0));
+    // warp-shared streams: slabs start on shuffle windows (order is window-local)
+    if (shared) cut[k] = std::min(n, (cut[k] + kShuffleWindow / 2) / kShuffleWindow * kShuffleWindow);
+  }
   cut[chunks] = n;
   const bool counters = a->method == FSB_METHOD_STOCHASTIC;
   // Slabs alternate between two compute streams so that one slab's last
@@ -151,10 +155,16 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
       case FSB_METHOD_TELESCOPING:
         FS_TRY(telescoping(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, r, v, cs));
         break;
-      default:
-        FS_TRY(stochastic(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, nullptr,
-                          (int)a->n_samples, a->rr_mode, a->seed, a->query_offset + lo, r, v, ps,
-                          pc, cs));
+      default: {
+        int32_t* pp = nullptr;
+        if (shared) {  // the slab's window-local shuffle, keyed on global positions
+          pp = perm.as<int32_t>() + lo;
+          FS_TRY(shuffle_order(m, a->seed, a->query_offset + lo, pp, cs));
+        }
+        FS_TRY(stochastic(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, pp, (int)a->n_samples,
+                          a->rr_mode, a->seed, a->query_offset + lo, r, v, ps, pc, cs,
+                          shared ? a->rng_group_log2 : 0));
+      }
     }
     if (!counters) {
       FS_CK(cudaMemsetAsync(ps, 0, sizeof(int64_t) * (size_t)m, cs));
@@ -234,7 +244,8 @@ extern "C" int fsb_evaluate_field_host(fsb_tree* tree, const fsb_eval_args* a,
     return 1;
   }
   if (a->method == FSB_METHOD_STOCHASTIC &&
-      (a->n_samples < 1 || a->n_samples > (1LL << 30) || a->rr_mode < 0 || a->rr_mode > 2)) {
+      (a->n_samples < 1 || a->n_samples > (1LL << 30) || a->rr_mode < 0 || a->rr_mode > 2 ||
+       a->rng_group_log2 < 0 || a->rng_group_log2 > 20)) {
     set_error("bad samples_per_subdomain / rr mode");
     return 1;
   }

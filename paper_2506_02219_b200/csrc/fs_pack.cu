@@ -22,7 +22,7 @@ void free_tree(FsTree* t) {
                   t->perm, t->points, t->masses, t->weights, t->lo2pre, t->pre2lo, t->skip,
                   t->fc_lo, t->bh32, t->bh64, t->lo_geo32, t->lo_mass32, t->lo_geo64,
                   t->lo_mass64, t->lo_topo, t->pts32a, t->pts32b, t->pts64a, t->pts64b,
-                  t->lo_cm32, t->lo_m12_32, t->lo_begin, t->pt_path};
+                  t->lo_cm32, t->lo_m12_32, t->lo_begin, t->pt_path, t->lo_cmp};
   // the handle's owner may still have work queued on any stream: wait for the
   // device once, then return every array to the pool
   cudaDeviceSynchronize();
@@ -339,6 +339,25 @@ int ensure_path(FsTree* t, cudaStream_t s) {
   t->path_levels = bits <= 16 ? 64 / bits : 0;
   k_point_path<<<grid_for(t->m, 256), 256, 0, s>>>(t->lo_topo, t->m, bits, t->path_levels,
                                                    t->pt_path);
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+__global__ void k_pack_pairs(const float4* __restrict__ cm, int64_t n, float4* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (2 * i >= n) return;
+  const float4 u = cm[2 * i];
+  const float4 v = 2 * i + 1 < n ? cm[2 * i + 1] : make_float4(u.x, u.y, u.z, 0.f);
+  out[2 * i] = make_float4(u.x, v.x, u.y, v.y);
+  out[2 * i + 1] = make_float4(u.z, v.z, -u.w, -v.w);
+}
+
+int ensure_pairs(FsTree* t, cudaStream_t s) {
+  if (t->lo_cmp) return 0;
+  FS_TRY(ensure_fast(t, s));
+  const int64_t np = (t->n + 1) / 2;
+  FS_TRY(dalloc(&t->lo_cmp, 2 * np, s));
+  k_pack_pairs<<<grid_for(np, 256), 256, 0, s>>>(t->lo_cm32, t->n, t->lo_cmp);
   FS_CK(cudaGetLastError());
   return 0;
 }

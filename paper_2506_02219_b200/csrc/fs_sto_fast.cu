@@ -28,6 +28,7 @@
 //    order, so a query's value never depends on which lane served its walks.
 //  * FP32 terms and residuals, FP64 accumulation across chunks/subdomains.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "fs_common.cuh"
@@ -46,6 +47,7 @@ struct FastView {
   const float4* __restrict__ pa;   // permuted points {x, y, z, m0}
   const float4* __restrict__ pb;   // {m1, m2, 0, 0}
   const uint64_t* __restrict__ path;  // per point: sibling rank per level (ensure_path)
+  const float4* __restrict__ cmp;  // Coulomb node pairs, packed (ensure_pairs; warp kernel)
   int path_bits, path_levels;
   int n1, base2, n2, first_multi;
   int per_chunk;                   // (a, s) samples per thread between drains
@@ -617,6 +619,13 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 //    committing once its roulette fails; the walk ends when no lane is alive.
 //    No queue, no sort, no result slots: residuals accumulate in (a, s) order.
 constexpr int kWarpBlock = 256;
+#ifdef FSB_WARP_STATS
+__device__ unsigned long long g_warp_stats[8];
+#define WSTAT(i, v) \
+  if (lane == 0) atomicAdd(&g_warp_stats[i], (unsigned long long)(v))
+#else
+#define WSTAT(i, v)
+#endif
 #ifndef FSB_WARP_MINB
 #define FSB_WARP_MINB 4
 #endif
@@ -655,6 +664,9 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
 #define s_b2(i) sh_i[o_b2 + (i)]
 #define s_lut(i) sh_u16[o_lut + (i)]
 #define s_p2(i) sh_f4[o_p2 + (i)]
+  const int o_int = o_lut + n1 * (kLut + 1), o_leaf = o_int + n1;  // 2 B subdomain lists
+#define s_int(i) sh_u16[o_int + (i)]
+#define s_leaf(i) sh_u16[o_leaf + (i)]
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < n1; i += kWarpBlock) {
     s_cm1(i) = V.cm[1 + i];
@@ -690,12 +702,17 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     }
     s_lut(i) = (unsigned short)c;
   }
-  int seen_base = n1, n_int = 0;
+  // internal subdomains (sampled) and leaf subdomains (exact), in order
+  int seen_base = n1, n_int = 0, n_leaf = 0;
   for (int a = 0; a < n1; ++a) {
     const int4 tpa = s_tp1(a);
     if (tpa.y > 0) {
       seen_base += S * (tpa.y + 1);
+      if (tid == 0) s_int(n_int) = (unsigned short)a;
       ++n_int;
+    } else {
+      if (tid == 0) s_leaf(n_leaf) = (unsigned short)a;
+      ++n_leaf;
     }
   }
   __syncthreads();
@@ -703,13 +720,18 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   const uint64_t hseed = mix64(seed + kGamma);
   const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
   const float2 w0 = make_float2(0.f, 0.f);
-  const int nslot = n1 * S;
+  const int nslot = n_int * S;
   const int64_t nchunks = (n + 31) / 32;
+  // 32-query chunks from a global counter; the next chunk is claimed one chunk
+  // ahead so the atomic's latency hides behind the current chunk
+  unsigned int next = 0;
+  if (lane == 0) next = atomicAdd(chunk_ctr, 1u);
+  next = __shfl_sync(0xffffffffu, next, 0);
   while (true) {
-    unsigned int ch = 0;
-    if (lane == 0) ch = atomicAdd(chunk_ctr, 1u);
-    ch = __shfl_sync(0xffffffffu, ch, 0);
+    const unsigned int ch = next;
     if ((int64_t)ch >= nchunks) break;
+    unsigned int claim = 0;
+    if (lane == 0) claim = atomicAdd(chunk_ctr, 1u);
     const int64_t t = (int64_t)ch * 32 + lane;
     const bool live = t < n;
     const int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
@@ -726,23 +748,25 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
                    nz = make_float2(-qz, -qz);
       const float f2 = kp.dfloor_f * kp.dfloor_f;
       const float2 fl2 = make_float2(f2, f2);
-      int k = 0;
-      for (; k < np2; k += 8) {
+      auto pair_term = [&](int i, float2 a) {
+        const float4 A = s_p2(2 * i), B = s_p2(2 * i + 1);
+        const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
+        const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
+        const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
+        const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
+        const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+        return __ffma2_rn(make_float2(B.z, B.w), ri, a);
+      };
+      for (int k = 0; k < np2; k += 8) {  // FP32 partials over 16 records
         const int e = min(k + 8, np2);
         float2 a0 = make_float2(0.f, 0.f), a1 = a0;
-#pragma unroll 4
-        for (int i = k; i < e; ++i) {
-          const float4 A = s_p2(2 * i), B = s_p2(2 * i + 1);
-          const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
-          const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
-          const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
-          const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
-          const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
-          if (i & 1)
-            a1 = __ffma2_rn(make_float2(B.z, B.w), ri, a1);
-          else
-            a0 = __ffma2_rn(make_float2(B.z, B.w), ri, a0);
+        int i = k;
+#pragma unroll 2
+        for (; i + 1 < e; i += 2) {
+          a0 = pair_term(i, a0);
+          a1 = pair_term(i + 1, a1);
         }
+        if (i < e) a0 = pair_term(i, a0);
         acc += (double)((a0.x + a0.y) + (a1.x + a1.y));
       }
     } else if (!l2_multi) {
@@ -777,10 +801,10 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
         acc += (double)v;
       }
     }
-    for (int a_ord = 0; a_ord < n1; ++a_ord) {  // leaf subdomains: exact, never sampled
+    for (int l = 0; l < n_leaf; ++l) {  // leaf subdomains: exact, never sampled
+      const int a_ord = s_leaf(l);
       const int4 tpa = s_tp1(a_ord);
-      if (tpa.y == 0)
-        acc += (double)((tpa.w - tpa.z > 1)
+      acc += (double)((tpa.w - tpa.z > 1)
                             ? leaf_exact<KID>(V, tpa.z, tpa.w, qx, qy, qz, kp)
                             : fterm<KID>(s_cm1(a_ord), KID == KID_WINDING ? s_w1(a_ord) : w0, qx,
                                          qy, qz, kp));
@@ -796,9 +820,10 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
       {
         const int f = f0 + lane;
         if (f < nslot) {
-          const int a_ord = f / S, sm = f - a_ord * S;
+          const int ai = f / S, sm = f - ai * S;
+          const int a_ord = s_int(ai);
           const int4 tpa = s_tp1(a_ord);
-          if (tpa.y > 0) {
+          {
             const uint64_t hs = key_fold(key_fold(hq, (uint64_t)a_ord), (uint64_t)sm);
             const uint64_t ki = key_fold(hs, 0);
             my_kr = key_fold(hs, 1);
@@ -834,7 +859,9 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
         float prr = rr_fast_t<RR>(fdist(s_cm1(a_ord), qx, qy, qz) * id1, rp);
         const float ua = __shfl_sync(0xffffffffu, u_l, 0);
         bool alive = live && (RR == 2 || prr >= 1.f || ua < prr);
+        WSTAT(6, 1);
         if (!__any_sync(0xffffffffu, alive)) continue;
+        WSTAT(0, 1);
         if (alive) ++steps;
         float cvn = fterm<KID>(c2, KID == KID_WINDING ? s_w2(lo) : w0, qx, qy, qz, kp);
         const int2 t2 = s_t2(lo);
@@ -847,11 +874,25 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
           float ks0 = 0.f, ks1 = 0.f;
           int le = 0, c = 0;
           const unsigned am = __ballot_sync(0xffffffffu, alive);
-          if (FSB_WARP_SERIAL && !cmulti && lvl < V.path_levels &&
+          const bool use_path = !cmulti && lvl < V.path_levels;
+          WSTAT(1, 1);
+          WSTAT(2, __popc(am));
+          WSTAT(5, tp.y);
+          WSTAT(7, __popc(am) * tp.y);
+          // with the path, the picked child is known up front: its record and
+          // topology load while the children are summed
+          int4 tpn = make_int4(0, 0, 0, 0);
+          float4 cch = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (use_path) {
+            le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
+            tpn = V.topo[tp.x + le - 1];
+            cch = V.cm[tp.x + le - 1];
+          }
+          if (FSB_WARP_SERIAL && use_path &&
               __popc(am) * (((tp.y + 31) >> 5) * 11 + 14) < tp.y * 10) {
             // few live queries: one at a time, lanes over the children, then a
             // butterfly sum (work ~ live queries x children, not 32 x children)
-            le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
+            WSTAT(4, 1);
             for (unsigned mm = am; mm; mm &= mm - 1) {
               const int src = __ffs(mm) - 1;
               const float sx = __shfl_sync(0xffffffffu, qx, src),
@@ -865,8 +906,41 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
               for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
               if (lane == src) ks0 = part;
             }
-          } else if (!cmulti && lvl < V.path_levels) {
-            le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
+          } else if (kPack && use_path) {
+            // packed children: node pairs (2i, 2i+1) in one 32-byte load, two
+            // terms per FADD2/FFMA2 (floor as r2 + floor^2)
+            const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy),
+                         nz = make_float2(-qz, -qz);
+            const float f2 = kp.dfloor_f * kp.dfloor_f;
+            const float2 fl2 = make_float2(f2, f2);
+            float2 a2 = make_float2(0.f, 0.f), b2 = a2;
+            const int e = tp.x + tp.y;
+            int r = tp.x;
+            if (r & 1) {
+              ks0 += fterm<KID>(V.cm[r], w0, qx, qy, qz, kp);
+              ++r;
+            }
+            auto pair_acc = [&](int rr, float2 acc2) {
+              float4 A, B;
+              ld_pair(V.cmp + rr, A, B);  // rr even: records rr, rr + 1
+              const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
+              const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
+              const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
+              const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
+              const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+              return __ffma2_rn(make_float2(B.z, B.w), ri, acc2);
+            };
+            for (; r + 3 < e; r += 4) {
+              a2 = pair_acc(r, a2);
+              b2 = pair_acc(r + 2, b2);
+            }
+            if (r + 1 < e) {
+              a2 = pair_acc(r, a2);
+              r += 2;
+            }
+            if (r < e) ks0 += fterm<KID>(V.cm[r], w0, qx, qy, qz, kp);
+            ks1 = (a2.x + a2.y) + (b2.x + b2.y);
+          } else if (use_path) {
             if (tp.x & 1) {
               ks0 += fterm<KID>(V.cm[tp.x], KID == KID_WINDING ? V.m12[tp.x] : w0, qx, qy, qz, kp);
               c = 1;
@@ -903,7 +977,10 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             }
           }
           const int cidx = tp.x + le - 1;
-          const float4 cch = V.cm[cidx];
+          if (!use_path) {
+            cch = V.cm[cidx];
+            tpn = V.topo[cidx];
+          }
           if (alive) {
             seen += tp.y + 1;
             const float pagg = (float)(tp.w - tp.z) / (float)count_a;
@@ -922,12 +999,13 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             prr *= p;
             rp = rc;
           }
-          tp = V.topo[cidx];
+          tp = tpn;
           ++lvl;
         }
         acc_deep += (double)resid;
       }
     }
+    next = __shfl_sync(0xffffffffu, claim, 0);
     if (live) {
       out[qi] = (float)(acc + acc_deep / (double)S);
       if (visited) visited[qi] = seen;
@@ -944,6 +1022,8 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
 #undef s_b2
 #undef s_lut
 #undef s_p2
+#undef s_int
+#undef s_leaf
 }
 
 // returns 1 if the fast path does not apply (caller falls back), 0 on launch
@@ -965,6 +1045,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   V.pb = t->pts32b;
   FS_TRY(ensure_path(t, s));
   V.path = t->pt_path;
+  V.cmp = nullptr;
   V.path_bits = t->path_bits;
   V.path_levels = t->path_levels;
   V.n1 = t->root_kids;
@@ -1024,10 +1105,14 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     return 1;
   }
   if (share == 5 && (qoff & 31) == 0 && !std::getenv("FSB_STO_WARP_OFF")) {
+    if (kid == KID_COULOMB && FSB_WARP_DENSE2) {
+      FS_TRY(ensure_pairs(t, s));
+      V.cmp = t->lo_cmp;
+    }
     // warp-shared streams on warp-aligned groups: the warp-uniform kernel
     const size_t wsmem =
         ((16 * (2 * n1 + n2 + (kid == KID_COULOMB && FSB_WARP_DENSE2 ? 2 * ((n2 + 1) / 2) : 0)) +
-          8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 1)) +
+          8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 3)) +
          15) & ~(size_t)15;
     auto launch_w = [&](auto kern) -> int {
       if (wsmem > 48 * 1024)
@@ -1038,10 +1123,24 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
       Scratch ctr;
       FS_TRY(ctr.alloc(sizeof(unsigned int), s));
       FS_CK(cudaMemsetAsync(ctr.p, 0, sizeof(unsigned int), s));
+#ifdef FSB_WARP_STATS
+      unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      FS_CK(cudaMemcpyToSymbolAsync(g_warp_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
+#endif
       kern<<<(unsigned)grid, kWarpBlock, wsmem, s>>>(V, q, n, qperm, n_samples, seed, qoff, kp,
                                                      ctr.as<unsigned int>(), out, visited,
                                                      path_steps, path_count);
       FS_CK(cudaGetLastError());
+#ifdef FSB_WARP_STATS
+      FS_CK(cudaMemcpyFromSymbolAsync(z, g_warp_stats, sizeof(z), 0, cudaMemcpyDeviceToHost, s));
+      FS_CK(cudaStreamSynchronize(s));
+      const double nw = (double)((n + 31) / 32);
+      fprintf(stderr,
+              "warp stats per 32-query chunk: pairs %.1f, walks %.1f, levels %.1f (serial %.1f), "
+              "live lanes/level %.2f, children/level %.1f, useful child evals %.0f of %.0f\n",
+              z[6] / nw, z[0] / nw, z[1] / nw, z[4] / nw, (double)z[2] / std::max(1ull, z[1]),
+              (double)z[5] / std::max(1ull, z[1]), z[7] / nw, 32.0 * z[5] / nw);
+#endif
       return 0;
     };
     switch (kid * 3 + rr_mode) {

@@ -58,6 +58,9 @@ struct FsTree {
   float4* lo_cm32 = nullptr;     // {cx, cy, cz, m0} per level-order node
   float2* lo_m12_32 = nullptr;   // {m1, m2} (winding)
   int32_t* lo_begin = nullptr;   // point-range begin per level-order node
+  // Coulomb records of node pairs (2i, 2i+1) interleaved for packed FP32 math:
+  // {x0, x1, y0, y1}, {z0, z1, -m0, -m1} (ensure_pairs)
+  float4* lo_cmp = nullptr;
   // per (permuted) point: rank of its ancestor among its siblings at levels
   // 1..path_levels, path_bits bits per level (child pick without begins)
   uint64_t* pt_path = nullptr;

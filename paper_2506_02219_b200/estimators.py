@@ -174,8 +174,8 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
             # the paper's recipe: shuffled evaluation order, 32 consecutive
             # positions share one stream (fsb_stochastic_batch_shared)
             order = dev.empty(n, torch.int32)
-            _lib.check(L.fsb_shuffle_order(n, int(config.seed) & ((1 << 64) - 1), _vp(order),
-                                           _sp()))
+            _lib.check(L.fsb_shuffle_order(n, int(config.seed) & ((1 << 64) - 1),
+                                           int(query_offset), _vp(order), _sp()))
             _lib.check(L.fsb_stochastic_batch_shared(
                 h, kid, alpha, dfloor, prec, _vp(q), n, _vp(order),
                 int(config.samples_per_subdomain), _RR_CODES[config.rr_mode],
@@ -240,9 +240,6 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
     a slab of a larger query set evaluates exactly as inside the whole set.
     """
     _check_channels(sources, kernel)
-    if config.method == "stochastic" and getattr(config, "rng_sharing", "query") == "warp":
-        return evaluate_field_device(config, sources, kernel, queries, tree,
-                                     query_offset=query_offset).to_host()
     L = _lib.lib()
     torch = dev.torch()
     q = np.ascontiguousarray(queries.positions, dtype=np.float64)
@@ -259,6 +256,9 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
     args.query_offset = int(query_offset)
     args.smooth = 1 if kernel.kind == "smooth_exp" else 0
     args.query_order = 1
+    # the paper's warp-shared streams (shuffled windows, fsb_shuffle_order)
+    args.rng_group_log2 = 5 if (config.method == "stochastic"
+                                and getattr(config, "rng_sharing", "query") == "warp") else 0
     h = None
     keep = []
     if config.method == "brute_force":

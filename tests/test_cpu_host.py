@@ -35,7 +35,7 @@ def test_abi_library_loads_and_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert set(names) == set(_lib.SIGNATURES), "ctypes signatures must cover the header"
     L = _lib.load(build_if_missing=False)
-    assert L.fsb_abi_version() == 1
+    assert L.fsb_abi_version() == 2
 
 
 def test_abi_validates_arguments_without_touching_the_gpu():
@@ -75,6 +75,7 @@ def test_host_pipeline_validates_arguments_without_touching_the_gpu():
     assert call(method=0) == 1 and b"brute force" in L.fsb_last_error()  # needs device sources
     assert call(method=1, beta=0.0) == 1
     assert call(rr_mode=7) == 1
+    assert call(rng_group_log2=21) == 1
 
 
 def test_no_cpu_fallback():

@@ -197,20 +197,51 @@ def test_warp_kernel_tracks_fp64_shared_kernel(fs, case, kind, rr):
                 assert same.all()
 
 
-def test_shuffle_order_is_a_seeded_permutation(fs):
+def test_shuffle_order_is_a_seeded_window_local_permutation(fs):
+    """fsb_shuffle_order: a permutation mapping every 2^15-position window onto
+    itself, deterministic in (seed, query_offset), different across seeds and
+    window keys."""
     from paper_2506_02219_b200 import _device as dev, _lib
     import ctypes as C
-    L = _lib.lib()
     import torch
-    for n in (1, 2, 31, 1000, 65537):
-        outs = []
-        for seed in (5, 5, 6):
-            p = dev.empty(n, torch.int32)
-            _lib.check(L.fsb_shuffle_order(n, seed, C.c_void_p(dev.ptr(p)),
-                                           C.c_void_p(dev.stream_ptr())))
-            outs.append(p.cpu().numpy())
-        np.testing.assert_array_equal(np.sort(outs[0]), np.arange(n))
-        np.testing.assert_array_equal(outs[0], outs[1])
+    L = _lib.lib()
+    W = 1 << 15
+
+    def order(n, seed, off=0):
+        p = dev.empty(n, torch.int32)
+        _lib.check(L.fsb_shuffle_order(n, seed, off, C.c_void_p(dev.ptr(p)),
+                                       C.c_void_p(dev.stream_ptr())))
+        return p.cpu().numpy().astype(np.int64)
+
+    for n in (1, 2, 31, 1000, 2 * W + 17):
+        a, b, c = order(n, 5), order(n, 5), order(n, 6)
+        np.testing.assert_array_equal(np.sort(a), np.arange(n))
+        np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(a // W, np.arange(n) // W)  # window-local
         if n > 31:
-            assert (outs[0] != outs[2]).mean() > 0.9
-            assert (outs[0] != np.arange(n)).mean() > 0.9
+            assert (a != c).mean() > 0.9 and (a != np.arange(n)).mean() > 0.9
+    # a window-aligned slab with its offset reproduces the whole call's order
+    whole = order(3 * W, 9)
+    np.testing.assert_array_equal(order(W, 9, off=2 * W), whole[2 * W:] - 2 * W)
+    assert (order(W, 9, off=W) != whole[:W]).mean() > 0.9
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_warp_mode_host_pipeline_equals_device_path(fs, prec):
+    """evaluate_field (host pipeline, window-aligned slabs, any slab count) gives
+    the device path's warp-shared results bit for bit, counters included."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    s = scenes.build_sources(dict(kind="mesh_torus", m=30000, seed=3))
+    kern = fs.KernelSpec("coulomb")
+    rng = np.random.default_rng(4)
+    q = rng.uniform(-0.6, 0.6, (3 * (1 << 15) + 1000, 3))
+    t = fs.build_tree(s, 4)
+    cfg = fs.EstimatorConfig("stochastic", seed=21, precision=prec, rng_sharing="warp")
+    ref = evaluate_field_device(cfg, s, kern, dev.to_device(q), t, query_offset=64).to_host()
+    for chunks in (1, 2, 3, 8):
+        r = fs.evaluate_field(cfg, s, kern, fs.QuerySet(q), tree=t, chunks=chunks,
+                              query_offset=64)
+        np.testing.assert_array_equal(r.raw, ref.raw)
+        np.testing.assert_array_equal(r.path_steps, ref.path_steps)
+        np.testing.assert_array_equal(r.visited_nodes, ref.visited_nodes)
