@@ -120,9 +120,9 @@ int fsb_telescoping_batch(fsb_tree *tree, int kid, double alpha, double dfloor, 
 int fsb_query_order(const double *queries, int64_t n, int32_t *perm_out, void *stream);
 
 /* Seeded evaluation order of the paper's RNG-sharing groups: perm_out (n,) int32,
- * a permutation of 0..n-1 that maps every window of 2^15 consecutive positions
+ * a permutation of 0..n-1 that maps every window of 2^16 consecutive positions
  * onto itself (window w: a 4-round Feistel network keyed on (seed,
- * query_offset + w * 2^15), cycle-walked into the window; one kernel, no sort).
+ * query_offset + w * 2^16), cycle-walked into a partial window; one kernel).
  * Window-local order lets evaluate_field_host pipeline window-aligned slabs. */
 int fsb_shuffle_order(int64_t n, uint64_t seed, int64_t query_offset, int32_t *perm_out,
                       void *stream);

@@ -121,36 +121,58 @@ int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s) {
 // seeded pseudo-random evaluation order (the paper shuffles the query grid so that
 // RNG-sharing groups are spatially scattered)
 // Seeded evaluation order of the warp-shared mode: positions are cut into
-// windows of kShuffleWindow, and window w (positions [wW, min((w+1)W, n)))
-// is permuted by a 4-round balanced Feistel network keyed on (seed,
-// query_offset + wW) over the smallest 2^(2h) >= its size, cycle-walked back
-// into range (a bijection; < 4 walking rounds on average).  One pass, no sort.
+// windows of kShuffleWindow = 2^16, and window w (positions [wW, min((w+1)W, n)))
+// is permuted by a 4-round balanced Feistel network (32-bit lowbias32 rounds)
+// keyed on (seed, query_offset + wW) over the smallest 2^(2h) >= its size
+// (exactly 2^16 for full windows), cycle-walked back into range for the last
+// partial window (a bijection).  One pass, no sort.
 // Windows keep the order slab-local, so the host pipeline can copy, evaluate
 // and return window-aligned slabs independently (same result as one launch).
-__device__ __forceinline__ uint64_t feistel4(uint64_t x, int hb, const uint64_t (&ks)[4]) {
-  const uint64_t mask = (1ull << hb) - 1ull;
-  uint64_t l = x >> hb, r = x & mask;
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {  // lowbias32 finalizer
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  return x ^ (x >> 16);
+}
+
+__device__ __forceinline__ uint32_t feistel4(uint32_t x, int hb, const uint32_t (&ks)[4]) {
+  const uint32_t mask = (1u << hb) - 1u;
+  uint32_t l = x >> hb, r = x & mask;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const uint64_t f = mix64(ks[i] ^ r) & mask;
-    const uint64_t nl = r;
+    const uint32_t f = hash32(ks[i] ^ r) & mask;
+    const uint32_t nl = r;
     r = l ^ f;
     l = nl;
   }
   return (l << hb) | r;
 }
 
-__global__ void k_shuffle(int64_t n, uint64_t h, int64_t qoff, int32_t* __restrict__ perm) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// blocks of 256 positions never straddle a window (kShuffleWindow % 256 == 0):
+// thread 0 derives the window's round keys once per block
+__global__ void __launch_bounds__(256) k_shuffle(int64_t n, uint64_t h, int64_t qoff,
+                                                 int32_t* __restrict__ perm) {
+  __shared__ uint32_t s_ks[4];
+  const int64_t b0 = blockIdx.x * (int64_t)blockDim.x;
+  const int64_t base = b0 & ~(int64_t)(kShuffleWindow - 1);
+  if (threadIdx.x == 0) {
+    const uint64_t hw = key_fold(h, (uint64_t)(qoff + base));
+    const uint64_t hw1 = key_fold(hw, 1);
+    s_ks[0] = (uint32_t)hw;
+    s_ks[1] = (uint32_t)(hw >> 32);
+    s_ks[2] = (uint32_t)hw1;
+    s_ks[3] = (uint32_t)(hw1 >> 32);
+  }
+  __syncthreads();
+  const int64_t i = b0 + threadIdx.x;
   if (i >= n) return;
-  const int64_t base = i & ~(int64_t)(kShuffleWindow - 1);
-  const int64_t size = min((int64_t)kShuffleWindow, n - base);
-  int hb = 1;
-  while ((1ll << (2 * hb)) < size) ++hb;
-  const uint64_t hw = key_fold(h, (uint64_t)(qoff + base));
-  const uint64_t ks[4] = {key_fold(hw, 0), key_fold(hw, 1), key_fold(hw, 2), key_fold(hw, 3)};
-  uint64_t y = feistel4((uint64_t)(i - base), hb, ks);
-  while (y >= (uint64_t)size) y = feistel4(y, hb, ks);
+  const uint32_t size = (uint32_t)min((int64_t)kShuffleWindow, n - base);
+  int hb = 1;  // full windows: 2^(2 hb) == size, no cycle walking
+  while ((1u << (2 * hb)) < size) ++hb;
+  const uint32_t ks[4] = {s_ks[0], s_ks[1], s_ks[2], s_ks[3]};
+  uint32_t y = feistel4((uint32_t)(i - base), hb, ks);
+  while (y >= size) y = feistel4(y, hb, ks);
   perm[i] = (int32_t)(base + (int64_t)y);
 }
 

@@ -540,8 +540,8 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
             const int cidx = tp.x + le - 1;
             const float4 cch = V.cm[cidx];  // L1 hit: just streamed
             atomicAdd(&s_seen(owner), tp.y + 1);
-            const float pagg = (float)(tp.w - tp.z) / (float)count_a;
-            resid += (ks - cvn) * rcp_ftz(pagg * prr);
+            // swap / (p_agg * p_rr), p_agg = points(node) / points(a)
+            resid += (ks - cvn) * ((float)count_a * rcp_ftz((float)(tp.w - tp.z) * prr));
             const float rc =
                 fdist(cch, qq.x, qq.y, qq.z) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
             const float p = rr_fast_t<RR>(rp, rc);
@@ -635,6 +635,10 @@ __device__ unsigned long long g_warp_stats[8];
 #ifndef FSB_WARP_SERIAL
 #define FSB_WARP_SERIAL 1
 #endif
+#ifndef FSB_WARP_DENSE_UNROLL
+#define FSB_WARP_DENSE_UNROLL 4
+#endif
+constexpr int kDenseUnroll = FSB_WARP_DENSE_UNROLL;
 
 template <int KID, int RR>
 __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
         const int e = min(k + 8, np2);
         float2 a0 = make_float2(0.f, 0.f), a1 = a0;
         int i = k;
-#pragma unroll 2
+#pragma unroll kDenseUnroll
         for (; i + 1 < e; i += 2) {
           a0 = pair_term(i, a0);
           a1 = pair_term(i + 1, a1);
@@ -817,6 +821,8 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
       // _core.py:166-169, level-1 step from shared memory
       int my_a = -1, my_lo = 0, my_j = 0;
       uint64_t my_kr = 0;
+      float my_u0 = 0.f, my_u1 = 0.f, my_u2 = 0.f;  // roulette draws, counters 0..2
+      uint64_t my_path = 0;  // the sampled point's sibling ranks (loaded early)
       {
         const int f = f0 + lane;
         if (f < nslot) {
@@ -839,6 +845,12 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             my_a = a_ord;
             my_lo = k0 + c;
             my_j = j;
+            my_path = V.path[j];
+            if (RR != 2) {
+              my_u0 = draw24(my_kr, 0);
+              my_u1 = draw24(my_kr, 1);
+              my_u2 = draw24(my_kr, 2);
+            }
           }
         }
       }
@@ -850,14 +862,14 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
         const int jj = __shfl_sync(0xffffffffu, my_j, i);
         const uint64_t kr = ((uint64_t)__shfl_sync(0xffffffffu, (unsigned)(my_kr >> 32), i) << 32) |
                             __shfl_sync(0xffffffffu, (unsigned)my_kr, i);
-        // roulette uniforms of this walk: lane L holds the draw with counter L
-        const float u_l = RR == 2 ? 0.f : draw24(kr, (uint64_t)lane);
+        const float u1 = __shfl_sync(0xffffffffu, my_u1, i),
+                    u2 = __shfl_sync(0xffffffffu, my_u2, i);
         const int4 tpa = s_tp1(a_ord);
-        const int count_a = tpa.w - tpa.z;
+        const float fcount_a = (float)(tpa.w - tpa.z);
         const float4 c2 = s_cm2(lo);
         float rp = fdist(c2, qx, qy, qz) * id2;
         float prr = rr_fast_t<RR>(fdist(s_cm1(a_ord), qx, qy, qz) * id1, rp);
-        const float ua = __shfl_sync(0xffffffffu, u_l, 0);
+        const float ua = __shfl_sync(0xffffffffu, my_u0, i);
         bool alive = live && (RR == 2 || prr >= 1.f || ua < prr);
         WSTAT(6, 1);
         if (!__any_sync(0xffffffffu, alive)) continue;
@@ -866,7 +878,9 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
         float cvn = fterm<KID>(c2, KID == KID_WINDING ? s_w2(lo) : w0, qx, qy, qz, kp);
         const int2 t2 = s_t2(lo);
         int4 tp = make_int4(t2.x & 0x1ffffff, (int)((unsigned)t2.x >> 25), 0, t2.y);
-        const uint64_t path = V.path[jj];
+        const uint64_t path =
+            ((uint64_t)__shfl_sync(0xffffffffu, (unsigned)(my_path >> 32), i) << 32) |
+            __shfl_sync(0xffffffffu, (unsigned)my_path, i);
         int lvl = 2;
         float resid = 0.f;
         while (tp.y > 0) {  // warp-uniform: every lane walks the same node
@@ -981,16 +995,16 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             cch = V.cm[cidx];
             tpn = V.topo[cidx];
           }
-          if (alive) {
+          if (alive) {  // swap / (p_agg * p_rr), p_agg = points(node) / points(a)
             seen += tp.y + 1;
-            const float pagg = (float)(tp.w - tp.z) / (float)count_a;
-            resid += ((ks0 + ks1) - cvn) * rcp_ftz(pagg * prr);
+            resid += ((ks0 + ks1) - cvn) * (fcount_a * rcp_ftz((float)(tp.w - tp.z) * prr));
           }
           const float rc = fdist(cch, qx, qy, qz) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
           const float p = rr_fast_t<RR>(rp, rc);
-          const int ctr = lvl - 1;  // levels descended so far
-          const float u = ctr < 32 ? __shfl_sync(0xffffffffu, u_l, ctr & 31)
-                                   : (RR == 2 ? 0.f : draw24(kr, (uint64_t)ctr));
+          const int ctr = lvl - 1;  // levels descended so far (uniform)
+          const float u = ctr == 1 ? u1
+                          : ctr == 2 ? u2
+                                     : (RR == 2 ? 0.f : draw24(kr, (uint64_t)ctr));
           alive = alive && (RR == 2 || p >= 1.f || u < p);
           if (!__any_sync(0xffffffffu, alive)) break;
           if (alive) {

@@ -198,14 +198,14 @@ def test_warp_kernel_tracks_fp64_shared_kernel(fs, case, kind, rr):
 
 
 def test_shuffle_order_is_a_seeded_window_local_permutation(fs):
-    """fsb_shuffle_order: a permutation mapping every 2^15-position window onto
+    """fsb_shuffle_order: a permutation mapping every 2^16-position window onto
     itself, deterministic in (seed, query_offset), different across seeds and
     window keys."""
     from paper_2506_02219_b200 import _device as dev, _lib
     import ctypes as C
     import torch
     L = _lib.lib()
-    W = 1 << 15
+    W = 1 << 16
 
     def order(n, seed, off=0):
         p = dev.empty(n, torch.int32)
@@ -235,7 +235,7 @@ def test_warp_mode_host_pipeline_equals_device_path(fs, prec):
     s = scenes.build_sources(dict(kind="mesh_torus", m=30000, seed=3))
     kern = fs.KernelSpec("coulomb")
     rng = np.random.default_rng(4)
-    q = rng.uniform(-0.6, 0.6, (3 * (1 << 15) + 1000, 3))
+    q = rng.uniform(-0.6, 0.6, (3 * (1 << 16) + 1000, 3))
     t = fs.build_tree(s, 4)
     cfg = fs.EstimatorConfig("stochastic", seed=21, precision=prec, rng_sharing="warp")
     ref = evaluate_field_device(cfg, s, kern, dev.to_device(q), t, query_offset=64).to_host()
