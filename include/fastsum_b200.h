@@ -79,6 +79,18 @@ int fsb_barnes_hut_batch(fsb_tree *tree, int kid, double alpha, double dfloor, i
                          const double *queries, int64_t n, const int32_t *qperm, double beta,
                          void *out, int64_t *visited, void *stream);
 
+/* The paper's GPU Barnes-Hut, not the reference's: warp voting.
+ * Queries are grouped as 32 consecutive positions of `order` (NULL: 0..n-1); a
+ * node is accepted for the whole group (each query adds its _node_term) when it
+ * is a leaf or every query of the group sees ffr >= beta, and opened for the
+ * whole group otherwise, so a group walks one preorder sequence: more accurate
+ * than per-query BH at the same beta, no divergence.  visited = nodes walked
+ * by the group.  FP64 matches the oracle restatement bitwise. */
+int fsb_barnes_hut_vote_batch(fsb_tree *tree, int kid, double alpha, double dfloor,
+                              int precision, const double *queries, int64_t n,
+                              const int32_t *order, double beta, void *out, int64_t *visited,
+                              void *stream);
+
 /* stochastic_batch(*core, kid, alpha, dfloor, queries, n_samples, rr_mode, seed,
  * query_offset, out, visited, path_steps, path_count) -- _core.py:215-267.
  * RNG streams are keyed on (seed, query index + query_offset, subdomain, sample). */
@@ -167,6 +179,8 @@ typedef struct fsb_eval_args {
   int c;
   int rng_group_log2;     /* stochastic: 0 = per-query streams (reference); 5 = the
                              paper's warp-shared streams over fsb_shuffle_order */
+  int bh_warp_vote;       /* barnes_hut: warp voting over the evaluation order
+                             (fsb_barnes_hut_vote_batch; evaluated as one slab) */
 } fsb_eval_args;
 
 int fsb_evaluate_field_host(fsb_tree *tree, const fsb_eval_args *args, const double *queries,

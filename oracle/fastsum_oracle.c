@@ -261,14 +261,18 @@ static inline double sample_residual(const tree_t *t, int kid, double alpha, dou
     return resid;
 }
 
-/* stochastic_batch, _core.py:215-267 */
-void or_stochastic_batch(const double *diam, const double *agg_mass, const double *com,
-                         const int64_t *cs, const int64_t *cc, const int64_t *ci,
-                         const int64_t *b, const int64_t *e, const double *pts,
-                         const double *ms, int64_t num_nodes, int c, int kid, double alpha,
-                         double dfloor, const double *q, int64_t n, int64_t n_samples,
-                         int rr_mode, uint64_t seed, int64_t query_offset, double *out,
-                         int64_t *visited, int64_t *path_steps, int64_t *path_count) {
+/* stochastic_batch, _core.py:215-267.  keys == NULL: query qi draws from the
+ * streams of index qi + query_offset (the reference).  keys != NULL: from the
+ * streams of index keys[qi] (the paper's shared streams: every query of a
+ * group carries the group's key). */
+static void stochastic_core(const double *diam, const double *agg_mass, const double *com,
+                            const int64_t *cs, const int64_t *cc, const int64_t *ci,
+                            const int64_t *b, const int64_t *e, const double *pts,
+                            const double *ms, int64_t num_nodes, int c, int kid, double alpha,
+                            double dfloor, const double *q, int64_t n, int64_t n_samples,
+                            int rr_mode, uint64_t seed, int64_t query_offset,
+                            const uint64_t *keys, double *out, int64_t *visited,
+                            int64_t *path_steps, int64_t *path_count) {
     tree_t t = mk_tree(diam, agg_mass, com, cs, cc, ci, b, e, pts, ms, num_nodes, c);
     int64_t root_kids = t.child_count[0];
 #pragma omp parallel for schedule(dynamic, 16)
@@ -298,8 +302,8 @@ void or_stochastic_batch(const double *diam, const double *agg_mass, const doubl
                 int64_t st, se;
                 double resid = sample_residual(&t, kid, alpha, dfloor, a, a_ord, count_a,
                                                delta_a, qx, qy, qz,
-                                               (uint64_t)(qi + query_offset), (uint64_t)s,
-                                               seed, rr_mode, &st, &se);
+                                               keys ? keys[qi] : (uint64_t)(qi + query_offset),
+                                               (uint64_t)s, seed, rr_mode, &st, &se);
                 fa += resid;
                 steps_total += st;
                 seen += se;
@@ -311,6 +315,95 @@ void or_stochastic_batch(const double *diam, const double *agg_mass, const doubl
         visited[qi] = seen;
         path_steps[qi] = steps_total;
         path_count[qi] = paths;
+    }
+}
+
+void or_stochastic_batch(const double *diam, const double *agg_mass, const double *com,
+                         const int64_t *cs, const int64_t *cc, const int64_t *ci,
+                         const int64_t *b, const int64_t *e, const double *pts,
+                         const double *ms, int64_t num_nodes, int c, int kid, double alpha,
+                         double dfloor, const double *q, int64_t n, int64_t n_samples,
+                         int rr_mode, uint64_t seed, int64_t query_offset, double *out,
+                         int64_t *visited, int64_t *path_steps, int64_t *path_count) {
+    stochastic_core(diam, agg_mass, com, cs, cc, ci, b, e, pts, ms, num_nodes, c, kid, alpha,
+                    dfloor, q, n, n_samples, rr_mode, seed, query_offset, NULL, out, visited,
+                    path_steps, path_count);
+}
+
+/* The paper's shared streams (not in the reference): query
+ * qi draws from the streams of index keys[qi]. */
+void or_stochastic_keyed_batch(const double *diam, const double *agg_mass, const double *com,
+                               const int64_t *cs, const int64_t *cc, const int64_t *ci,
+                               const int64_t *b, const int64_t *e, const double *pts,
+                               const double *ms, int64_t num_nodes, int c, int kid,
+                               double alpha, double dfloor, const double *q, int64_t n,
+                               int64_t n_samples, int rr_mode, uint64_t seed,
+                               const uint64_t *keys, double *out, int64_t *visited,
+                               int64_t *path_steps, int64_t *path_count) {
+    stochastic_core(diam, agg_mass, com, cs, cc, ci, b, e, pts, ms, num_nodes, c, kid, alpha,
+                    dfloor, q, n, n_samples, rr_mode, seed, 0, keys, out, visited, path_steps,
+                    path_count);
+}
+
+/* Warp-voting Barnes-Hut (Alg. 1 with the acceptance test voted
+ * over a group; not in the reference).  Queries are grouped as 32 consecutive
+ * positions of `order`; a group walks one DFS preorder (children pushed
+ * reversed, as _core.py:101-129): a node is accepted -- every query of the
+ * group adds its _node_term -- when it is a leaf or every query of the group
+ * sees ffr >= beta, and is opened for the whole group otherwise.  visited =
+ * nodes popped by the group. */
+void or_barnes_hut_vote_batch(const double *diam, const double *agg_mass, const double *com,
+                              const int64_t *cs, const int64_t *cc, const int64_t *ci,
+                              const int64_t *b, const int64_t *e, const double *pts,
+                              const double *ms, int64_t num_nodes, int c, int kid,
+                              double alpha, double dfloor, const double *q, int64_t n,
+                              const int32_t *order, double beta, double *out,
+                              int64_t *visited) {
+    tree_t t = mk_tree(diam, agg_mass, com, cs, cc, ci, b, e, pts, ms, num_nodes, c);
+    int64_t groups = (n + 31) / 32;
+#pragma omp parallel
+    {
+        int64_t *stack = (int64_t *)malloc(sizeof(int64_t) * (size_t)(num_nodes + 8));
+#pragma omp for schedule(dynamic, 4)
+        for (int64_t g = 0; g < groups; ++g) {
+            int64_t idx[32];
+            double acc[32];
+            int cnt = 0;
+            for (int64_t p = 32 * g; p < n && p < 32 * g + 32; ++p) {
+                idx[cnt] = order ? (int64_t)order[p] : p;
+                acc[cnt] = 0.0;
+                ++cnt;
+            }
+            int64_t top = 1, seen = 0;
+            stack[0] = 0;
+            while (top > 0) {
+                int64_t a = stack[--top];
+                seen += 1;
+                int accept = t.child_count[a] == 0;
+                if (!accept) {
+                    accept = 1;
+                    for (int k = 0; k < cnt && accept; ++k) {
+                        const double *qq = q + 3 * idx[k];
+                        accept = ffr(&t, a, qq[0], qq[1], qq[2]) >= beta;
+                    }
+                }
+                if (accept) {
+                    for (int k = 0; k < cnt; ++k) {
+                        const double *qq = q + 3 * idx[k];
+                        acc[k] += node_term(&t, kid, alpha, dfloor, a, qq[0], qq[1], qq[2]);
+                    }
+                } else {
+                    int64_t s0 = t.child_start[a];
+                    for (int64_t k = t.child_count[a] - 1; k >= 0; --k)
+                        stack[top++] = t.child_index[s0 + k];
+                }
+            }
+            for (int k = 0; k < cnt; ++k) {
+                out[idx[k]] = acc[k];
+                visited[idx[k]] = seen;
+            }
+        }
+        free(stack);
     }
 }
 

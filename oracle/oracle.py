@@ -150,6 +150,47 @@ def stochastic_batch(*args):
     path_count[:] = pc
 
 
+def stochastic_keyed_batch(*args):
+    """The paper's shared streams (not in the reference): stochastic_batch with query i
+    drawing from the streams of index keys[i]; args = core11 + (kid, alpha, dfloor,
+    queries, n_samples, rr_mode, seed, keys, out, visited, path_steps, path_count)."""
+    core11 = args[:11]
+    (kid, alpha, dfloor, queries, n_samples, rr_mode, seed, keys, out, visited,
+     path_steps, path_count) = args[11:]
+    keep, targs = _tree_args(core11)
+    q = _f64(queries)
+    n = q.shape[0]
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    res = np.zeros(n)
+    vis, st, pc = (np.zeros(n, dtype=np.int64) for _ in range(3))
+    lib().or_stochastic_keyed_batch(*targs, C.c_int(kid), C.c_double(alpha), C.c_double(dfloor),
+                                    _dp(q), C.c_int64(n), C.c_int64(n_samples), C.c_int(rr_mode),
+                                    C.c_uint64(int(seed)), k.ctypes.data_as(C.c_void_p),
+                                    _dp(res), _ip(vis), _ip(st), _ip(pc))
+    out[:] = res
+    visited[:] = vis
+    path_steps[:] = st
+    path_count[:] = pc
+
+
+def barnes_hut_vote_batch(*args):
+    """Warp-voting BH (not in the reference): groups of 32 consecutive
+    positions of `order`; args = core11 + (kid, alpha, dfloor, queries, order, beta, out,
+    visited)."""
+    core11, (kid, alpha, dfloor, queries, order, beta, out, visited) = args[:11], args[11:]
+    keep, targs = _tree_args(core11)
+    q = _f64(queries)
+    o = None if order is None else np.ascontiguousarray(order, dtype=np.int32)
+    res = np.zeros(q.shape[0])
+    vis = np.zeros(q.shape[0], dtype=np.int64)
+    lib().or_barnes_hut_vote_batch(*targs, C.c_int(kid), C.c_double(alpha), C.c_double(dfloor),
+                                   _dp(q), C.c_int64(q.shape[0]),
+                                   None if o is None else o.ctypes.data_as(C.c_void_p),
+                                   C.c_double(beta), _dp(res), _ip(vis))
+    out[:] = res
+    visited[:] = vis
+
+
 def stochastic_moments_batch(*args):
     """_core.py:270-336."""
     core11 = args[:11]

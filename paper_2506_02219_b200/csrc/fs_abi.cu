@@ -330,6 +330,20 @@ int fsb_barnes_hut_batch(fsb_tree* tree, int kid, double alpha, double dfloor, i
                          out, visited, S(stream));
 }
 
+int fsb_barnes_hut_vote_batch(fsb_tree* tree, int kid, double alpha, double dfloor,
+                              int precision, const double* queries, int64_t n,
+                              const int32_t* order, double beta, void* out, int64_t* visited,
+                              void* stream) {
+  ABI_TREE(tree);
+  if (int rc = check_common(kid, precision, n)) return rc;
+  if (!(beta > 0)) {
+    set_error("beta must be positive");
+    return 1;
+  }
+  return fsb::barnes_hut(tree->t, kid, alpha, dfloor, precision == 0, queries, n, order, beta,
+                         out, visited, S(stream), true);
+}
+
 int fsb_stochastic_batch(fsb_tree* tree, int kid, double alpha, double dfloor, int precision,
                          const double* queries, int64_t n, const int32_t* qperm,
                          int64_t n_samples, int rr_mode, uint64_t seed, int64_t query_offset,

@@ -77,7 +77,7 @@ __device__ __forceinline__ double bh_node_value(const BhSplitCtx& C, const float
 }
 
 // units [u0, u1): top-level chunks (items == false) or queued items (items == true)
-template <int KID, bool ITEMS>
+template <int KID, bool ITEMS, bool VOTE>
 __global__ void __launch_bounds__(128) k_bh_units(BhSplitCtx C, KParams kp, unsigned int u0,
                                                   unsigned int u1, unsigned int* __restrict__ work) {
   const int lane = threadIdx.x & 31;
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(128) k_bh_units(BhSplitCtx C, KParams kp, unsi
       ++iters;
       const bool mine = i == cur;
       float4 g = make_float4(0.f, 0.f, 0.f, 0.f), mm = g;
-      bool opens = false;
+      bool opens = false, accept = false;
       uint32_t skip = 0;
       if (mine) {
         g = C.rec[2 * (int64_t)cur];
@@ -130,7 +130,12 @@ __global__ void __launch_bounds__(128) k_bh_units(BhSplitCtx C, KParams kp, unsi
         const float dx = qx - g.x, dy = qy - g.y, dz = qz - g.z;
         const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
         const float thr = C.beta * fmaxf(g.w, 1e-12f);
-        if (leaf || d2 >= thr * thr) {
+        accept = leaf || d2 >= thr * thr;
+      }
+      // warp voting: open unless every live lane accepts
+      if (VOTE) accept = __all_sync(0xffffffffu, !mine || accept);
+      if (mine) {
+        if (accept) {
           acc += bh_node_value<KID>(C, g, mm, qx, qy, qz, kp);
           i = skip;
         } else {
@@ -204,7 +209,7 @@ static int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-template <int KID>
+template <int KID, bool VOTE>
 static int bh_split_launch(FsTree* t, const double* q, int64_t n, const int32_t* qperm,
                            double beta, KParams kp, float* out, int64_t* visited, int sms,
                            int cap, cudaStream_t s, bool* done, unsigned int* emitted) {
@@ -243,7 +248,8 @@ static int bh_split_launch(FsTree* t, const double* q, int64_t n, const int32_t*
   C.seen_item = sitem.as<int32_t>();
 
   int per_sm = 1;
-  FS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bh_units<KID, false>, 128, 0));
+  FS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bh_units<KID, false, VOTE>, 128,
+                                                      0));
   const int64_t max_grid = (int64_t)sms * std::max(per_sm, 1);
   auto run = [&](auto kern, unsigned int u0, unsigned int u1) -> int {
     FS_CK(cudaMemsetAsync(work.p, 0, sizeof(unsigned int), s));
@@ -253,7 +259,7 @@ static int bh_split_launch(FsTree* t, const double* q, int64_t n, const int32_t*
     FS_CK(cudaGetLastError());
     return 0;
   };
-  FS_TRY(run(k_bh_units<KID, false>, 0u, (unsigned int)nchunks));
+  FS_TRY(run(k_bh_units<KID, false, VOTE>, 0u, (unsigned int)nchunks));
   // follow-up launches walk the emitted items (which may emit more)
   unsigned int done_items = 0, h[2] = {0, 0};
   while (true) {
@@ -265,7 +271,7 @@ static int bh_split_launch(FsTree* t, const double* q, int64_t n, const int32_t*
     }
     const unsigned int total = std::min<unsigned int>(h[0], (unsigned int)C.cap);
     if (total == done_items) break;
-    FS_TRY(run(k_bh_units<KID, true>, done_items, total));
+    FS_TRY(run(k_bh_units<KID, true, VOTE>, done_items, total));
     done_items = total;
   }
   // order each chunk's items by subtree start (preorder) and fold
@@ -305,7 +311,7 @@ static int bh_split_launch(FsTree* t, const double* q, int64_t n, const int32_t*
 
 int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                      const int32_t* qperm, double beta, float* out, int64_t* visited,
-                     cudaStream_t s, bool* done) {
+                     cudaStream_t s, bool* done, bool vote) {
   KParams kp;
   kp.alpha = alpha;
   kp.dfloor = dfloor;
@@ -328,10 +334,16 @@ int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const doub
   for (int attempt = 0; attempt < 4; ++attempt) {
     unsigned int emitted = 0;
     int rc = 0;
-    switch (kid) {
-      case 0: rc = bh_split_launch<0>(t, q, n, qperm, beta, kp, out, visited, sms, (int)cap, s, done, &emitted); break;
-      case 1: rc = bh_split_launch<1>(t, q, n, qperm, beta, kp, out, visited, sms, (int)cap, s, done, &emitted); break;
-      default: rc = bh_split_launch<2>(t, q, n, qperm, beta, kp, out, visited, sms, (int)cap, s, done, &emitted); break;
+    auto go = [&](auto launch) {
+      return launch(t, q, n, qperm, beta, kp, out, visited, sms, (int)cap, s, done, &emitted);
+    };
+    switch (kid * 2 + (vote ? 1 : 0)) {
+      case 0: rc = go(bh_split_launch<0, false>); break;
+      case 1: rc = go(bh_split_launch<0, true>); break;
+      case 2: rc = go(bh_split_launch<1, false>); break;
+      case 3: rc = go(bh_split_launch<1, true>); break;
+      case 4: rc = go(bh_split_launch<2, false>); break;
+      default: rc = go(bh_split_launch<2, true>); break;
     }
     if (rc) return rc;
     if (std::getenv("FSB_BH_DEBUG"))

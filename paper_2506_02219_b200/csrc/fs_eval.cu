@@ -93,7 +93,7 @@ __device__ __forceinline__ double ffr(const typename Prec<F64>::V4& g, double qx
 // accept: skip[i]); a warp processes the union of its lanes' node sequences in
 // increasing preorder index, so every record load is one broadcast transaction
 // while each lane still sees exactly its own sequence (results unchanged).
-template <int KID, bool F64>
+template <int KID, bool F64, bool VOTE>
 __global__ void __launch_bounds__(128) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
                                             const typename Prec<F64>::V4* __restrict__ pa,
                                             const typename Prec<F64>::V4* __restrict__ pb,
@@ -123,11 +123,14 @@ __global__ void __launch_bounds__(128) k_bh(const typename Prec<F64>::V4* __rest
     while (true) {
       uint32_t cur = warp_min_u32(i);
       if (cur >= nn) break;
-      if (i == cur) {
-        V4 g = rec[2 * (int64_t)cur];
-        V4 mm = rec[2 * (int64_t)cur + 1];
+      const bool mine = i == cur;
+      V4 g, mm;
+      uint32_t skip = 0;
+      bool accept = false;
+      if (mine) {
+        g = rec[2 * (int64_t)cur];
+        mm = rec[2 * (int64_t)cur + 1];
         ++seen;
-        uint32_t skip;
         if constexpr (F64)
           skip = (uint32_t)__double_as_longlong(mm.w);
         else
@@ -143,7 +146,14 @@ __global__ void __launch_bounds__(128) k_bh(const typename Prec<F64>::V4* __rest
           float thr = beta_f * fmaxf(g.w, 1e-12f);
           far = d2 >= thr * thr;
         }
-        if (leaf || far) {
+        accept = leaf || far;
+      }
+      // warp voting: a node is accepted only when every live
+      // lane accepts it, else the whole warp opens it (all live lanes walk one
+      // sequence: more accurate per query, no divergence)
+      if (VOTE) accept = __all_sync(0xffffffffu, !mine || accept);
+      if (mine) {
+        if (accept) {
           double v;
           if (g.w < 0) {  // multi-point leaf: exact per-point sum
             int64_t b, e;
@@ -776,7 +786,7 @@ static LoTree<KID, F64> lo_view(const FsTree* t) {
 
 int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, double beta, void* out, int64_t* visited,
-               cudaStream_t s) {
+               cudaStream_t s, bool vote) {
   if (n <= 0) return 0;
   FS_TRY(ensure_bh(t, f64, s));
   FS_TRY(ensure_lo(t, f64, s));  // packed points for multi-point leaves
@@ -785,7 +795,7 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
   if (!f64 && !(split_env && split_env[0] == '0')) {  // load-balanced FP32 BH
     bool done = false;
     FS_TRY(barnes_hut_split(t, kid, alpha, dfloor, q, n, qperm, beta, (float*)out, visited, s,
-                            &done));
+                            &done, vote));
     if (done) return 0;
   }
   Scratch work;  // chunk counter of the persistent warps
@@ -805,14 +815,19 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
       pa = t->pts32a;
       pb = t->pts32b;
     }
-    int per_sm = 1, dev = 0;
-    cudaGetDevice(&dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bh<KID, F64>, 128, 0);
-    const int64_t grid =
-        std::min<int64_t>((n + 127) / 128, (int64_t)sm_count() * std::max(per_sm, 1));
-    k_bh<KID, F64><<<(unsigned)grid, 128, 0, s>>>(rec, pa, pb, (uint32_t)t->n, q, n, qperm, beta,
-                                                   kp, (typename Prec<F64>::Out*)out, visited,
-                                                   work.as<unsigned int>());
+    auto launch = [&](auto kern) {
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0);
+      const int64_t grid =
+          std::min<int64_t>((n + 127) / 128, (int64_t)sm_count() * std::max(per_sm, 1));
+      kern<<<(unsigned)grid, 128, 0, s>>>(rec, pa, pb, (uint32_t)t->n, q, n, qperm, beta, kp,
+                                          (typename Prec<F64>::Out*)out, visited,
+                                          work.as<unsigned int>());
+    };
+    if (vote)
+      launch(k_bh<KID, F64, true>);
+    else
+      launch(k_bh<KID, F64, false>);
   });
 }
 

@@ -12,9 +12,11 @@ int brute_force(int kid, double alpha, double dfloor, bool f64, const double* pt
 int brute_force_f32_acc64(int kid, double alpha, double dfloor, const double* pts,
                           const double* ms, int64_t m, int c, const double* q, int64_t n,
                           double* out, cudaStream_t s);
+// vote: warp-voting BH (a warp opens a node unless all its live
+// lanes accept it; groups = 32 consecutive positions of the evaluation order)
 int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, double beta, void* out, int64_t* visited,
-               cudaStream_t s);
+               cudaStream_t s, bool vote = false);
 // share = 0: per-query RNG streams (reference); share = k > 0: the 2^k consecutive
 // positions of the processing order (qperm) share one stream (paper recipe)
 int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
@@ -32,7 +34,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
                     int64_t* path_count, cudaStream_t s, bool* used);
 int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                      const int32_t* qperm, double beta, float* out, int64_t* visited,
-                     cudaStream_t s, bool* done);
+                     cudaStream_t s, bool* done, bool vote = false);
 int post_transform(const void* raw, int raw_f32, int64_t n, int smooth, double alpha,
                    double* values, double* raw64, uint8_t* flagged, cudaStream_t s);
 }  // namespace fsb

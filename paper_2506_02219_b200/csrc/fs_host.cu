@@ -107,6 +107,8 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   // slab boundaries: the first and last slabs are half-size, since the first
   // H2D and the last D2H copies cannot overlap any evaluation
   chunks = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, n));
+  // warp-voting BH: the groups come from the whole set's Morton order (one slab)
+  if (a->method == FSB_METHOD_BARNES_HUT && a->bh_warp_vote) chunks = 1;
   std::vector<int64_t> cut(chunks + 1, 0);
   for (int k = 1; k < chunks; ++k) {
     cut[k] = (int64_t)((double)n * (k - 0.5) / (chunks - 1.0));
@@ -149,7 +151,8 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
           pp = perm.as<int32_t>() + lo;
           FS_TRY(query_order(qs, m, pp, cs));
         }
-        FS_TRY(barnes_hut(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, pp, a->beta, r, v, cs));
+        FS_TRY(barnes_hut(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, pp, a->beta, r, v, cs,
+                          a->bh_warp_vote != 0));
         break;
       }
       case FSB_METHOD_TELESCOPING:

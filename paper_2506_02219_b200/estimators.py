@@ -165,8 +165,10 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
             perm = dev.empty(n, torch.int32)
             _lib.check(L.fsb_query_order(_vp(q), n, _vp(perm), _sp()))
         if config.method == "barnes_hut":
-            _lib.check(L.fsb_barnes_hut_batch(h, kid, alpha, dfloor, prec, _vp(q), n, _vp(perm),
-                                              float(config.beta), _vp(raw), _vp(visited), _sp()))
+            fn = (L.fsb_barnes_hut_vote_batch if getattr(config, "bh_warp_vote", False)
+                  else L.fsb_barnes_hut_batch)
+            _lib.check(fn(h, kid, alpha, dfloor, prec, _vp(q), n, _vp(perm), float(config.beta),
+                          _vp(raw), _vp(visited), _sp()))
         elif config.method == "telescoping_exhaustive":
             _lib.check(L.fsb_telescoping_batch(h, kid, alpha, dfloor, prec, _vp(q), n, _vp(raw),
                                                _vp(visited), _sp()))
@@ -259,6 +261,7 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
     # the paper's warp-shared streams (shuffled windows, fsb_shuffle_order)
     args.rng_group_log2 = 5 if (config.method == "stochastic"
                                 and getattr(config, "rng_sharing", "query") == "warp") else 0
+    args.bh_warp_vote = 1 if getattr(config, "bh_warp_vote", False) else 0
     h = None
     keep = []
     if config.method == "brute_force":

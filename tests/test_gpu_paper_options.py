@@ -1,0 +1,166 @@
+"""The paper's GPU options (not in the reference), checked against the
+oracle's restatement of the paper's algorithm: warp-voting Barnes-Hut
+and warp-shared RNG streams.  FP64 bitwise vs the oracle; FP32
+vs FP64 to FP32 rounding.  Needs a GPU."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fs():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_02219_b200 as fs
+    return fs
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    return oracle
+
+
+CASES = [
+    (dict(kind="mesh_torus", m=20000, seed=9), "coulomb"),
+    (dict(kind="manydup", m=3000, seed=4, posmass=True), "coulomb"),
+    (dict(kind="mesh_sphere_winding", m=6000, seed=8, channels=3), "winding_dipole"),
+    (dict(kind="duplicates", m=5000, seed=5, posmass=True), "smooth_exp"),
+]
+KID = {"coulomb": 0, "winding_dipole": 1, "smooth_exp": 2}
+
+
+def _same(a, b, kind):
+    """Bitwise for coulomb/winding; smooth_exp to 1e-10 relative, 1e-13 of the field's
+    scale absolute (device exp vs glibc exp, amplified by cancelling swaps)."""
+    if kind == "smooth_exp":
+        np.testing.assert_allclose(a, b, rtol=1e-10, atol=1e-13 * np.abs(b).max())
+    else:
+        np.testing.assert_array_equal(a, b)
+
+
+def _morton(fs, qd, n):
+    import torch
+    from paper_2506_02219_b200 import _device as dev, _lib
+    p = dev.empty(n, torch.int32)
+    _lib.check(_lib.lib().fsb_query_order(C.c_void_p(dev.ptr(qd)), n, C.c_void_p(dev.ptr(p)),
+                                          C.c_void_p(dev.stream_ptr())))
+    return p.cpu().numpy()
+
+
+@pytest.mark.parametrize("case,kind", CASES, ids=lambda c: c if isinstance(c, str) else c["kind"])
+def test_vote_bh_f64_bitwise_vs_oracle(fs, O, case, kind):
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    s = scenes.build_sources(case)
+    kern = fs.KernelSpec(kind)
+    q = np.random.default_rng(3).uniform(-1.1, 1.1, (1000, 3))
+    n = len(q)
+    qd = dev.to_device(q)
+    t = fs.build_tree(s, 2)
+    ca = t.core_arrays()
+    for beta in (1.0, 2.0, 6.0):
+        cfg = fs.EstimatorConfig("barnes_hut", beta=beta, bh_warp_vote=True)
+        for morton in (False, True):
+            r = evaluate_field_device(cfg, s, kern, qd, t, query_order=morton)
+            order = _morton(fs, qd, n) if morton else None
+            out, vis = np.zeros(n), np.zeros(n, dtype=np.int64)
+            O.barnes_hut_vote_batch(*ca, KID[kind], kern.alpha, kern.distance_floor, q, order,
+                                    beta, out, vis)
+            _same(r.raw.cpu().numpy(), out, kind)
+            np.testing.assert_array_equal(r.visited.cpu().numpy(), vis)
+
+
+@pytest.mark.parametrize("split", ["1", "0"], ids=["split", "warp"])
+@pytest.mark.parametrize("case,kind", CASES, ids=lambda c: c if isinstance(c, str) else c["kind"])
+def test_vote_bh_f32_matches_f64_vote(fs, case, kind, split, monkeypatch):
+    """FP32 voting BH (load-balanced split kernel, or the warp-coherent one) walks
+    the FP64 voting BH's node sets (up to acceptance tests at the FP32 boundary)
+    and agrees to 1e-5 * (1 + |ref|) where the sets agree."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    monkeypatch.setenv("FSB_BH_SPLIT", split)
+    monkeypatch.setenv("FSB_BH_SPLIT_AFTER", "16")  # force items on small trees
+    monkeypatch.setenv("FSB_BH_MIN_SPLIT", "4")
+    s = scenes.build_sources(case)
+    kern = fs.KernelSpec(kind)
+    qd = dev.to_device(np.random.default_rng(5).uniform(-1.1, 1.1, (3000, 3)))
+    t = fs.build_tree(s, 2)
+    for beta in (1.0, 4.0):
+        a = evaluate_field_device(fs.EstimatorConfig("barnes_hut", beta=beta, precision="f32",
+                                                     bh_warp_vote=True), s, kern, qd, t)
+        b = evaluate_field_device(fs.EstimatorConfig("barnes_hut", beta=beta, precision="f64",
+                                                     bh_warp_vote=True), s, kern, qd, t)
+        va, vb = a.visited.cpu().numpy(), b.visited.cpu().numpy()
+        same = va == vb
+        assert same.mean() >= 0.9, same.mean()
+        ra, rb = a.raw.cpu().numpy(), b.raw.cpu().numpy()
+        fin = np.isfinite(rb) & same
+        assert (np.abs(ra[fin] - rb[fin]) / (1 + np.abs(rb[fin]))).max() <= 1e-5
+
+
+def test_vote_bh_is_more_accurate_and_host_pipeline_matches(fs):
+    """Voting opens a superset of each query's nodes: error at a given beta is no
+    worse than per-query BH's (median), and evaluate_field (host pipeline, one
+    slab) returns the device path's values bit for bit."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    s = scenes.build_sources(dict(kind="mesh_torus", m=30000, seed=3))
+    kern = fs.KernelSpec("coulomb")
+    q = np.random.default_rng(6).uniform(-0.6, 0.6, (20000, 3))
+    t = fs.build_tree(s, 2)
+    truth = fs.evaluate_field(fs.EstimatorConfig("brute_force"), s, kern, fs.QuerySet(q)).values
+    for prec in ("f32", "f64"):
+        cfg_v = fs.EstimatorConfig("barnes_hut", beta=3.0, precision=prec, bh_warp_vote=True)
+        cfg_p = fs.EstimatorConfig("barnes_hut", beta=3.0, precision=prec)
+        rv = fs.evaluate_field(cfg_v, s, kern, fs.QuerySet(q), tree=t, chunks=4)
+        rp = fs.evaluate_field(cfg_p, s, kern, fs.QuerySet(q), tree=t)
+        assert (rv.visited_nodes >= rp.visited_nodes).mean() > 0.99
+        ev = np.median(np.abs(rv.values - truth) / np.abs(truth))
+        ep = np.median(np.abs(rp.values - truth) / np.abs(truth))
+        assert ev <= ep
+        rd = evaluate_field_device(cfg_v, s, kern, dev.to_device(q), t).to_host()
+        np.testing.assert_array_equal(rv.raw, rd.raw)
+        np.testing.assert_array_equal(rv.visited_nodes, rd.visited_nodes)
+
+
+@pytest.mark.parametrize("rr", ["paper_ratio", "fixed_half", "disabled"])
+@pytest.mark.parametrize("case,kind", CASES, ids=lambda c: c if isinstance(c, str) else c["kind"])
+def test_warp_shared_streams_f64_bitwise_vs_oracle(fs, O, case, kind, rr):
+    """rng_sharing="warp" in FP64 (k_stochastic with group keys) against the oracle
+    with keys[order[t]] = (t + query_offset) >> 5: values and counters bitwise."""
+    import torch
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev, _lib
+    s = scenes.build_sources(case)
+    kern = fs.KernelSpec(kind)
+    q = np.random.default_rng(7).uniform(-1.1, 1.1, (700, 3))
+    n = len(q)
+    qd = dev.to_device(q)
+    t = fs.build_tree(s, 4)
+    ca = t.core_arrays()
+    codes = {"paper_ratio": 0, "fixed_half": 1, "disabled": 2}
+    for S, seed, off in ((1, 11, 0), (3, 12, 64), (2, 2 ** 64 - 1, 7)):
+        cfg = fs.EstimatorConfig("stochastic", samples_per_subdomain=S, rr_mode=rr, seed=seed,
+                                 rng_sharing="warp")
+        r = evaluate_field_device(cfg, s, kern, qd, t, query_offset=off)
+        p = dev.empty(n, torch.int32)
+        _lib.check(_lib.lib().fsb_shuffle_order(n, seed, off, C.c_void_p(dev.ptr(p)),
+                                                C.c_void_p(dev.stream_ptr())))
+        order = p.cpu().numpy().astype(np.int64)
+        keys = np.zeros(n, dtype=np.uint64)
+        keys[order] = ((np.arange(n) + off) >> 5).astype(np.uint64)
+        res = [np.zeros(n)] + [np.zeros(n, dtype=np.int64) for _ in range(3)]
+        O.stochastic_keyed_batch(*ca, KID[kind], kern.alpha, kern.distance_floor, q, S,
+                                 codes[rr], seed, keys, *res)
+        _same(r.raw.cpu().numpy(), res[0], kind)
+        np.testing.assert_array_equal(r.visited.cpu().numpy(), res[1])
+        np.testing.assert_array_equal(r.path_steps.cpu().numpy(), res[2])
+        np.testing.assert_array_equal(r.path_count.cpu().numpy(), res[3])

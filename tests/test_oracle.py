@@ -108,3 +108,52 @@ def test_oracle_cores_match_reference(entry):
                 O.stochastic_moments_batch(*ca, kid, alpha, 1e-12, q, 50, 0, 7, out, var)
                 _assert_close(out, A[pre + run + "_mean"], entry["kernel"], run)
                 _assert_close(var, A[pre + run + "_var"], entry["kernel"], run + " var")
+
+
+def _small_tree(seed=3, m=3000, d=2):
+    s = scenes.build_sources(dict(kind="mesh_torus", m=m, seed=seed))
+    t = O.build_tree(s.positions, s.masses, s.weights, d, 32)
+    return s, O.core_arrays(t)
+
+
+def test_oracle_vote_bh_properties():
+    """The warp-voting BH restatement: at beta -> inf it equals the
+    reference's BH bitwise (every node opened down to the leaves either way); at
+    finite beta each query's node set contains its own BH set (visited >=) and the
+    group shares one count."""
+    s, ca = _small_tree()
+    q = np.random.default_rng(2).uniform(-0.6, 0.6, (200, 3))
+    n = len(q)
+    for beta in (1e9, 2.0):
+        a, va = np.zeros(n), np.zeros(n, dtype=np.int64)
+        b, vb = np.zeros(n), np.zeros(n, dtype=np.int64)
+        O.barnes_hut_batch(*ca, 0, 200.0, 1e-12, q, beta, 0, a, va)
+        O.barnes_hut_vote_batch(*ca, 0, 200.0, 1e-12, q, None, beta, b, vb)
+        if beta > 1e8:
+            np.testing.assert_array_equal(a, b)
+            np.testing.assert_array_equal(va, vb)
+        else:
+            assert (vb >= va).all() and (vb > va).any()
+            for g in range(0, n, 32):
+                assert len(set(vb[g:g + 32])) == 1
+    # the group order matters only through the grouping
+    order = np.random.default_rng(5).permutation(n).astype(np.int32)
+    c, vc = np.zeros(n), np.zeros(n, dtype=np.int64)
+    O.barnes_hut_vote_batch(*ca, 0, 200.0, 1e-12, q, order, 2.0, c, vc)
+    for g in range(0, n, 32):
+        assert len(set(vc[order[g:g + 32]])) == 1
+
+
+def test_oracle_keyed_stochastic_reduces_to_reference():
+    """keys[i] = i + offset reproduces stochastic_batch exactly; a shared key gives
+    every query of the group the same sampled paths (same path_count)."""
+    s, ca = _small_tree(d=4)
+    q = np.random.default_rng(4).uniform(-0.6, 0.6, (64, 3))
+    n = len(q)
+    ref = [np.zeros(n)] + [np.zeros(n, dtype=np.int64) for _ in range(3)]
+    O.stochastic_batch(*ca, 0, 200.0, 1e-12, q, 2, 0, 9, 100, *ref)
+    got = [np.zeros(n)] + [np.zeros(n, dtype=np.int64) for _ in range(3)]
+    O.stochastic_keyed_batch(*ca, 0, 200.0, 1e-12, q, 2, 0, 9,
+                             np.arange(n, dtype=np.uint64) + 100, *got)
+    for x, y in zip(ref, got):
+        np.testing.assert_array_equal(x, y)
