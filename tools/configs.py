@@ -1,6 +1,7 @@
-"""Secondary rows of BASELINE.json's configs on one B200: S=1 stochastic vs the
-GPU deterministic BH at matched median error, per config (SURVEY 8(d) C1, C2,
-C3, C5).  C4 is bench.py's headline.  Writes one JSON line per row to stdout.
+"""Secondary rows of BASELINE.json's configs on one B200: S=1 stochastic (per-query
+streams, and the paper's warp-shared streams) vs the GPU deterministic BH at
+matched median error, per config.  C4 is bench.py's
+headline.  Writes one JSON line per row to stdout.
 
     python tools/configs.py [C1 C2s C2t C3 C5]
 
@@ -65,16 +66,28 @@ def scene(name):
     raise ValueError(name)
 
 
-def timed(fn, reps=3):
+CLOCKS = []  # (label, clocks summary) of every timed region
+
+
+def timed(fn, reps=3, label="", trials=3):
+    """Best of `trials` means over `reps` calls (CUDA events), after one warm-up call."""
     fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(reps):
-        r = fn()
-    b.record()
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) / reps, r
+    best = None
+    with bench.Clocks(torch.cuda.current_device()) as clk:
+        clk.active = True
+        for _ in range(trials):
+            a.record()
+            for _ in range(reps):
+                r = fn()
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / reps
+            best = ms if best is None else min(best, ms)
+        clk.active = False
+    CLOCKS.append((label, clk.summary()))
+    return best, r
 
 
 def error(kind, est, truth, flagged_t=None, flagged_e=None):
@@ -119,18 +132,24 @@ def run(name):
 
     t4, t2 = fs.build_tree(src, 4), fs.build_tree(src, 2)
     cfg = fs.EstimatorConfig("stochastic", seed=1, precision="f32")
-    s1_ms, r = timed(lambda: evaluate_field_device(cfg, src, kern, q, t4))
+    s1_ms, r = timed(lambda: evaluate_field_device(cfg, src, kern, q, t4), label="s1")
     s1_err = err_of(r)
+    # the paper's GPU recipe: warp-shared streams over a shuffled order
+    cfg_w = fs.EstimatorConfig("stochastic", seed=1, precision="f32", rng_sharing="warp")
+    w_ms, rw = timed(lambda: evaluate_field_device(cfg_w, src, kern, q, t4), label="s1_warp")
+    w_err = err_of(rw)
     sweep = []
     for beta in BETAS:
         cfgb = fs.EstimatorConfig("barnes_hut", beta=beta, precision="f32")
-        ms_b, rb = timed(lambda: evaluate_field_device(cfgb, src, kern, q, t2), reps=1)
+        ms_b, rb = timed(lambda: evaluate_field_device(cfgb, src, kern, q, t2), reps=2,
+                         label=f"bh{beta}")
         e = err_of(rb)
         sweep.append({"beta": beta, "ms": ms_b, "err": e,
                       "visited_mean": float(rb.visited.double().mean().item())})
-        if e < 0.5 * s1_err or ms_b > 20000:
+        if e < 0.5 * min(s1_err, w_err) or ms_b > 20000:
             break
     matched = bench.loglog_interp([(p["err"], p["ms"]) for p in sweep], s1_err)
+    matched_w = bench.loglog_interp([(p["err"], p["ms"]) for p in sweep], w_err)
     row = {"config": name, "workload": desc, "queries": n, "sources": len(src),
            "error_metric": {"rel": "median relative error", "abs": "median absolute error",
                             "abs_unflagged": "median absolute error of values, unflagged"}[ekind],
@@ -138,7 +157,14 @@ def run(name):
                     + (", 10^6-query subset)" if sub.step else ")"),
            "s1_ms": s1_ms, "s1_queries_per_s": n / (s1_ms * 1e-3), "s1_err": s1_err,
            "bh_sweep": sweep, "matched_bh_ms": matched,
-           "speedup_at_matched_error": (matched / s1_ms) if matched else None}
+           "speedup_at_matched_error": (matched / s1_ms) if matched else None,
+           "warp_streams": {"s1_ms": w_ms, "s1_queries_per_s": n / (w_ms * 1e-3),
+                            "s1_err": w_err, "matched_bh_ms": matched_w,
+                            "speedup_at_matched_error": (matched_w / w_ms) if matched_w else None}}
+    mins = [c.get("sm_mhz_min") for _, c in CLOCKS if c.get("sm_mhz_min")]
+    reasons = sorted({x for _, c in CLOCKS for x in c.get("reasons", [])})
+    row["clocks"] = {"sm_mhz_min": min(mins) if mins else None, "reasons": reasons}
+    CLOCKS.clear()
     if kern.kind == "smooth_exp":
         row["flagged_fraction"] = float(r.flagged.double().mean().item())
     print(json.dumps(row), flush=True)
