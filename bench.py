@@ -307,9 +307,9 @@ def run_ours(args):
 
     def kernel_only():
         if args.streams == "warp":  # k_sto_warp (the order is computed once, outside)
-            _lib.check(L.fsb_stochastic_batch_shared(
+            _lib.check(L.fsb_stochastic_batch_ex(
                 h, 0, kern.alpha, kern.distance_floor, 1, C.c_void_p(dev.ptr(q_dev)), n,
-                C.c_void_p(dev.ptr(order)), 1, 0, 1, qoff, 5, C.c_void_p(dev.ptr(raw)),
+                C.c_void_p(dev.ptr(order)), 1, 0, 1, qoff, 5, 0, C.c_void_p(dev.ptr(raw)),
                 C.c_void_p(dev.ptr(vis)), None, None, sp))
         else:  # k_sto_fast
             _lib.check(L.fsb_stochastic_batch(h, 0, kern.alpha, kern.distance_floor, 1,

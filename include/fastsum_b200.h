@@ -100,20 +100,24 @@ int fsb_stochastic_batch(fsb_tree *tree, int kid, double alpha, double dfloor, i
                          void *out, int64_t *visited, int64_t *path_steps,
                          int64_t *path_count, void *stream);
 
-/* The paper's GPU recipe, not the reference's: queries are
- * evaluated in `order` (a permutation; the paper shuffles the grid) and each
- * group of 2^group_log2 consecutive positions shares one RNG stream keyed on
- * (seed, (position + query_offset) >> group_log2, subdomain, sample), so a warp
- * follows one sampled path.  Unbiased per query; group_log2 = 0 is
- * fsb_stochastic_batch with an evaluation order.  FP32 with group_log2 = 5 and
- * query_offset % 32 == 0 runs the warp-uniform kernel (k_sto_warp); other
- * cases run the per-query kernels with the group keys. */
-int fsb_stochastic_batch_shared(fsb_tree *tree, int kid, double alpha, double dfloor,
-                                int precision, const double *queries, int64_t n,
-                                const int32_t *order, int64_t n_samples, int rr_mode,
-                                uint64_t seed, int64_t query_offset, int group_log2, void *out,
-                                int64_t *visited, int64_t *path_steps, int64_t *path_count,
-                                void *stream);
+/* stochastic_batch plus the paper's options (not the reference's):
+ *  - evaluation order and shared RNG streams: queries are
+ *    evaluated in `order` (a permutation, NULL = 0..n-1; the paper shuffles the
+ *    grid, see fsb_shuffle_order) and each group of 2^group_log2 consecutive
+ *    positions shares one stream keyed on (seed, (position + query_offset) >>
+ *    group_log2, subdomain, sample), so a warp follows one sampled path.
+ *    Unbiased per query.  FP32 with group_log2 = 5 and query_offset % 32 == 0
+ *    runs the warp-uniform kernel (k_sto_warp);
+ *  - variant 1 = Alg. 2 of the paper's supplemental (roulette before each swap,
+ *    including the subdomain's own; unbiased; the generic per-query kernel in
+ *    either precision).  variant 0 is the reference's walk.
+ * group_log2 = 0, variant = 0 and order = NULL is fsb_stochastic_batch. */
+int fsb_stochastic_batch_ex(fsb_tree *tree, int kid, double alpha, double dfloor,
+                            int precision, const double *queries, int64_t n,
+                            const int32_t *order, int64_t n_samples, int rr_mode, uint64_t seed,
+                            int64_t query_offset, int group_log2, int variant, void *out,
+                            int64_t *visited, int64_t *path_steps, int64_t *path_count,
+                            void *stream);
 
 /* stochastic_moments_batch(*core, kid, alpha, dfloor, queries, n_reps, rr_mode, seed,
  * mean_out, var_out) -- _core.py:270-336.  FP64 only. */
@@ -181,6 +185,7 @@ typedef struct fsb_eval_args {
                              paper's warp-shared streams over fsb_shuffle_order */
   int bh_warp_vote;       /* barnes_hut: warp voting over the evaluation order
                              (fsb_barnes_hut_vote_batch; evaluated as one slab) */
+  int path_variant;       /* stochastic: 0 = the reference's walk, 1 = Alg. 2 */
 } fsb_eval_args;
 
 int fsb_evaluate_field_host(fsb_tree *tree, const fsb_eval_args *args, const double *queries,

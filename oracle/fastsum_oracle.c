@@ -221,7 +221,7 @@ static inline double sample_residual(const tree_t *t, int kid, double alpha, dou
                                      int64_t a, int64_t a_ord, int64_t count_a,
                                      double delta_a, double qx, double qy, double qz,
                                      uint64_t qi, uint64_t s, uint64_t seed, int rr_mode,
-                                     int64_t *steps_out, int64_t *seen_out) {
+                                     int variant, int64_t *steps_out, int64_t *seen_out) {
     uint64_t key_i = or_stream_key(seed, qi, (uint64_t)a_ord, s, 0);
     uint64_t key_r = or_stream_key(seed, qi, (uint64_t)a_ord, s, 1);
     double u0 = or_uniform_draw(key_i, 0);
@@ -230,6 +230,39 @@ static inline double sample_residual(const tree_t *t, int kid, double alpha, dou
     int64_t node = a, steps = 0, seen = 0;
     uint64_t rctr = 0;
     double prr = 1.0, resid = 0.0;
+    if (variant == 1) {
+        /* the paper's Alg. 2 (supplemental pseudocode pathSampleEstimator): the
+         * roulette at T_{I,k} gates the swap at T_{I,k}; seen +1 per roulette
+         * test, +children per committed swap (not in the reference) */
+        while (t->child_count[node] > 0) {
+            int64_t child = -1, cs = t->child_start[node];
+            for (int64_t k = 0; k < t->child_count[node]; ++k) {
+                int64_t cc = t->child_index[cs + k];
+                if (t->begin[cc] <= j && j < t->end[cc]) { child = cc; break; }
+            }
+            double p = or_rr_probability(ffr(t, node, qx, qy, qz), ffr(t, child, qx, qy, qz),
+                                         rr_mode);
+            double u = or_uniform_draw(key_r, rctr);
+            rctr += 1;
+            seen += 1;
+            if (u >= p) break;
+            double delta;
+            if (node == a)
+                delta = delta_a;
+            else
+                delta = children_sum(t, kid, alpha, dfloor, node, qx, qy, qz)
+                        - agg_term(t, kid, alpha, dfloor, node, qx, qy, qz);
+            seen += t->child_count[node];
+            prr *= p;
+            double pagg = (double)(t->end[node] - t->begin[node]) / (double)count_a;
+            resid += delta / (pagg * prr);
+            node = child;
+            steps += 1;
+        }
+        *steps_out = steps;
+        *seen_out = seen;
+        return resid;
+    }
     while (t->child_count[node] > 0) {
         int64_t child = -1, cs = t->child_start[node];
         for (int64_t k = 0; k < t->child_count[node]; ++k) {
@@ -271,7 +304,7 @@ static void stochastic_core(const double *diam, const double *agg_mass, const do
                             const double *ms, int64_t num_nodes, int c, int kid, double alpha,
                             double dfloor, const double *q, int64_t n, int64_t n_samples,
                             int rr_mode, uint64_t seed, int64_t query_offset,
-                            const uint64_t *keys, double *out, int64_t *visited,
+                            const uint64_t *keys, int variant, double *out, int64_t *visited,
                             int64_t *path_steps, int64_t *path_count) {
     tree_t t = mk_tree(diam, agg_mass, com, cs, cc, ci, b, e, pts, ms, num_nodes, c);
     int64_t root_kids = t.child_count[0];
@@ -303,7 +336,8 @@ static void stochastic_core(const double *diam, const double *agg_mass, const do
                 double resid = sample_residual(&t, kid, alpha, dfloor, a, a_ord, count_a,
                                                delta_a, qx, qy, qz,
                                                keys ? keys[qi] : (uint64_t)(qi + query_offset),
-                                               (uint64_t)s, seed, rr_mode, &st, &se);
+                                               (uint64_t)s, seed, rr_mode, variant, &st,
+                                               &se);
                 fa += resid;
                 steps_total += st;
                 seen += se;
@@ -326,23 +360,24 @@ void or_stochastic_batch(const double *diam, const double *agg_mass, const doubl
                          int rr_mode, uint64_t seed, int64_t query_offset, double *out,
                          int64_t *visited, int64_t *path_steps, int64_t *path_count) {
     stochastic_core(diam, agg_mass, com, cs, cc, ci, b, e, pts, ms, num_nodes, c, kid, alpha,
-                    dfloor, q, n, n_samples, rr_mode, seed, query_offset, NULL, out, visited,
+                    dfloor, q, n, n_samples, rr_mode, seed, query_offset, NULL, 0, out, visited,
                     path_steps, path_count);
 }
 
-/* The paper's shared streams (not in the reference): query
- * qi draws from the streams of index keys[qi]. */
-void or_stochastic_keyed_batch(const double *diam, const double *agg_mass, const double *com,
-                               const int64_t *cs, const int64_t *cc, const int64_t *ci,
-                               const int64_t *b, const int64_t *e, const double *pts,
-                               const double *ms, int64_t num_nodes, int c, int kid,
-                               double alpha, double dfloor, const double *q, int64_t n,
-                               int64_t n_samples, int rr_mode, uint64_t seed,
-                               const uint64_t *keys, double *out, int64_t *visited,
-                               int64_t *path_steps, int64_t *path_count) {
+/* The paper's options (not in the reference): shared streams (PAPER.md:323,
+ * 392) -- query qi draws from the streams of index keys[qi] (keys == NULL:
+ * qi + query_offset) -- and variant 1 = Alg. 2 (roulette before each swap). */
+void or_stochastic_ex_batch(const double *diam, const double *agg_mass, const double *com,
+                            const int64_t *cs, const int64_t *cc, const int64_t *ci,
+                            const int64_t *b, const int64_t *e, const double *pts,
+                            const double *ms, int64_t num_nodes, int c, int kid, double alpha,
+                            double dfloor, const double *q, int64_t n, int64_t n_samples,
+                            int rr_mode, uint64_t seed, int64_t query_offset,
+                            const uint64_t *keys, int variant, double *out, int64_t *visited,
+                            int64_t *path_steps, int64_t *path_count) {
     stochastic_core(diam, agg_mass, com, cs, cc, ci, b, e, pts, ms, num_nodes, c, kid, alpha,
-                    dfloor, q, n, n_samples, rr_mode, seed, 0, keys, out, visited, path_steps,
-                    path_count);
+                    dfloor, q, n, n_samples, rr_mode, seed, query_offset, keys, variant, out,
+                    visited, path_steps, path_count);
 }
 
 /* Warp-voting Barnes-Hut (Alg. 1 with the acceptance test voted
@@ -457,7 +492,8 @@ void or_stochastic_moments_batch(const double *diam, const double *agg_mass,
                     int64_t a = sub_nodes[u], st, se;
                     tt += sample_residual(&t, kid, alpha, dfloor, a, sub_ords[u],
                                           t.end[a] - t.begin[a], sub_delta[u], qx, qy, qz,
-                                          (uint64_t)qi, (uint64_t)r, seed, rr_mode, &st, &se);
+                                          (uint64_t)qi, (uint64_t)r, seed, rr_mode, 0, &st,
+                                          &se);
                 }
                 acc += tt;
                 acc2 += tt * tt;

@@ -150,23 +150,25 @@ def stochastic_batch(*args):
     path_count[:] = pc
 
 
-def stochastic_keyed_batch(*args):
-    """The paper's shared streams (not in the reference): stochastic_batch with query i
-    drawing from the streams of index keys[i]; args = core11 + (kid, alpha, dfloor,
-    queries, n_samples, rr_mode, seed, keys, out, visited, path_steps, path_count)."""
+def stochastic_ex_batch(*args, keys=None, variant=0):
+    """stochastic_batch plus the paper's options (not in the reference): query i draws
+    from the streams of index keys[i] (None: i + query_offset), variant 1 = Alg. 2;
+    args = core11 + (kid, alpha, dfloor, queries, n_samples, rr_mode, seed, query_offset,
+    out, visited, path_steps, path_count)."""
     core11 = args[:11]
-    (kid, alpha, dfloor, queries, n_samples, rr_mode, seed, keys, out, visited,
+    (kid, alpha, dfloor, queries, n_samples, rr_mode, seed, query_offset, out, visited,
      path_steps, path_count) = args[11:]
     keep, targs = _tree_args(core11)
     q = _f64(queries)
     n = q.shape[0]
-    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    k = None if keys is None else np.ascontiguousarray(keys, dtype=np.uint64)
     res = np.zeros(n)
     vis, st, pc = (np.zeros(n, dtype=np.int64) for _ in range(3))
-    lib().or_stochastic_keyed_batch(*targs, C.c_int(kid), C.c_double(alpha), C.c_double(dfloor),
-                                    _dp(q), C.c_int64(n), C.c_int64(n_samples), C.c_int(rr_mode),
-                                    C.c_uint64(int(seed)), k.ctypes.data_as(C.c_void_p),
-                                    _dp(res), _ip(vis), _ip(st), _ip(pc))
+    lib().or_stochastic_ex_batch(*targs, C.c_int(kid), C.c_double(alpha), C.c_double(dfloor),
+                                 _dp(q), C.c_int64(n), C.c_int64(n_samples), C.c_int(rr_mode),
+                                 C.c_uint64(int(seed)), C.c_int64(query_offset),
+                                 None if k is None else k.ctypes.data_as(C.c_void_p),
+                                 C.c_int(variant), _dp(res), _ip(vis), _ip(st), _ip(pc))
     out[:] = res
     visited[:] = vis
     path_steps[:] = st

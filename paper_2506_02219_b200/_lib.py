@@ -30,7 +30,7 @@ class EvalArgs(C.Structure):
                 ("beta", _D), ("n_samples", _I64), ("rr_mode", _I), ("seed", C.c_uint64),
                 ("query_offset", _I64), ("smooth", _I), ("query_order", _I),
                 ("src_pts", _P), ("src_ms", _P), ("m", _I64), ("c", _I),
-                ("rng_group_log2", _I), ("bh_warp_vote", _I)]
+                ("rng_group_log2", _I), ("bh_warp_vote", _I), ("path_variant", _I)]
 
 
 METHOD_CODES = {"brute_force": 0, "barnes_hut": 1, "telescoping_exhaustive": 2, "stochastic": 3}
@@ -51,8 +51,8 @@ SIGNATURES = {
     "fsb_barnes_hut_vote_batch": [_P, _I, _D, _D, _I, _P, _I64, _P, _D, _P, _P, _P],
     "fsb_stochastic_batch": [_P, _I, _D, _D, _I, _P, _I64, _P, _I64, _I, C.c_uint64, _I64, _P,
                              _P, _P, _P, _P],
-    "fsb_stochastic_batch_shared": [_P, _I, _D, _D, _I, _P, _I64, _P, _I64, _I, C.c_uint64, _I64,
-                                    _I, _P, _P, _P, _P, _P],
+    "fsb_stochastic_batch_ex": [_P, _I, _D, _D, _I, _P, _I64, _P, _I64, _I, C.c_uint64, _I64,
+                                _I, _I, _P, _P, _P, _P, _P],
     "fsb_stochastic_moments_batch": [_P, _I, _D, _D, _P, _I64, _I64, _I, C.c_uint64, _P, _P, _P],
     "fsb_telescoping_batch": [_P, _I, _D, _D, _I, _P, _I64, _P, _P, _P],
     "fsb_query_order": [_P, _I64, _P, _P],

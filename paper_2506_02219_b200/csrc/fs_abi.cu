@@ -364,22 +364,21 @@ int fsb_stochastic_batch(fsb_tree* tree, int kid, double alpha, double dfloor, i
                          path_count, S(stream));
 }
 
-int fsb_stochastic_batch_shared(fsb_tree* tree, int kid, double alpha, double dfloor,
-                                int precision, const double* queries, int64_t n,
-                                const int32_t* order, int64_t n_samples, int rr_mode,
-                                uint64_t seed, int64_t query_offset, int group_log2, void* out,
-                                int64_t* visited, int64_t* path_steps, int64_t* path_count,
-                                void* stream) {
+int fsb_stochastic_batch_ex(fsb_tree* tree, int kid, double alpha, double dfloor, int precision,
+                            const double* queries, int64_t n, const int32_t* order,
+                            int64_t n_samples, int rr_mode, uint64_t seed, int64_t query_offset,
+                            int group_log2, int variant, void* out, int64_t* visited,
+                            int64_t* path_steps, int64_t* path_count, void* stream) {
   ABI_TREE(tree);
   if (int rc = check_common(kid, precision, n)) return rc;
   if (n_samples < 1 || n_samples > (1LL << 30) || rr_mode < 0 || rr_mode > 2 || group_log2 < 0 ||
-      group_log2 > 20) {
-    set_error("bad samples_per_subdomain / rr mode / group size");
+      group_log2 > 20 || variant < 0 || variant > 1) {
+    set_error("bad samples_per_subdomain / rr mode / group size / variant");
     return 1;
   }
   return fsb::stochastic(tree->t, kid, alpha, dfloor, precision == 0, queries, n, order,
                          (int)n_samples, rr_mode, seed, query_offset, out, visited, path_steps,
-                         path_count, S(stream), group_log2);
+                         path_count, S(stream), group_log2, variant);
 }
 
 int fsb_stochastic_moments_batch(fsb_tree* tree, int kid, double alpha, double dfloor,

@@ -232,7 +232,7 @@ __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int
                                                   uint64_t key_i, uint64_t key_r, int rr_mode,
                                                   double qx, double qy, double qz,
                                                   const KParams& kp, int64_t& steps,
-                                                  int64_t& seen) {
+                                                  int64_t& seen, int variant) {
   int64_t count_a = (int64_t)tpa.w - tpa.z;
   double u0 = uniform_draw(key_i, 0);
   int64_t j = tpa.z + (int64_t)__dmul_rn(u0, (double)count_a);
@@ -241,6 +241,35 @@ __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int
   int4 tp = tpa;
   double prr = 1.0, resid = 0.0;
   uint64_t rctr = 0;
+  if (variant == 1) {
+    // the paper's Alg. 2 (pathSampleEstimator, PAPER.md supplemental): the
+    // roulette at T_{I,k} gates the swap at T_{I,k} (the reference commits the
+    // swap first); counters: +1 per roulette test, +children per swap
+    while (tp.y > 0) {
+      int child = T.child_of(tp, j);
+      double rp = ffr<F64>(T.geo[node], qx, qy, qz);
+      double rc = ffr<F64>(T.geo[child], qx, qy, qz);
+      double p = rr_probability(rp, rc, rr_mode);
+      double u = uniform_draw(key_r, rctr);
+      ++rctr;
+      ++seen;
+      if (u >= p) break;
+      double delta;
+      if (node == a)
+        delta = delta_a;
+      else
+        delta = F64 ? __dsub_rn(T.children_sum(tp, qx, qy, qz, kp), T.agg_term(node, qx, qy, qz, kp))
+                    : T.children_sum(tp, qx, qy, qz, kp) - T.agg_term(node, qx, qy, qz, kp);
+      seen += tp.y;
+      prr = __dmul_rn(prr, p);
+      double pagg = __ddiv_rn((double)(tp.w - tp.z), (double)count_a);
+      resid = __dadd_rn(resid, __ddiv_rn(delta, __dmul_rn(pagg, prr)));
+      node = child;
+      tp = T.topo[node];
+      ++steps;
+    }
+    return resid;
+  }
   while (tp.y > 0) {
     int child = T.child_of(tp, j);
     double delta;
@@ -273,7 +302,7 @@ __global__ void __launch_bounds__(128) k_stochastic(LoTree<KID, F64> T, int root
                                                     const double* __restrict__ q, int64_t n,
                                                     const int32_t* __restrict__ qperm, int S,
                                                     int rr_mode, uint64_t seed, int64_t qoff,
-                                                    int share, KParams kp,
+                                                    int share, int variant, KParams kp,
                                                     typename Prec<F64>::Out* __restrict__ out,
                                                     int64_t* __restrict__ visited,
                                                     int64_t* __restrict__ path_steps,
@@ -308,7 +337,7 @@ __global__ void __launch_bounds__(128) k_stochastic(LoTree<KID, F64> T, int root
         uint64_t hs = key_fold(ha, (uint64_t)s);
         uint64_t key_i = key_fold(hs, 0), key_r = key_fold(hs, 1);
         double resid = sample_residual<KID, F64>(T, a, tpa, delta_a, key_i, key_r, rr_mode, qx,
-                                                 qy, qz, kp, steps, seen);
+                                                 qy, qz, kp, steps, seen, variant);
         fa = __dadd_rn(fa, resid);
         ++paths;
       }
@@ -363,7 +392,7 @@ __global__ void __launch_bounds__(128) k_moments(LoTree<KID, F64> T, int root_ki
       uint64_t hs = key_fold(key_fold(hq, (uint64_t)a_ord), (uint64_t)r);
       tsum = __dadd_rn(tsum, sample_residual<KID, F64>(T, a, tpa, delta[a_ord], key_fold(hs, 0),
                                                        key_fold(hs, 1), rr_mode, qx, qy, qz, kp,
-                                                       st, se));
+                                                       st, se, 0));
     }
     acc = __dadd_rn(acc, tsum);
     acc2 = __dadd_rn(acc2, __dmul_rn(tsum, tsum));
@@ -834,9 +863,11 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
 int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                int64_t query_offset, void* out, int64_t* visited, int64_t* path_steps,
-               int64_t* path_count, cudaStream_t s, int share) {
+               int64_t* path_count, cudaStream_t s, int share, int variant) {
   if (n <= 0) return 0;
-  if (!f64 && !std::getenv("FSB_DISABLE_FAST")) {
+  // the fast FP32 kernels implement the reference variant; Alg. 2 runs the
+  // generic per-query kernel in either precision
+  if (!f64 && variant == 0 && !std::getenv("FSB_DISABLE_FAST")) {
     bool used = false;
     FS_TRY(stochastic_fast(t, kid, alpha, dfloor, q, n, qperm, n_samples, rr_mode, seed,
                            query_offset, share, (float*)out, visited, path_steps, path_count, s,
@@ -850,7 +881,7 @@ int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
     constexpr bool F64 = decltype(P)::value;
     k_stochastic<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(
         lo_view<KID, F64>(t), t->root_kids, q, n, qperm, n_samples, rr_mode, seed, query_offset,
-        share, kp, (typename Prec<F64>::Out*)out, visited, path_steps, path_count);
+        share, variant, kp, (typename Prec<F64>::Out*)out, visited, path_steps, path_count);
   });
 }
 

@@ -22,7 +22,7 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
 int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                int64_t query_offset, void* out, int64_t* visited, int64_t* path_steps,
-               int64_t* path_count, cudaStream_t s, int share = 0);
+               int64_t* path_count, cudaStream_t s, int share = 0, int variant = 0);
 int stochastic_moments(FsTree* t, int kid, double alpha, double dfloor, const double* q,
                        int64_t n, int64_t n_reps, int rr_mode, uint64_t seed, double* mean_out,
                        double* var_out, cudaStream_t s);

@@ -166,7 +166,7 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
         }
         FS_TRY(stochastic(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, pp, (int)a->n_samples,
                           a->rr_mode, a->seed, a->query_offset + lo, r, v, ps, pc, cs,
-                          shared ? a->rng_group_log2 : 0));
+                          shared ? a->rng_group_log2 : 0, a->path_variant));
       }
     }
     if (!counters) {
@@ -248,7 +248,8 @@ extern "C" int fsb_evaluate_field_host(fsb_tree* tree, const fsb_eval_args* a,
   }
   if (a->method == FSB_METHOD_STOCHASTIC &&
       (a->n_samples < 1 || a->n_samples > (1LL << 30) || a->rr_mode < 0 || a->rr_mode > 2 ||
-       a->rng_group_log2 < 0 || a->rng_group_log2 > 20)) {
+       a->rng_group_log2 < 0 || a->rng_group_log2 > 20 || a->path_variant < 0 ||
+       a->path_variant > 1)) {
     set_error("bad samples_per_subdomain / rr mode");
     return 1;
   }

@@ -172,17 +172,20 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
         elif config.method == "telescoping_exhaustive":
             _lib.check(L.fsb_telescoping_batch(h, kid, alpha, dfloor, prec, _vp(q), n, _vp(raw),
                                                _vp(visited), _sp()))
-        elif getattr(config, "rng_sharing", "query") == "warp":
-            # the paper's recipe: shuffled evaluation order, 32 consecutive
-            # positions share one stream (fsb_stochastic_batch_shared)
-            order = dev.empty(n, torch.int32)
-            _lib.check(L.fsb_shuffle_order(n, int(config.seed) & ((1 << 64) - 1),
-                                           int(query_offset), _vp(order), _sp()))
-            _lib.check(L.fsb_stochastic_batch_shared(
+        elif (getattr(config, "rng_sharing", "query") == "warp"
+              or _variant(config) != 0):
+            # the paper's options (fsb_stochastic_batch_ex): shared streams over a
+            # shuffled order (32 consecutive positions per stream), Alg. 2 walk
+            order, group = None, 0
+            if getattr(config, "rng_sharing", "query") == "warp":
+                order, group = dev.empty(n, torch.int32), 5
+                _lib.check(L.fsb_shuffle_order(n, int(config.seed) & ((1 << 64) - 1),
+                                               int(query_offset), _vp(order), _sp()))
+            _lib.check(L.fsb_stochastic_batch_ex(
                 h, kid, alpha, dfloor, prec, _vp(q), n, _vp(order),
                 int(config.samples_per_subdomain), _RR_CODES[config.rr_mode],
-                int(config.seed) & ((1 << 64) - 1), int(query_offset), 5, _vp(raw),
-                _vp(visited), _vp(steps), _vp(count), _sp()))
+                int(config.seed) & ((1 << 64) - 1), int(query_offset), group, _variant(config),
+                _vp(raw), _vp(visited), _vp(steps), _vp(count), _sp()))
         else:
             _lib.check(L.fsb_stochastic_batch(
                 h, kid, alpha, dfloor, prec, _vp(q), n, _vp(perm),
@@ -197,6 +200,11 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
                                     _vp(raw64), _vp(flagged), _sp()))
     return DeviceField(values=values, raw=raw64, flagged=flagged, visited=visited,
                        path_steps=steps, path_count=count, method=config.method)
+
+
+def _variant(config) -> int:
+    """fsb path variant: 0 the reference's walk, 1 the paper's Alg. 2."""
+    return 1 if getattr(config, "path_order", "swap_then_roulette") == "roulette_then_swap" else 0
 
 
 _PINNED: list = []  # (tensor, ndarray) pinned output blocks, reused once unreferenced
@@ -262,6 +270,7 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
     args.rng_group_log2 = 5 if (config.method == "stochastic"
                                 and getattr(config, "rng_sharing", "query") == "warp") else 0
     args.bh_warp_vote = 1 if getattr(config, "bh_warp_vote", False) else 0
+    args.path_variant = _variant(config)
     h = None
     keep = []
     if config.method == "brute_force":

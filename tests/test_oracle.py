@@ -153,7 +153,29 @@ def test_oracle_keyed_stochastic_reduces_to_reference():
     ref = [np.zeros(n)] + [np.zeros(n, dtype=np.int64) for _ in range(3)]
     O.stochastic_batch(*ca, 0, 200.0, 1e-12, q, 2, 0, 9, 100, *ref)
     got = [np.zeros(n)] + [np.zeros(n, dtype=np.int64) for _ in range(3)]
-    O.stochastic_keyed_batch(*ca, 0, 200.0, 1e-12, q, 2, 0, 9,
-                             np.arange(n, dtype=np.uint64) + 100, *got)
+    O.stochastic_ex_batch(*ca, 0, 200.0, 1e-12, q, 2, 0, 9, 0, *got,
+                          keys=np.arange(n, dtype=np.uint64) + 100)
     for x, y in zip(ref, got):
         np.testing.assert_array_equal(x, y)
+
+
+def test_oracle_alg2_walk_is_unbiased():
+    """The paper's Alg. 2 (roulette before each swap): the mean over many keys
+    converges to brute force (an unbiased estimator, like the reference's walk)."""
+    s, ca = _small_tree(d=4, m=2000)
+    q = np.random.default_rng(8).uniform(-0.7, 0.7, (8, 3))
+    n = len(q)
+    truth = np.zeros(n)
+    O.brute_force_batch(0, 200.0, 1e-12, s.positions, s.masses, q, truth)
+    reps = 4000
+    runs = np.zeros((reps, n))
+    for r in range(reps):
+        out = [np.zeros(n)] + [np.zeros(n, dtype=np.int64) for _ in range(3)]
+        O.stochastic_ex_batch(*ca, 0, 200.0, 1e-12, q, 1, 0, 17, r * n, *out, variant=1)
+        runs[r] = out[0]
+    se = runs.std(axis=0, ddof=1) / np.sqrt(reps)
+    assert (np.abs(runs.mean(axis=0) - truth) <= 4 * se + 1e-9 * np.abs(truth)).all()
+    # it differs from the reference walk draw for draw
+    ref = [np.zeros(n)] + [np.zeros(n, dtype=np.int64) for _ in range(3)]
+    O.stochastic_batch(*ca, 0, 200.0, 1e-12, q, 1, 0, 17, 0, *ref)
+    assert not np.array_equal(ref[0], runs[0])

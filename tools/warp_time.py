@@ -33,8 +33,8 @@ S = int(os.environ.get("S", "1"))
 
 
 def run(group):
-    _lib.check(L.fsb_stochastic_batch_shared(h, 0, kern.alpha, kern.distance_floor, 1, vp(q), n,
-                                             vp(order), S, 0, 1, 0, group, vp(out), None, None,
+    _lib.check(L.fsb_stochastic_batch_ex(h, 0, kern.alpha, kern.distance_floor, 1, vp(q), n,
+                                             vp(order), S, 0, 1, 0, group, 0, vp(out), None, None,
                                              None, sp))
 
 
