@@ -632,9 +632,6 @@ __device__ unsigned long long g_warp_stats[8];
 #ifndef FSB_WARP_DENSE2
 #define FSB_WARP_DENSE2 1
 #endif
-#ifndef FSB_WARP_SERIAL
-#define FSB_WARP_SERIAL 1
-#endif
 #ifndef FSB_WARP_DENSE_UNROLL
 #define FSB_WARP_DENSE_UNROLL 4
 #endif
@@ -887,8 +884,10 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
           const bool cmulti = lvl + 1 >= V.first_multi;
           float ks0 = 0.f, ks1 = 0.f;
           int le = 0, c = 0;
-          const unsigned am = __ballot_sync(0xffffffffu, alive);
           const bool use_path = !cmulti && lvl < V.path_levels;
+#ifdef FSB_WARP_STATS
+          const unsigned am = __ballot_sync(0xffffffffu, alive);
+#endif
           WSTAT(1, 1);
           WSTAT(2, __popc(am));
           WSTAT(5, tp.y);
@@ -902,25 +901,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             tpn = V.topo[tp.x + le - 1];
             cch = V.cm[tp.x + le - 1];
           }
-          if (FSB_WARP_SERIAL && use_path &&
-              __popc(am) * (((tp.y + 31) >> 5) * 11 + 14) < tp.y * 10) {
-            // few live queries: one at a time, lanes over the children, then a
-            // butterfly sum (work ~ live queries x children, not 32 x children)
-            WSTAT(4, 1);
-            for (unsigned mm = am; mm; mm &= mm - 1) {
-              const int src = __ffs(mm) - 1;
-              const float sx = __shfl_sync(0xffffffffu, qx, src),
-                          sy = __shfl_sync(0xffffffffu, qy, src),
-                          sz = __shfl_sync(0xffffffffu, qz, src);
-              float part = 0.f;
-              for (int k = lane; k < tp.y; k += 32)
-                part += fterm<KID>(V.cm[tp.x + k], KID == KID_WINDING ? V.m12[tp.x + k] : w0, sx,
-                                   sy, sz, kp);
-#pragma unroll
-              for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-              if (lane == src) ks0 = part;
-            }
-          } else if (kPack && use_path) {
+          if (kPack && use_path) {
             // packed children: node pairs (2i, 2i+1) in one 32-byte load, two
             // terms per FADD2/FFMA2 (floor as r2 + floor^2)
             const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy),
@@ -1150,9 +1131,9 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
       FS_CK(cudaStreamSynchronize(s));
       const double nw = (double)((n + 31) / 32);
       fprintf(stderr,
-              "warp stats per 32-query chunk: pairs %.1f, walks %.1f, levels %.1f (serial %.1f), "
+              "warp stats per 32-query chunk: pairs %.1f, walks %.1f, levels %.1f, "
               "live lanes/level %.2f, children/level %.1f, useful child evals %.0f of %.0f\n",
-              z[6] / nw, z[0] / nw, z[1] / nw, z[4] / nw, (double)z[2] / std::max(1ull, z[1]),
+              z[6] / nw, z[0] / nw, z[1] / nw, (double)z[2] / std::max(1ull, z[1]),
               (double)z[5] / std::max(1ull, z[1]), z[7] / nw, 32.0 * z[5] / nw);
 #endif
       return 0;
