@@ -668,7 +668,11 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   const int o_int = o_lut + n1 * (kLut + 1), o_leaf = o_int + n1;  // 2 B subdomain lists
 #define s_int(i) sh_u16[o_int + (i)]
 #define s_leaf(i) sh_u16[o_leaf + (i)]
+  // per-warp sample table (16-B units, after the 2-B lists): 32 x {a_ord, lo, j, u0},
+  // 32 x {kr.lo, kr.hi, u1, u2}, 32 x {path.lo, path.hi, -, -}
+  const int o_smp = (o_leaf + n1 + 7) / 8;
   const int tid = threadIdx.x, lane = tid & 31;
+  int4* const s_smp = reinterpret_cast<int4*>(sh_i4 + o_smp) + (tid >> 5) * 96;
   for (int i = tid; i < n1; i += kWarpBlock) {
     s_cm1(i) = V.cm[1 + i];
     s_tp1(i) = V.topo[1 + i];
@@ -722,6 +726,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
   const float2 w0 = make_float2(0.f, 0.f);
   const int nslot = n_int * S;
+  const float inv_s = __frcp_rn((float)S);
   const int64_t nchunks = (n + 31) / 32;
   // 32-query chunks from a global counter; the next chunk is claimed one chunk
   // ahead so the atomic's latency hides behind the current chunk
@@ -735,9 +740,13 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     if (lane == 0) claim = atomicAdd(chunk_ctr, 1u);
     const int64_t t = (int64_t)ch * 32 + lane;
     const bool live = t < n;
-    const int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
-    const float qx = live ? (float)q[3 * qi] : 0.f, qy = live ? (float)q[3 * qi + 1] : 0.f,
-                qz = live ? (float)q[3 * qi + 2] : 0.f;
+    float qx = 0.f, qy = 0.f, qz = 0.f;
+    if (live) {  // (the index is reloaded for the stores: fewer live registers)
+      const int64_t qi = qperm ? (int64_t)qperm[t] : t;
+      qx = (float)q[3 * qi];
+      qy = (float)q[3 * qi + 1];
+      qz = (float)q[3 * qi + 2];
+    }
     const uint64_t hq = key_fold(hseed, (uint64_t)(((int64_t)ch * 32 + qoff) >> 5));
 
     // ---- dense part: every level-2 record (as k_sto_fast) + leaf subdomains
@@ -812,15 +821,16 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     }
 
     int seen = seen_base, steps = 0;
-    double acc_deep = 0.0;
+    float acc_deep = 0.f;  // FP32 sum of the walks' residuals (<= n1 * S terms)
     for (int f0 = 0; f0 < nslot; f0 += 32) {
       // lane L draws sample f0 + L for the whole warp: index draw exactly as
       // _core.py:166-169, level-1 step from shared memory
-      int my_a = -1, my_lo = 0, my_j = 0;
-      uint64_t my_kr = 0;
-      float my_u0 = 0.f, my_u1 = 0.f, my_u2 = 0.f;  // roulette draws, counters 0..2
-      uint64_t my_path = 0;  // the sampled point's sibling ranks (loaded early)
+      // the warp's sample table (broadcast reads below): a_ord < 0 = no sample
       {
+        int my_a = -1, my_lo = 0, my_j = 0;
+        uint64_t my_kr = 0;
+        float my_u0 = 0.f, my_u1 = 0.f, my_u2 = 0.f;  // roulette draws, counters 0..2
+        uint64_t my_path = 0;  // the sampled point's sibling ranks (loaded early)
         const int f = f0 + lane;
         if (f < nslot) {
           const int ai = f / S, sm = f - ai * S;
@@ -850,23 +860,28 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             }
           }
         }
+        __syncwarp();  // the previous round's readers are done
+        s_smp[lane] = make_int4(my_a, my_lo, my_j, __float_as_int(my_u0));
+        s_smp[32 + lane] = make_int4((int)(uint32_t)my_kr, (int)(uint32_t)(my_kr >> 32),
+                                     __float_as_int(my_u1), __float_as_int(my_u2));
+        s_smp[64 + lane] = make_int4((int)(uint32_t)my_path, (int)(uint32_t)(my_path >> 32), 0, 0);
+        __syncwarp();
       }
       const int cnt = min(32, nslot - f0);
       for (int i = 0; i < cnt; ++i) {
-        const int a_ord = __shfl_sync(0xffffffffu, my_a, i);
+        const int4 sa = s_smp[i];
+        const int a_ord = sa.x;
         if (a_ord < 0) continue;  // warp-uniform
-        const int lo = __shfl_sync(0xffffffffu, my_lo, i);
-        const int jj = __shfl_sync(0xffffffffu, my_j, i);
-        const uint64_t kr = ((uint64_t)__shfl_sync(0xffffffffu, (unsigned)(my_kr >> 32), i) << 32) |
-                            __shfl_sync(0xffffffffu, (unsigned)my_kr, i);
-        const float u1 = __shfl_sync(0xffffffffu, my_u1, i),
-                    u2 = __shfl_sync(0xffffffffu, my_u2, i);
+        const int lo = sa.y, jj = sa.z;
+        const float ua = __int_as_float(sa.w);
+        const int4 sb = s_smp[32 + i];
+        const uint64_t kr = ((uint64_t)(uint32_t)sb.y << 32) | (uint32_t)sb.x;
+        const float u1 = __int_as_float(sb.z), u2 = __int_as_float(sb.w);
         const int4 tpa = s_tp1(a_ord);
         const float fcount_a = (float)(tpa.w - tpa.z);
         const float4 c2 = s_cm2(lo);
         float rp = fdist(c2, qx, qy, qz) * id2;
         float prr = rr_fast_t<RR>(fdist(s_cm1(a_ord), qx, qy, qz) * id1, rp);
-        const float ua = __shfl_sync(0xffffffffu, my_u0, i);
         bool alive = live && (RR == 2 || prr >= 1.f || ua < prr);
         WSTAT(6, 1);
         if (!__any_sync(0xffffffffu, alive)) continue;
@@ -875,9 +890,8 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
         float cvn = fterm<KID>(c2, KID == KID_WINDING ? s_w2(lo) : w0, qx, qy, qz, kp);
         const int2 t2 = s_t2(lo);
         int4 tp = make_int4(t2.x & 0x1ffffff, (int)((unsigned)t2.x >> 25), 0, t2.y);
-        const uint64_t path =
-            ((uint64_t)__shfl_sync(0xffffffffu, (unsigned)(my_path >> 32), i) << 32) |
-            __shfl_sync(0xffffffffu, (unsigned)my_path, i);
+        const int2 sp = *reinterpret_cast<const int2*>(&s_smp[64 + i]);
+        const uint64_t path = ((uint64_t)(uint32_t)sp.y << 32) | (uint32_t)sp.x;
         int lvl = 2;
         float resid = 0.f;
         while (tp.y > 0) {  // warp-uniform: every lane walks the same node
@@ -997,12 +1011,13 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
           tp = tpn;
           ++lvl;
         }
-        acc_deep += (double)resid;
+        acc_deep += resid;
       }
     }
     next = __shfl_sync(0xffffffffu, claim, 0);
     if (live) {
-      out[qi] = (float)(acc + acc_deep / (double)S);
+      const int64_t qi = qperm ? (int64_t)qperm[t] : t;
+      out[qi] = (float)(acc + (double)(acc_deep * inv_s));
       if (visited) visited[qi] = seen;
       if (path_steps) path_steps[qi] = steps;
       if (path_count) path_count[qi] = (int64_t)S * n_int;
@@ -1107,8 +1122,8 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     // warp-shared streams on warp-aligned groups: the warp-uniform kernel
     const size_t wsmem =
         ((16 * (2 * n1 + n2 + (kid == KID_COULOMB && FSB_WARP_DENSE2 ? 2 * ((n2 + 1) / 2) : 0)) +
-          8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 3)) +
-         15) & ~(size_t)15;
+          8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 3) + 128) & ~(size_t)127) +
+        (size_t)(kWarpBlock / 32) * 96 * 16;  // + per-warp sample tables
     auto launch_w = [&](auto kern) -> int {
       if (wsmem > 48 * 1024)
         FS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
