@@ -337,8 +337,10 @@ int ensure_path(FsTree* t, cudaStream_t s) {
   FS_TRY(dalloc(&t->pt_path, t->m, s));
   t->path_bits = bits;
   t->path_levels = bits <= 16 ? 64 / bits : 0;
+  t->max_children = kids;
   k_point_path<<<grid_for(t->m, 256), 256, 0, s>>>(t->lo_topo, t->m, bits, t->path_levels,
                                                    t->pt_path);
+
   FS_CK(cudaGetLastError());
   return 0;
 }

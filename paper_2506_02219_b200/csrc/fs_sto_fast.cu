@@ -874,9 +874,6 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
         if (a_ord < 0) continue;  // warp-uniform
         const int lo = sa.y, jj = sa.z;
         const float ua = __int_as_float(sa.w);
-        const int4 sb = s_smp[32 + i];
-        const uint64_t kr = ((uint64_t)(uint32_t)sb.y << 32) | (uint32_t)sb.x;
-        const float u1 = __int_as_float(sb.z), u2 = __int_as_float(sb.w);
         const int4 tpa = s_tp1(a_ord);
         const float fcount_a = (float)(tpa.w - tpa.z);
         const float4 c2 = s_cm2(lo);
@@ -909,11 +906,9 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
           // with the path, the picked child is known up front: its record and
           // topology load while the children are summed
           int4 tpn = make_int4(0, 0, 0, 0);
-          float4 cch = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (use_path) {
+          if (use_path) {  // the next node's topology loads while the children are summed
             le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
             tpn = V.topo[tp.x + le - 1];
-            cch = V.cm[tp.x + le - 1];
           }
           if (kPack && use_path) {
             // packed children: node pairs (2i, 2i+1) in one 32-byte load, two
@@ -986,10 +981,8 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             }
           }
           const int cidx = tp.x + le - 1;
-          if (!use_path) {
-            cch = V.cm[cidx];
-            tpn = V.topo[cidx];
-          }
+          const float4 cch = V.cm[cidx];  // one of the children just summed: L1 hit
+          if (!use_path) tpn = V.topo[cidx];
           if (alive) {  // swap / (p_agg * p_rr), p_agg = points(node) / points(a)
             seen += tp.y + 1;
             resid += ((ks0 + ks1) - cvn) * (fcount_a * rcp_ftz((float)(tp.w - tp.z) * prr));
@@ -997,9 +990,14 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
           const float rc = fdist(cch, qx, qy, qz) * V.inv_diam[min(lvl + 1, kFastMaxLevels - 1)];
           const float p = rr_fast_t<RR>(rp, rc);
           const int ctr = lvl - 1;  // levels descended so far (uniform)
-          const float u = ctr == 1 ? u1
-                          : ctr == 2 ? u2
-                                     : (RR == 2 ? 0.f : draw24(kr, (uint64_t)ctr));
+          float u = 0.f;  // roulette draws from the sample table (counters 1, 2) or the stream
+          if (RR != 2) {
+            const int4 sb = s_smp[32 + i];
+            u = ctr == 1   ? __int_as_float(sb.z)
+                : ctr == 2 ? __int_as_float(sb.w)
+                           : draw24(((uint64_t)(uint32_t)sb.y << 32) | (uint32_t)sb.x,
+                                    (uint64_t)ctr);
+          }
           alive = alive && (RR == 2 || p >= 1.f || u < p);
           if (!__any_sync(0xffffffffu, alive)) break;
           if (alive) {
@@ -1054,6 +1052,9 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   V.pa = t->pts32a;
   V.pb = t->pts32b;
   FS_TRY(ensure_path(t, s));
+  // the packed level-2 topology {first child | count << 25} needs < 128 children
+  // per node (branching <= 5) and < 2^25 nodes
+  if (t->max_children >= 128 || t->n >= (1ll << 25)) return 0;
   V.path = t->pt_path;
   V.cmp = nullptr;
   V.path_bits = t->path_bits;

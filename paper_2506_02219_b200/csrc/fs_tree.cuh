@@ -65,6 +65,7 @@ struct FsTree {
   // 1..path_levels, path_bits bits per level (child pick without begins)
   uint64_t* pt_path = nullptr;
   int path_bits = 0, path_levels = 0;
+  int max_children = 0;  // (ensure_path)
 };
 
 }  // namespace fsb

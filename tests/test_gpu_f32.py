@@ -245,3 +245,24 @@ def test_warp_mode_host_pipeline_equals_device_path(fs, prec):
         np.testing.assert_array_equal(r.raw, ref.raw)
         np.testing.assert_array_equal(r.path_steps, ref.path_steps)
         np.testing.assert_array_equal(r.visited_nodes, ref.visited_nodes)
+
+
+@pytest.mark.parametrize("d", [5, 6])
+def test_wide_trees_fall_back_or_run_fast(fs, d):
+    """Branching 5 (125 children) runs the fast FP32 kernels; branching 6 (216
+    children) exceeds their packed topology (count < 128) and runs the generic
+    kernel.  Both track the FP64 kernel on the same draws, in both stream modes."""
+    s = scenes.build_sources(dict(kind="mesh_torus", m=20000, seed=9))
+    kern = fs.KernelSpec("coulomb")
+    q = fs.QuerySet(np.random.default_rng(3).uniform(-0.6, 0.6, (1000, 3)))
+    t = fs.build_tree(s, d)
+    for sharing in ("query", "warp"):
+        a = fs.evaluate_field(fs.EstimatorConfig("stochastic", seed=4, precision="f32",
+                                                 branching_per_dim=d, rng_sharing=sharing),
+                              s, kern, q, tree=t)
+        b = fs.evaluate_field(fs.EstimatorConfig("stochastic", seed=4, precision="f64",
+                                                 branching_per_dim=d, rng_sharing=sharing),
+                              s, kern, q, tree=t)
+        close = _rel(a.raw, b.raw) <= 1e-4
+        assert close.mean() >= 0.97, (sharing, close.mean())
+        assert ((a.path_steps == b.path_steps).mean()) >= 0.97
