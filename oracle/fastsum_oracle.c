@@ -771,3 +771,44 @@ void or_draws(uint64_t seed, uint64_t qi, uint64_t sub, uint64_t sample, uint64_
     uint64_t key = or_stream_key(seed, qi, sub, sample, stream);
     for (int64_t i = 0; i < count; ++i) out[i] = or_uniform_draw(key, (uint64_t)i);
 }
+
+/* The warp-shared mode's evaluation order (not in the reference; restates
+ * k_shuffle in csrc/fs_abi.cu): windows of 2^16 positions, each permuted by a
+ * 4-round balanced Feistel network (lowbias32 rounds) keyed on (seed,
+ * query_offset + window start), cycle-walked into a partial last window. */
+static inline uint64_t key_fold(uint64_t h, uint64_t v) { return mix64(h ^ (v + GAMMA)); }
+
+static inline uint32_t hash32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    return x ^ (x >> 16);
+}
+
+static inline uint32_t feistel4(uint32_t x, int hb, const uint32_t ks[4]) {
+    uint32_t mask = (1u << hb) - 1u, l = x >> hb, r = x & mask;
+    for (int i = 0; i < 4; ++i) {
+        uint32_t f = hash32(ks[i] ^ r) & mask, nl = r;
+        r = l ^ f;
+        l = nl;
+    }
+    return (l << hb) | r;
+}
+
+void or_shuffle_order(int64_t n, uint64_t seed, int64_t query_offset, int32_t *perm) {
+    const int64_t W = (int64_t)1 << 16;
+    const uint64_t h = key_fold(mix64(seed + GAMMA), 0x73687566ull);
+    for (int64_t base = 0; base < n; base += W) {
+        uint32_t size = (uint32_t)(n - base < W ? n - base : W);
+        int hb = 1;
+        while ((1u << (2 * hb)) < size) ++hb;
+        uint64_t hw = key_fold(h, (uint64_t)(query_offset + base)), hw1 = key_fold(hw, 1);
+        uint32_t ks[4] = {(uint32_t)hw, (uint32_t)(hw >> 32), (uint32_t)hw1, (uint32_t)(hw1 >> 32)};
+        for (uint32_t i = 0; i < size; ++i) {
+            uint32_t y = feistel4(i, hb, ks);
+            while (y >= size) y = feistel4(y, hb, ks);
+            perm[base + i] = (int32_t)(base + y);
+        }
+    }
+}

@@ -287,3 +287,20 @@ def rr_probability(rp, rc, mode) -> float:
 def np_sum(a) -> float:
     a = _f64(a)
     return float(lib().or_np_sum(_dp(a), a.shape[0]))
+
+
+def shuffle_order(n, seed, query_offset=0):
+    """The warp-shared mode's evaluation order (restates fsb_shuffle_order)."""
+    perm = np.zeros(int(n), dtype=np.int32)
+    lib().or_shuffle_order(C.c_int64(n), C.c_uint64(int(seed)), C.c_int64(query_offset),
+                           perm.ctypes.data_as(C.c_void_p))
+    return perm
+
+
+def shared_keys(n, seed, query_offset=0, group_log2=5):
+    """keys[i] of stochastic_ex_batch for the warp-shared mode: the group index of the
+    position query i takes in shuffle_order (positions offset by query_offset)."""
+    order = shuffle_order(n, seed, query_offset).astype(np.int64)
+    keys = np.zeros(int(n), dtype=np.uint64)
+    keys[order] = ((np.arange(n) + query_offset) >> group_log2).astype(np.uint64)
+    return keys

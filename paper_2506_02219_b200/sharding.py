@@ -4,7 +4,9 @@ Queries are independent and every stochastic draw is keyed on the *global*
 query index (stochastic_batch's ``query_offset``, reference _core.py:219,258),
 so rank r evaluates the contiguous slab [r*N/P, (r+1)*N/P) with
 query_offset = slab start and the gathered field is identical to a
-single-process evaluation.  The tree is a replica per rank (the GPU build is
+single-process evaluation (with the paper's warp-shared streams the slab
+boundaries are multiples of the 2^16-position shuffle window, so the same holds).
+The tree is a replica per rank (the GPU build is
 deterministic, so every rank builds the same bits); results are gathered with
 one all_gather -- the only collective on this path.
 """
@@ -13,24 +15,34 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["slab", "gather_slabs", "evaluate_field_sharded"]
+__all__ = ["slab", "gather_slabs", "evaluate_field_sharded", "SHUFFLE_WINDOW"]
+
+SHUFFLE_WINDOW = 1 << 16  # positions per window of fsb_shuffle_order (warp-shared mode)
 
 
-def slab(n: int, rank: int, world: int) -> tuple[int, int]:
-    """[start, stop) of rank's contiguous, balanced share of n queries."""
-    if world < 1 or not 0 <= rank < world:
-        raise ValueError("bad rank / world size")
-    base, extra = divmod(n, world)
-    start = rank * base + min(rank, extra)
-    return start, start + base + (1 if rank < extra else 0)
+def slab(n: int, rank: int, world: int, align: int = 1) -> tuple[int, int]:
+    """[start, stop) of rank's contiguous, balanced share of n queries; with align > 1
+    every boundary but the end is a multiple of align (the warp-shared mode's 2^16
+    shuffle windows, so slabs evaluate exactly as inside the whole set)."""
+    if world < 1 or not 0 <= rank < world or align < 1:
+        raise ValueError("bad rank / world size / alignment")
+
+    def cut(r):
+        if r >= world:
+            return n
+        base, extra = divmod(n, world)
+        c = r * base + min(r, extra)
+        return min(n, (c + align // 2) // align * align) if align > 1 else c
+
+    return cut(rank), cut(rank + 1)
 
 
-def gather_slabs(local, n: int, group=None):
+def gather_slabs(local, n: int, group=None, align: int = 1):
     """All-gather equal-or-ragged slabs (torch tensors, 1-D) into the full (n,) field."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    sizes = [slab(n, r, world)[1] - slab(n, r, world)[0] for r in range(world)]
+    sizes = [slab(n, r, world, align)[1] - slab(n, r, world, align)[0] for r in range(world)]
     width = max(sizes)
     pad = torch.zeros(width, dtype=local.dtype, device=local.device)
     pad[: local.shape[0]] = local
@@ -47,7 +59,16 @@ def evaluate_field_sharded(config, sources, kernel, queries, tree=None, group=No
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     n = len(queries)
-    a, b = slab(n, rank, world)
-    local = evaluate_field_device(config, sources, kernel, QuerySet(queries.positions[a:b]), tree,
-                                  query_offset=a)
-    return gather_slabs(local.values, n, group).cpu().numpy()
+    a, b = slab(n, rank, world, SHUFFLE_WINDOW if _shared(config) else 1)
+    if b > a:
+        local = evaluate_field_device(config, sources, kernel, QuerySet(queries.positions[a:b]),
+                                      tree, query_offset=a).values
+    else:  # more ranks than slabs: this rank contributes nothing
+        import torch
+        local = torch.empty(0, dtype=torch.float64, device="cuda")
+    return gather_slabs(local, n, group, SHUFFLE_WINDOW if _shared(config) else 1).cpu().numpy()
+
+
+def _shared(config) -> bool:
+    return (getattr(config, "method", "") == "stochastic"
+            and getattr(config, "rng_sharing", "query") == "warp")

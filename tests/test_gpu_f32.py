@@ -220,6 +220,10 @@ def test_shuffle_order_is_a_seeded_window_local_permutation(fs):
         np.testing.assert_array_equal(a // W, np.arange(n) // W)  # window-local
         if n > 31:
             assert (a != c).mean() > 0.9 and (a != np.arange(n)).mean() > 0.9
+    # the oracle restatement (used by the CPU sharding tests) is the same permutation
+    from oracle import oracle as O
+    for n, seed, off in ((1000, 5, 0), (2 * W + 17, 7, 3 * W), (W, 2 ** 64 - 1, 12345)):
+        np.testing.assert_array_equal(order(n, seed, off), O.shuffle_order(n, seed, off))
     # a window-aligned slab with its offset reproduces the whole call's order
     whole = order(3 * W, 9)
     np.testing.assert_array_equal(order(W, 9, off=2 * W), whole[2 * W:] - 2 * W)
