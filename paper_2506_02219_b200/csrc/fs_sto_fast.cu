@@ -629,13 +629,13 @@ __device__ unsigned long long g_warp_stats[8];
 #ifndef FSB_WARP_MINB
 #define FSB_WARP_MINB 4
 #endif
+#ifndef FSB_DENSE_CHUNK
+#define FSB_DENSE_CHUNK 16  // record pairs per FP32 partial of the dense part (0.513 / 0.499 / 0.494 ms at 4 / 8 / 16)
+#endif
+constexpr int kDenseChunk = FSB_DENSE_CHUNK;
 #ifndef FSB_WARP_DENSE2
 #define FSB_WARP_DENSE2 1
 #endif
-#ifndef FSB_WARP_DENSE_UNROLL
-#define FSB_WARP_DENSE_UNROLL 4
-#endif
-constexpr int kDenseUnroll = FSB_WARP_DENSE_UNROLL;
 
 template <int KID, int RR>
 __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
@@ -767,17 +767,20 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
         const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
         return __ffma2_rn(make_float2(B.z, B.w), ri, a);
       };
-      for (int k = 0; k < np2; k += 8) {  // FP32 partials over 16 records
-        const int e = min(k + 8, np2);
+      int k = 0;
+      for (; k + kDenseChunk <= np2; k += kDenseChunk) {  // FP32 partials, fully unrolled
         float2 a0 = make_float2(0.f, 0.f), a1 = a0;
-        int i = k;
-#pragma unroll kDenseUnroll
-        for (; i + 1 < e; i += 2) {
-          a0 = pair_term(i, a0);
-          a1 = pair_term(i + 1, a1);
+#pragma unroll
+        for (int u = 0; u < kDenseChunk; u += 2) {
+          a0 = pair_term(k + u, a0);
+          a1 = pair_term(k + u + 1, a1);
         }
-        if (i < e) a0 = pair_term(i, a0);
         acc += (double)((a0.x + a0.y) + (a1.x + a1.y));
+      }
+      if (k < np2) {
+        float2 a0 = make_float2(0.f, 0.f);
+        for (; k < np2; ++k) a0 = pair_term(k, a0);
+        acc += (double)(a0.x + a0.y);
       }
     } else if (!l2_multi) {
       int k = 0;
