@@ -154,6 +154,63 @@ __device__ __forceinline__ bool survive(float p, uint64_t kr, uint64_t ctr) {
 // index-draw buckets per subdomain (top FSB_LUT_BITS bits of the draw)
 constexpr int kLutBits = FSB_LUT_BITS, kLut = 1 << kLutBits;
 
+#ifndef FSB_WARP_DENSE2
+#define FSB_WARP_DENSE2 1  // Coulomb dense part on the packed FP32 pipe
+#endif
+#ifndef FSB_DENSE_CHUNK
+#define FSB_DENSE_CHUNK 16  // record pairs per FP32 partial of the dense part (0.513 / 0.499 / 0.494 ms at 4 / 8 / 16)
+#endif
+constexpr int kDenseChunk = FSB_DENSE_CHUNK;
+
+// Coulomb dense part over level-2 records staged in shared memory as pairs
+// {x0,x1,y0,y1}, {z0,z1,-m0,-m1} at sh_f4[o_p2 ...]: packed FP32 (FADD2/FFMA2),
+// two records per instruction, the distance floor as r2 + floor^2 (see
+// k_brute32_coulomb2), FP32 partials over 2 * kDenseChunk records in fully
+// unrolled chunks folded into FP64.
+__device__ __forceinline__ double dense_coulomb_pairs(int o_p2, int np2, float qx, float qy,
+                                                      float qz, float dfloor) {
+  const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy), nz = make_float2(-qz, -qz);
+  const float f2 = dfloor * dfloor;
+  const float2 fl2 = make_float2(f2, f2);
+  auto pair_term = [&](int i, float2 a) {
+    const float4 A = sh_f4[o_p2 + 2 * i], B = sh_f4[o_p2 + 2 * i + 1];
+    const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
+    const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
+    const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
+    const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
+    const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+    return __ffma2_rn(make_float2(B.z, B.w), ri, a);
+  };
+  double acc = 0.0;
+  int k = 0;
+  for (; k + kDenseChunk <= np2; k += kDenseChunk) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+#pragma unroll
+    for (int u = 0; u < kDenseChunk; u += 2) {
+      a0 = pair_term(k + u, a0);
+      a1 = pair_term(k + u + 1, a1);
+    }
+    acc += (double)((a0.x + a0.y) + (a1.x + a1.y));
+  }
+  if (k < np2) {
+    float2 a0 = make_float2(0.f, 0.f);
+    for (; k < np2; ++k) a0 = pair_term(k, a0);
+    acc += (double)(a0.x + a0.y);
+  }
+  return acc;
+}
+
+// stages level-2 records [base2, base2 + n2) as Coulomb pairs (odd tail: a massless copy)
+__device__ __forceinline__ void stage_coulomb_pairs(const float4* __restrict__ cm, int base2,
+                                                    int n2, int o_p2, int tid, int nthreads) {
+  for (int i = tid; i < (n2 + 1) / 2; i += nthreads) {
+    const float4 u = cm[base2 + 2 * i];
+    const float4 v = 2 * i + 1 < n2 ? cm[base2 + 2 * i + 1] : make_float4(u.x, u.y, u.z, 0.f);
+    sh_f4[o_p2 + 2 * i] = make_float4(u.x, v.x, u.y, v.y);
+    sh_f4[o_p2 + 2 * i + 1] = make_float4(u.z, v.z, -u.w, -v.w);
+  }
+}
+
 template <int KID, int RR>
 __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     k_sto_fast(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
@@ -178,6 +235,9 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   const int o_t2 = (o_count + 5) / 2;  // (8-byte units, aligned) level-2 {first child | count << 25, points}
   const int o_hist = 2 * (o_t2 + n2);  // walk starts per level-2 node, then their offsets
   const int o_lut = 2 * (o_hist + n2 + (n2 & 1));
+  // Coulomb: level-2 records also as packed pairs (16-B units, after the table)
+  constexpr bool kPack = KID == KID_COULOMB && FSB_WARP_DENSE2;
+  const int o_p2 = (2 * (o_lut + n1 * (kLut + 1)) + 15) / 16;
 #define s_q(i) sh_f4[(i)]
 #define s_cm1(i) sh_f4[o_cm1 + (i)]
 #define s_tp1(i) sh_i4[o_tp1 + (i)]
@@ -220,6 +280,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     s_b2(i) = b;
     s_t2(i) = make_int2(tp.y > 0 ? (tp.x | (tp.y << 25)) : 0, tp.w - tp.z);
   }
+  if (kPack && !l2_multi) stage_coulomb_pairs(V.cm, V.base2, n2, o_p2, tid, kBlock);
   if (tid < 4) s_count(tid) = 0;  // [0] queue length, [1] drain head
   s_seen(tid) = 0;
   s_steps(tid) = 0;
@@ -284,7 +345,9 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     // ---- dense part (see the header): every level-2 record, FP32 partial
     // sums over 16 records folded into the FP64 accumulator
     double acc = 0.0;
-    if (!l2_multi) {
+    if (kPack && !l2_multi) {
+      acc = dense_coulomb_pairs(o_p2, (n2 + 1) / 2, qx, qy, qz, kp.dfloor_f);
+    } else if (!l2_multi) {
       int k = 0;
       for (; k + 16 <= n2; k += 16) {
         float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
@@ -629,13 +692,6 @@ __device__ unsigned long long g_warp_stats[8];
 #ifndef FSB_WARP_MINB
 #define FSB_WARP_MINB 4
 #endif
-#ifndef FSB_DENSE_CHUNK
-#define FSB_DENSE_CHUNK 16  // record pairs per FP32 partial of the dense part (0.513 / 0.499 / 0.494 ms at 4 / 8 / 16)
-#endif
-constexpr int kDenseChunk = FSB_DENSE_CHUNK;
-#ifndef FSB_WARP_DENSE2
-#define FSB_WARP_DENSE2 1
-#endif
 
 template <int KID, int RR>
 __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
@@ -688,12 +744,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     s_b2(i) = b;
     s_t2(i) = make_int2(tp.y > 0 ? (tp.x | (tp.y << 25)) : 0, tp.w - tp.z);
   }
-  for (int i = tid; i < np2; i += kWarpBlock) {  // odd tail: a massless copy
-    const float4 u = V.cm[V.base2 + 2 * i];
-    const float4 v = 2 * i + 1 < n2 ? V.cm[V.base2 + 2 * i + 1] : make_float4(u.x, u.y, u.z, 0.f);
-    s_p2(2 * i) = make_float4(u.x, v.x, u.y, v.y);
-    s_p2(2 * i + 1) = make_float4(u.z, v.z, -u.w, -v.w);
-  }
+  if (kPack) stage_coulomb_pairs(V.cm, V.base2, n2, o_p2, tid, kWarpBlock);
   __syncthreads();
   for (int i = tid; i < n1 * (kLut + 1); i += kWarpBlock) {
     const int a = i / (kLut + 1), b = i - a * (kLut + 1);
@@ -752,36 +803,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     // ---- dense part: every level-2 record (as k_sto_fast) + leaf subdomains
     double acc = 0.0;
     if (kPack && !l2_multi) {
-      // packed FP32 (FADD2/FFMA2): two records per instruction; the distance
-      // floor enters as r2 + floor^2 (as k_brute32_coulomb2)
-      const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy),
-                   nz = make_float2(-qz, -qz);
-      const float f2 = kp.dfloor_f * kp.dfloor_f;
-      const float2 fl2 = make_float2(f2, f2);
-      auto pair_term = [&](int i, float2 a) {
-        const float4 A = s_p2(2 * i), B = s_p2(2 * i + 1);
-        const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
-        const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
-        const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
-        const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
-        const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
-        return __ffma2_rn(make_float2(B.z, B.w), ri, a);
-      };
-      int k = 0;
-      for (; k + kDenseChunk <= np2; k += kDenseChunk) {  // FP32 partials, fully unrolled
-        float2 a0 = make_float2(0.f, 0.f), a1 = a0;
-#pragma unroll
-        for (int u = 0; u < kDenseChunk; u += 2) {
-          a0 = pair_term(k + u, a0);
-          a1 = pair_term(k + u + 1, a1);
-        }
-        acc += (double)((a0.x + a0.y) + (a1.x + a1.y));
-      }
-      if (k < np2) {
-        float2 a0 = make_float2(0.f, 0.f);
-        for (; k < np2; ++k) a0 = pair_term(k, a0);
-        acc += (double)(a0.x + a0.y);
-      }
+      acc = dense_coulomb_pairs(o_p2, np2, qx, qy, qz, kp.dfloor_f);
     } else if (!l2_multi) {
       int k = 0;
       for (; k + 16 <= n2; k += 16) {
@@ -1079,7 +1101,8 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   const size_t n1 = (size_t)V.n1, n2 = (size_t)V.n2;
   size_t smem = 16 * ((size_t)kBlock + 2 * n1 + n2) + 8 * ((wind ? n1 + n2 : 0) + kBlock) +
                 4 * (2 * n2 + 2 * (size_t)kBlock + 6) + 8 * n2 + 2 * n1 * (kLut + 1);
-  smem = (smem + 15) & ~(size_t)15;
+  smem = (smem + 31) & ~(size_t)15;  // (+ alignment slack for the pair table)
+  if (kid == KID_COULOMB && FSB_WARP_DENSE2) smem += 32 * ((n2 + 1) / 2);
   if (n2 >= 65535 || (int64_t)nslot * kBlock >= (1ll << 31) || t->n >= (1ll << 25)) return 0;
   if (smem > 200 * 1024) return 0;
   KParams kp;
