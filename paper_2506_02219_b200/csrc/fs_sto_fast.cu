@@ -211,6 +211,47 @@ __device__ __forceinline__ void stage_coulomb_pairs(const float4* __restrict__ c
   }
 }
 
+// sum of the Coulomb terms of the contiguous children [first, first + count)
+// from the pair-interleaved records (ensure_pairs): one 32-byte load and packed
+// FP32 arithmetic per two children, the floor as r2 + floor^2
+__device__ __forceinline__ float children_coulomb_pairs(const float4* __restrict__ cmp,
+                                                        const float4* __restrict__ cm, int first,
+                                                        int count, float qx, float qy, float qz,
+                                                        const KParams& kp) {
+  const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy), nz = make_float2(-qz, -qz);
+  const float f2 = kp.dfloor_f * kp.dfloor_f;
+  const float2 fl2 = make_float2(f2, f2);
+  auto pair_acc = [&](int r, float2 acc2) {
+    float4 A, B;
+    ld_pair(cmp + r, A, B);  // r even: records r, r + 1
+    const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
+    const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
+    const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
+    const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
+    const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+    return __ffma2_rn(make_float2(B.z, B.w), ri, acc2);
+  };
+  const float2 z2 = make_float2(0.f, 0.f);
+  const int e = first + count;
+  int r = first;
+  float ks = 0.f;
+  if (r & 1) {
+    ks += contrib_fast<KID_COULOMB>(cm[r].w, 0.f, 0.f, cm[r].x, cm[r].y, cm[r].z, qx, qy, qz, kp);
+    ++r;
+  }
+  float2 a2 = z2, b2 = z2;
+  for (; r + 3 < e; r += 4) {
+    a2 = pair_acc(r, a2);
+    b2 = pair_acc(r + 2, b2);
+  }
+  if (r + 1 < e) {
+    a2 = pair_acc(r, a2);
+    r += 2;
+  }
+  if (r < e) ks += contrib_fast<KID_COULOMB>(cm[r].w, 0.f, 0.f, cm[r].x, cm[r].y, cm[r].z, qx, qy, qz, kp);
+  return ks + ((a2.x + a2.y) + (b2.x + b2.y));
+}
+
 template <int KID, int RR>
 __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     k_sto_fast(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
@@ -549,7 +590,9 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
               // the sampled point's path gives the child's rank: only the
               // aggregates are read (one 16-byte load per child)
               le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
-              // 32-byte loads of child pairs (one request per two children)
+              // 32-byte loads of child pairs (one request per two children).  (The
+              // pair-interleaved copy k_sto_warp uses measured slower here: these
+              // lanes walk different nodes, and the picked child is reread from cm.)
               if (tp.x & 1) {
                 ks0 += fterm<KID>(V.cm[tp.x], KID == KID_WINDING ? V.m12[tp.x] : w0, qq.x, qq.y,
                                   qq.z, kp);
@@ -936,39 +979,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             tpn = V.topo[tp.x + le - 1];
           }
           if (kPack && use_path) {
-            // packed children: node pairs (2i, 2i+1) in one 32-byte load, two
-            // terms per FADD2/FFMA2 (floor as r2 + floor^2)
-            const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy),
-                         nz = make_float2(-qz, -qz);
-            const float f2 = kp.dfloor_f * kp.dfloor_f;
-            const float2 fl2 = make_float2(f2, f2);
-            float2 a2 = make_float2(0.f, 0.f), b2 = a2;
-            const int e = tp.x + tp.y;
-            int r = tp.x;
-            if (r & 1) {
-              ks0 += fterm<KID>(V.cm[r], w0, qx, qy, qz, kp);
-              ++r;
-            }
-            auto pair_acc = [&](int rr, float2 acc2) {
-              float4 A, B;
-              ld_pair(V.cmp + rr, A, B);  // rr even: records rr, rr + 1
-              const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
-              const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
-              const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
-              const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
-              const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
-              return __ffma2_rn(make_float2(B.z, B.w), ri, acc2);
-            };
-            for (; r + 3 < e; r += 4) {
-              a2 = pair_acc(r, a2);
-              b2 = pair_acc(r + 2, b2);
-            }
-            if (r + 1 < e) {
-              a2 = pair_acc(r, a2);
-              r += 2;
-            }
-            if (r < e) ks0 += fterm<KID>(V.cm[r], w0, qx, qy, qz, kp);
-            ks1 = (a2.x + a2.y) + (b2.x + b2.y);
+            ks0 = children_coulomb_pairs(V.cmp, V.cm, tp.x, tp.y, qx, qy, qz, kp);
           } else if (use_path) {
             if (tp.x & 1) {
               ks0 += fterm<KID>(V.cm[tp.x], KID == KID_WINDING ? V.m12[tp.x] : w0, qx, qy, qz, kp);
@@ -1142,7 +1153,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     return 1;
   }
   if (share == 5 && (qoff & 31) == 0 && !std::getenv("FSB_STO_WARP_OFF")) {
-    if (kid == KID_COULOMB && FSB_WARP_DENSE2) {
+    if (kid == KID_COULOMB && FSB_WARP_DENSE2) {  // pair-interleaved records for the walks
       FS_TRY(ensure_pairs(t, s));
       V.cmp = t->lo_cmp;
     }
