@@ -303,14 +303,11 @@ def run_ours(args):
     vis = dev.empty(n, torch.int64)
     h = C.c_void_p(tree4._device_tree().handle)
 
-    order = dev.empty(n, torch.int32)
-    _lib.check(L.fsb_shuffle_order(n, 1, qoff, C.c_void_p(dev.ptr(order)), sp))
-
     def kernel_only():
-        if args.streams == "warp":  # k_sto_warp (the order is computed once, outside)
+        if args.streams == "warp":  # k_sto_warp (shuffled order computed in-kernel)
             _lib.check(L.fsb_stochastic_batch_ex(
                 h, 0, kern.alpha, kern.distance_floor, 1, C.c_void_p(dev.ptr(q_dev)), n,
-                C.c_void_p(dev.ptr(order)), 1, 0, 1, qoff, 5, 0, C.c_void_p(dev.ptr(raw)),
+                None, 1, 0, 1, qoff, 5, 2, C.c_void_p(dev.ptr(raw)),
                 C.c_void_p(dev.ptr(vis)), None, None, sp))
         else:  # k_sto_fast
             _lib.check(L.fsb_stochastic_batch(h, 0, kern.alpha, kern.distance_floor, 1,

@@ -102,20 +102,24 @@ int fsb_stochastic_batch(fsb_tree *tree, int kid, double alpha, double dfloor, i
 
 /* stochastic_batch plus the paper's options (not the reference's):
  *  - evaluation order and shared RNG streams: queries are
- *    evaluated in `order` (a permutation, NULL = 0..n-1; the paper shuffles the
- *    grid, see fsb_shuffle_order) and each group of 2^group_log2 consecutive
- *    positions shares one stream keyed on (seed, (position + query_offset) >>
- *    group_log2, subdomain, sample), so a warp follows one sampled path.
- *    Unbiased per query.  FP32 with group_log2 = 5 and query_offset % 32 == 0
- *    runs the warp-uniform kernel (k_sto_warp);
- *  - variant 1 = Alg. 2 of the paper's supplemental (roulette before each swap,
- *    including the subdomain's own; unbiased; the generic per-query kernel in
- *    either precision).  variant 0 is the reference's walk.
- * group_log2 = 0, variant = 0 and order = NULL is fsb_stochastic_batch. */
+ *    evaluated in `order` (a permutation, NULL = 0..n-1) and each group of
+ *    2^group_log2 consecutive positions shares one stream keyed on (seed,
+ *    (position + query_offset) >> group_log2, subdomain, sample), so a warp
+ *    follows one sampled path.  Unbiased per query.  FSB_FLAG_SHUFFLED: the
+ *    order is fsb_shuffle_order(n, seed, query_offset) (the paper shuffles the
+ *    grid), computed in-kernel by the warp-uniform kernel (`order` must be
+ *    NULL).  FP32 with group_log2 = 5 and query_offset % 32 == 0 runs that
+ *    kernel (k_sto_warp);
+ *  - FSB_FLAG_ALG2: Alg. 2 of the paper's supplemental (roulette before each
+ *    swap, including the subdomain's own; unbiased; the generic per-query
+ *    kernel in either precision).  Without it, the reference's walk.
+ * group_log2 = 0, flags = 0 and order = NULL is fsb_stochastic_batch. */
+#define FSB_FLAG_ALG2 1
+#define FSB_FLAG_SHUFFLED 2
 int fsb_stochastic_batch_ex(fsb_tree *tree, int kid, double alpha, double dfloor,
                             int precision, const double *queries, int64_t n,
                             const int32_t *order, int64_t n_samples, int rr_mode, uint64_t seed,
-                            int64_t query_offset, int group_log2, int variant, void *out,
+                            int64_t query_offset, int group_log2, int flags, void *out,
                             int64_t *visited, int64_t *path_steps, int64_t *path_count,
                             void *stream);
 

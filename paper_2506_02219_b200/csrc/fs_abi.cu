@@ -128,27 +128,6 @@ int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s) {
 // partial window (a bijection).  One pass, no sort.
 // Windows keep the order slab-local, so the host pipeline can copy, evaluate
 // and return window-aligned slabs independently (same result as one launch).
-__device__ __forceinline__ uint32_t hash32(uint32_t x) {  // lowbias32 finalizer
-  x ^= x >> 16;
-  x *= 0x7feb352du;
-  x ^= x >> 15;
-  x *= 0x846ca68bu;
-  return x ^ (x >> 16);
-}
-
-__device__ __forceinline__ uint32_t feistel4(uint32_t x, int hb, const uint32_t (&ks)[4]) {
-  const uint32_t mask = (1u << hb) - 1u;
-  uint32_t l = x >> hb, r = x & mask;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t f = hash32(ks[i] ^ r) & mask;
-    const uint32_t nl = r;
-    r = l ^ f;
-    l = nl;
-  }
-  return (l << hb) | r;
-}
-
 // blocks of 256 positions never straddle a window (kShuffleWindow % 256 == 0):
 // thread 0 derives the window's round keys once per block
 __global__ void __launch_bounds__(256) k_shuffle(int64_t n, uint64_t h, int64_t qoff,
@@ -176,9 +155,12 @@ __global__ void __launch_bounds__(256) k_shuffle(int64_t n, uint64_t h, int64_t 
   perm[i] = (int32_t)(base + (int64_t)y);
 }
 
+static_assert(kShuffleWindow == kShuffleWindowC, "one shuffle window size");
+static_assert(FSB_FLAG_ALG2 == kFlagAlg2 && FSB_FLAG_SHUFFLED == kFlagShuffled, "flag values");
+
 int shuffle_order(int64_t n, uint64_t seed, int64_t qoff, int32_t* perm, cudaStream_t s) {
   if (n <= 0) return 0;
-  const uint64_t h = key_fold(mix64(seed + kGamma), 0x73687566ull);  // "shuf"
+  const uint64_t h = shuffle_key(seed);
   k_shuffle<<<grid_for(n, 256), 256, 0, s>>>(n, h, qoff, perm);
   FS_CK(cudaGetLastError());
   return 0;
@@ -367,18 +349,22 @@ int fsb_stochastic_batch(fsb_tree* tree, int kid, double alpha, double dfloor, i
 int fsb_stochastic_batch_ex(fsb_tree* tree, int kid, double alpha, double dfloor, int precision,
                             const double* queries, int64_t n, const int32_t* order,
                             int64_t n_samples, int rr_mode, uint64_t seed, int64_t query_offset,
-                            int group_log2, int variant, void* out, int64_t* visited,
+                            int group_log2, int flags, void* out, int64_t* visited,
                             int64_t* path_steps, int64_t* path_count, void* stream) {
   ABI_TREE(tree);
   if (int rc = check_common(kid, precision, n)) return rc;
   if (n_samples < 1 || n_samples > (1LL << 30) || rr_mode < 0 || rr_mode > 2 || group_log2 < 0 ||
-      group_log2 > 20 || variant < 0 || variant > 1) {
-    set_error("bad samples_per_subdomain / rr mode / group size / variant");
+      group_log2 > 20 || flags < 0 || flags > 3) {
+    set_error("bad samples_per_subdomain / rr mode / group size / flags");
+    return 1;
+  }
+  if ((flags & FSB_FLAG_SHUFFLED) && order) {
+    set_error("FSB_FLAG_SHUFFLED computes the order itself: pass order = NULL");
     return 1;
   }
   return fsb::stochastic(tree->t, kid, alpha, dfloor, precision == 0, queries, n, order,
                          (int)n_samples, rr_mode, seed, query_offset, out, visited, path_steps,
-                         path_count, S(stream), group_log2, variant);
+                         path_count, S(stream), group_log2, flags);
 }
 
 int fsb_stochastic_moments_batch(fsb_tree* tree, int kid, double alpha, double dfloor,

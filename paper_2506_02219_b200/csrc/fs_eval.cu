@@ -863,16 +863,24 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
 int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                int64_t query_offset, void* out, int64_t* visited, int64_t* path_steps,
-               int64_t* path_count, cudaStream_t s, int share, int variant) {
+               int64_t* path_count, cudaStream_t s, int share, int flags) {
   if (n <= 0) return 0;
+  const int variant = flags & kFlagAlg2;
+  const bool shuffled = (flags & kFlagShuffled) != 0;  // order = shuffle_order(n, seed, qoff)
   // the fast FP32 kernels implement the reference variant; Alg. 2 runs the
   // generic per-query kernel in either precision
   if (!f64 && variant == 0 && !std::getenv("FSB_DISABLE_FAST")) {
     bool used = false;
     FS_TRY(stochastic_fast(t, kid, alpha, dfloor, q, n, qperm, n_samples, rr_mode, seed,
                            query_offset, share, (float*)out, visited, path_steps, path_count, s,
-                           &used));
+                           &used, shuffled));
     if (used) return 0;
+  }
+  Scratch order;  // the generic kernel reads the shuffled order from memory
+  if (shuffled) {
+    FS_TRY(order.alloc(sizeof(int32_t) * (size_t)n, s));
+    FS_TRY(shuffle_order(n, seed, query_offset, order.as<int32_t>(), s));
+    qperm = order.as<int32_t>();
   }
   FS_TRY(ensure_lo(t, f64, s));
   KParams kp = make_kp(alpha, dfloor);

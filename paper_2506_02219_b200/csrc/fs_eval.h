@@ -22,7 +22,11 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
 int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const double* q,
                int64_t n, const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                int64_t query_offset, void* out, int64_t* visited, int64_t* path_steps,
-               int64_t* path_count, cudaStream_t s, int share = 0, int variant = 0);
+               int64_t* path_count, cudaStream_t s, int share = 0, int flags = 0);
+// flags of stochastic(): the paper's Alg. 2 walk; the evaluation order is
+// shuffle_order(n, seed, query_offset) (qperm must be null; computed in-kernel
+// by the warp-uniform kernel)
+constexpr int kFlagAlg2 = 1, kFlagShuffled = 2;
 int stochastic_moments(FsTree* t, int kid, double alpha, double dfloor, const double* q,
                        int64_t n, int64_t n_reps, int rr_mode, uint64_t seed, double* mean_out,
                        double* var_out, cudaStream_t s);
@@ -31,7 +35,7 @@ int telescoping(FsTree* t, int kid, double alpha, double dfloor, bool f64, const
 int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                     const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                     int64_t qoff, int share, float* out, int64_t* visited, int64_t* path_steps,
-                    int64_t* path_count, cudaStream_t s, bool* used);
+                    int64_t* path_count, cudaStream_t s, bool* used, bool shuffled = false);
 int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                      const int32_t* qperm, double beta, float* out, int64_t* visited,
                      cudaStream_t s, bool* done, bool vote = false);

@@ -82,7 +82,7 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   FS_TRY(stp.alloc(sizeof(int64_t) * (size_t)n, s));
   FS_TRY(cnt.alloc(sizeof(int64_t) * (size_t)n, s));
   const bool shared = a->method == FSB_METHOD_STOCHASTIC && a->rng_group_log2 > 0;
-  if ((a->method == FSB_METHOD_BARNES_HUT && a->query_order) || shared)
+  if (a->method == FSB_METHOD_BARNES_HUT && a->query_order)
     FS_TRY(perm.alloc(sizeof(int32_t) * (size_t)n, s));
 
   Streams& st = streams_for_device();
@@ -158,16 +158,12 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
       case FSB_METHOD_TELESCOPING:
         FS_TRY(telescoping(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, r, v, cs));
         break;
-      default: {
-        int32_t* pp = nullptr;
-        if (shared) {  // the slab's window-local shuffle, keyed on global positions
-          pp = perm.as<int32_t>() + lo;
-          FS_TRY(shuffle_order(m, a->seed, a->query_offset + lo, pp, cs));
-        }
-        FS_TRY(stochastic(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, pp, (int)a->n_samples,
-                          a->rr_mode, a->seed, a->query_offset + lo, r, v, ps, pc, cs,
-                          shared ? a->rng_group_log2 : 0, a->path_variant));
-      }
+      default:
+        // shared streams: the slab's window-local shuffle, keyed on global positions
+        FS_TRY(stochastic(t, a->kid, a->alpha, a->dfloor, !f32, qs, m, nullptr,
+                          (int)a->n_samples, a->rr_mode, a->seed, a->query_offset + lo, r, v, ps,
+                          pc, cs, shared ? a->rng_group_log2 : 0,
+                          (a->path_variant ? kFlagAlg2 : 0) | (shared ? kFlagShuffled : 0)));
     }
     if (!counters) {
       FS_CK(cudaMemsetAsync(ps, 0, sizeof(int64_t) * (size_t)m, cs));

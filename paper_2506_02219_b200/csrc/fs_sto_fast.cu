@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
                const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff, KParams kp,
                unsigned int* __restrict__ chunk_ctr, float* __restrict__ out,
                int64_t* __restrict__ visited, int64_t* __restrict__ path_steps,
-               int64_t* __restrict__ path_count) {
+               int64_t* __restrict__ path_count, int shuffled) {
   // shared layout: 16 B s_cm1[n1] {com, m0}, s_tp1[n1] topology, s_cm2[n2];
   // 8 B s_w1[n1], s_w2[n2] (winding), s_t2[n2] {first child | count << 25, points};
   // 4 B s_b2[n2] begins; 2 B s_lut[n1][kLut + 1]
@@ -817,6 +817,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   __syncthreads();
 
   const uint64_t hseed = mix64(seed + kGamma);
+  const uint64_t shuf_h = shuffle_key(seed);
   const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
   const float2 w0 = make_float2(0.f, 0.f);
   const int nslot = n_int * S;
@@ -834,9 +835,16 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     if (lane == 0) claim = atomicAdd(chunk_ctr, 1u);
     const int64_t t = (int64_t)ch * 32 + lane;
     const bool live = t < n;
+    // shuffled order computed in place (fsb_shuffle_order's permutation): the
+    // 32 positions of a chunk share one window
+    uint32_t wks[4] = {0, 0, 0, 0};
+    if (shuffled) shuffle_window_keys(shuf_h, qoff, t & ~(kShuffleWindowC - 1), wks);
+    auto query_of = [&](int64_t tt) -> int64_t {
+      return shuffled ? shuffled_position(tt, n, wks) : (qperm ? (int64_t)qperm[tt] : tt);
+    };
     float qx = 0.f, qy = 0.f, qz = 0.f;
-    if (live) {  // (the index is reloaded for the stores: fewer live registers)
-      const int64_t qi = qperm ? (int64_t)qperm[t] : t;
+    if (live) {  // (the index is recomputed for the stores: fewer live registers)
+      const int64_t qi = query_of(t);
       qx = (float)q[3 * qi];
       qy = (float)q[3 * qi + 1];
       qz = (float)q[3 * qi + 2];
@@ -1050,7 +1058,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     }
     next = __shfl_sync(0xffffffffu, claim, 0);
     if (live) {
-      const int64_t qi = qperm ? (int64_t)qperm[t] : t;
+      const int64_t qi = query_of(t);
       out[qi] = (float)(acc + (double)(acc_deep * inv_s));
       if (visited) visited[qi] = seen;
       if (path_steps) path_steps[qi] = steps;
@@ -1074,8 +1082,10 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
 int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                     const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                     int64_t qoff, int share, float* out, int64_t* visited, int64_t* path_steps,
-                    int64_t* path_count, cudaStream_t s, bool* used) {
+                    int64_t* path_count, cudaStream_t s, bool* used, bool shuffled) {
   *used = false;
+  // an in-kernel shuffled order is only computed by the warp-uniform kernel
+  if (shuffled && !(share == 5 && (qoff & 31) == 0 && !std::getenv("FSB_STO_WARP_OFF"))) return 0;
   if (t->root_kids <= 0 || t->num_levels > kFastMaxLevels) return 0;
   FS_TRY(ensure_fast(t, s));
   FS_TRY(ensure_lo(t, false, s));  // packed points for multi-point leaves
@@ -1177,7 +1187,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
 #endif
       kern<<<(unsigned)grid, kWarpBlock, wsmem, s>>>(V, q, n, qperm, n_samples, seed, qoff, kp,
                                                      ctr.as<unsigned int>(), out, visited,
-                                                     path_steps, path_count);
+                                                     path_steps, path_count, shuffled ? 1 : 0);
       FS_CK(cudaGetLastError());
 #ifdef FSB_WARP_STATS
       FS_CK(cudaMemcpyFromSymbolAsync(z, g_warp_stats, sizeof(z), 0, cudaMemcpyDeviceToHost, s));

@@ -176,15 +176,13 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
               or _variant(config) != 0):
             # the paper's options (fsb_stochastic_batch_ex): shared streams over a
             # shuffled order (32 consecutive positions per stream), Alg. 2 walk
-            order, group = None, 0
-            if getattr(config, "rng_sharing", "query") == "warp":
-                order, group = dev.empty(n, torch.int32), 5
-                _lib.check(L.fsb_shuffle_order(n, int(config.seed) & ((1 << 64) - 1),
-                                               int(query_offset), _vp(order), _sp()))
+            # (FSB_FLAG_SHUFFLED = 2: fsb_shuffle_order's permutation, computed in-kernel)
+            shared = getattr(config, "rng_sharing", "query") == "warp"
             _lib.check(L.fsb_stochastic_batch_ex(
-                h, kid, alpha, dfloor, prec, _vp(q), n, _vp(order),
+                h, kid, alpha, dfloor, prec, _vp(q), n, None,
                 int(config.samples_per_subdomain), _RR_CODES[config.rr_mode],
-                int(config.seed) & ((1 << 64) - 1), int(query_offset), group, _variant(config),
+                int(config.seed) & ((1 << 64) - 1), int(query_offset), 5 if shared else 0,
+                _variant(config) | (2 if shared else 0),
                 _vp(raw), _vp(visited), _vp(steps), _vp(count), _sp()))
         else:
             _lib.check(L.fsb_stochastic_batch(
