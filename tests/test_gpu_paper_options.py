@@ -210,3 +210,30 @@ def test_alg2_walk_f64_bitwise_vs_oracle(fs, O, case, kind, rr):
         fin = np.isfinite(ref[0])
         close = np.abs(a[fin] - ref[0][fin]) / (1 + np.abs(ref[0][fin])) <= 1e-4
         assert close.mean() >= 0.97, close.mean()
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 33, 65537])
+def test_warp_shared_small_and_ragged_query_counts(fs, O, n):
+    """k_sto_warp with partial chunks and a partial last shuffle window: FP32 values
+    track the FP64 shared-key path, counters agree, every query is written once."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    s = scenes.build_sources(dict(kind="mesh_torus", m=20000, seed=9))
+    kern = fs.KernelSpec("coulomb")
+    q = np.random.default_rng(n).uniform(-0.7, 0.7, (n, 3))
+    qd = dev.to_device(q)
+    t = fs.build_tree(s, 4)
+    r = {}
+    for prec in ("f32", "f64"):
+        cfg = fs.EstimatorConfig("stochastic", seed=5, precision=prec, rng_sharing="warp")
+        r[prec] = evaluate_field_device(cfg, s, kern, qd, t, query_offset=32 * n)
+    a, b = r["f32"].raw.cpu().numpy(), r["f64"].raw.cpu().numpy()
+    assert np.isfinite(a).all() and (a != 0).all()
+    close = np.abs(a - b) / (1 + np.abs(b)) <= 1e-4
+    assert close.mean() >= 0.97
+    same = r["f32"].path_steps.cpu().numpy() == r["f64"].path_steps.cpu().numpy()
+    assert same.mean() >= 0.97
+    ref = [np.zeros(n)] + [np.zeros(n, dtype=np.int64) for _ in range(3)]
+    O.stochastic_ex_batch(*t.core_arrays(), 0, 200.0, 1e-12, q, 1, 0, 5, 0, *ref,
+                          keys=O.shared_keys(n, 5, 32 * n))
+    np.testing.assert_array_equal(b, ref[0])
