@@ -875,6 +875,10 @@ int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
                            query_offset, share, (float*)out, visited, path_steps, path_count, s,
                            &used, shuffled));
     if (used) return 0;
+    if (std::getenv("FSB_REQUIRE_FAST")) {  // tests: a silent fallback is an error
+      set_error("the fast FP32 stochastic kernel declined this tree / launch");
+      return 2;
+    }
   }
   Scratch order;  // the generic kernel reads the shuffled order from memory
   if (shuffled) {

@@ -252,7 +252,7 @@ __device__ __forceinline__ float children_coulomb_pairs(const float4* __restrict
   return ks + ((a2.x + a2.y) + (b2.x + b2.y));
 }
 
-template <int KID, int RR>
+template <int KID, int RR, bool PACK>
 __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     k_sto_fast(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
                const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff, int share,
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   const int o_hist = 2 * (o_t2 + n2);  // walk starts per level-2 node, then their offsets
   const int o_lut = 2 * (o_hist + n2 + (n2 & 1));
   // Coulomb: level-2 records also as packed pairs (16-B units, after the table)
-  constexpr bool kPack = KID == KID_COULOMB && FSB_WARP_DENSE2;
+  constexpr bool kPack = PACK && KID == KID_COULOMB;
   const int o_p2 = (2 * (o_lut + n1 * (kLut + 1)) + 15) / 16;
 #define s_q(i) sh_f4[(i)]
 #define s_cm1(i) sh_f4[o_cm1 + (i)]
@@ -736,7 +736,7 @@ __device__ unsigned long long g_warp_stats[8];
 #define FSB_WARP_MINB 4
 #endif
 
-template <int KID, int RR>
+template <int KID, int RR, bool PACK>
 __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     k_sto_warp(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
                const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff, KParams kp,
@@ -748,8 +748,9 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   // 4 B s_b2[n2] begins; 2 B s_lut[n1][kLut + 1]
   const int n1 = V.n1, n2 = V.n2;
   // Coulomb: level-2 records also as packed pairs {x0,x1,y0,y1}, {z0,z1,-m0,-m1}
-  constexpr bool kPack = KID == KID_COULOMB && FSB_WARP_DENSE2;
-  const int np2 = kPack ? (n2 + 1) / 2 : 0;
+  constexpr bool kPack = KID == KID_COULOMB && FSB_WARP_DENSE2;  // packed walk levels
+  constexpr bool pack = PACK && KID == KID_COULOMB;               // packed dense part
+  const int np2 = pack ? (n2 + 1) / 2 : 0;
   const int o_cm1 = 0, o_tp1 = n1, o_cm2 = 2 * n1, o_p2 = 2 * n1 + n2;
   const int o_w1 = 2 * (2 * n1 + n2 + 2 * np2), o_w2 = o_w1 + (KID == KID_WINDING ? n1 : 0);
   const int o_t2 = o_w2 + (KID == KID_WINDING ? n2 : 0);
@@ -787,7 +788,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     s_b2(i) = b;
     s_t2(i) = make_int2(tp.y > 0 ? (tp.x | (tp.y << 25)) : 0, tp.w - tp.z);
   }
-  if (kPack) stage_coulomb_pairs(V.cm, V.base2, n2, o_p2, tid, kWarpBlock);
+  if (pack) stage_coulomb_pairs(V.cm, V.base2, n2, o_p2, tid, kWarpBlock);
   __syncthreads();
   for (int i = tid; i < n1 * (kLut + 1); i += kWarpBlock) {
     const int a = i / (kLut + 1), b = i - a * (kLut + 1);
@@ -853,7 +854,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
 
     // ---- dense part: every level-2 record (as k_sto_fast) + leaf subdomains
     double acc = 0.0;
-    if (kPack && !l2_multi) {
+    if (pack && !l2_multi) {
       acc = dense_coulomb_pairs(o_p2, np2, qx, qy, qz, kp.dfloor_f);
     } else if (!l2_multi) {
       int k = 0;
@@ -1120,12 +1121,27 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   V.per_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(nslot, FSB_QCAP_MAX / kBlock));
   V.qcap = V.per_chunk * kBlock;
   const size_t n1 = (size_t)V.n1, n2 = (size_t)V.n2;
+  // shared memory: the packed pair table is an option, used when it fits
+  constexpr size_t kSmemMax = 220 * 1024;
+  const bool can_pack = kid == KID_COULOMB && FSB_WARP_DENSE2;
+  const size_t pairs_bytes = 32 * ((n2 + 1) / 2);
   size_t smem = 16 * ((size_t)kBlock + 2 * n1 + n2) + 8 * ((wind ? n1 + n2 : 0) + kBlock) +
                 4 * (2 * n2 + 2 * (size_t)kBlock + 6) + 8 * n2 + 2 * n1 * (kLut + 1);
   smem = (smem + 31) & ~(size_t)15;  // (+ alignment slack for the pair table)
-  if (kid == KID_COULOMB && FSB_WARP_DENSE2) smem += 32 * ((n2 + 1) / 2);
+  const bool pack_fast = can_pack && smem + pairs_bytes <= kSmemMax;
+  if (pack_fast) smem += pairs_bytes;
   if (n2 >= 65535 || (int64_t)nslot * kBlock >= (1ll << 31) || t->n >= (1ll << 25)) return 0;
-  if (smem > 200 * 1024) return 0;
+  // warp-uniform kernel's layout (sample tables after the level-1/2 records)
+  auto warp_smem = [&](bool pk) {
+    return ((16 * (2 * n1 + n2 + (pk ? 2 * ((n2 + 1) / 2) : 0)) +
+             8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 3) + 128) &
+            ~(size_t)127) +
+           (size_t)(kWarpBlock / 32) * 96 * 16;
+  };
+  const bool pack_warp = can_pack && warp_smem(true) <= kSmemMax;
+  const size_t wsmem = warp_smem(pack_warp);
+  const bool warp_path = share == 5 && (qoff & 31) == 0 && !std::getenv("FSB_STO_WARP_OFF");
+  if (warp_path ? wsmem > kSmemMax : smem > kSmemMax) return 0;
   KParams kp;
   kp.alpha = alpha;
   kp.dfloor = dfloor;
@@ -1162,16 +1178,12 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     set_error("unknown rr mode %d", rr_mode);
     return 1;
   }
-  if (share == 5 && (qoff & 31) == 0 && !std::getenv("FSB_STO_WARP_OFF")) {
-    if (kid == KID_COULOMB && FSB_WARP_DENSE2) {  // pair-interleaved records for the walks
+  if (warp_path) {
+    if (can_pack) {  // pair-interleaved records for the walks
       FS_TRY(ensure_pairs(t, s));
       V.cmp = t->lo_cmp;
     }
     // warp-shared streams on warp-aligned groups: the warp-uniform kernel
-    const size_t wsmem =
-        ((16 * (2 * n1 + n2 + (kid == KID_COULOMB && FSB_WARP_DENSE2 ? 2 * ((n2 + 1) / 2) : 0)) +
-          8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 3) + 128) & ~(size_t)127) +
-        (size_t)(kWarpBlock / 32) * 96 * 16;  // + per-warp sample tables
     auto launch_w = [&](auto kern) -> int {
       if (wsmem > 48 * 1024)
         FS_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
@@ -1202,30 +1214,30 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
       return 0;
     };
     switch (kid * 3 + rr_mode) {
-      case 0: rc = launch_w(k_sto_warp<0, 0>); break;
-      case 1: rc = launch_w(k_sto_warp<0, 1>); break;
-      case 2: rc = launch_w(k_sto_warp<0, 2>); break;
-      case 3: rc = launch_w(k_sto_warp<1, 0>); break;
-      case 4: rc = launch_w(k_sto_warp<1, 1>); break;
-      case 5: rc = launch_w(k_sto_warp<1, 2>); break;
-      case 6: rc = launch_w(k_sto_warp<2, 0>); break;
-      case 7: rc = launch_w(k_sto_warp<2, 1>); break;
-      case 8: rc = launch_w(k_sto_warp<2, 2>); break;
+      case 0: rc = pack_warp ? launch_w(k_sto_warp<0, 0, true>) : launch_w(k_sto_warp<0, 0, false>); break;
+      case 1: rc = pack_warp ? launch_w(k_sto_warp<0, 1, true>) : launch_w(k_sto_warp<0, 1, false>); break;
+      case 2: rc = pack_warp ? launch_w(k_sto_warp<0, 2, true>) : launch_w(k_sto_warp<0, 2, false>); break;
+      case 3: rc = launch_w(k_sto_warp<1, 0, false>); break;
+      case 4: rc = launch_w(k_sto_warp<1, 1, false>); break;
+      case 5: rc = launch_w(k_sto_warp<1, 2, false>); break;
+      case 6: rc = launch_w(k_sto_warp<2, 0, false>); break;
+      case 7: rc = launch_w(k_sto_warp<2, 1, false>); break;
+      case 8: rc = launch_w(k_sto_warp<2, 2, false>); break;
       default: set_error("unknown kernel id"); return 1;
     }
     if (rc == 0) *used = true;
     return rc;
   }
   switch (kid * 3 + rr_mode) {
-    case 0: rc = launch(k_sto_fast<0, 0>); break;
-    case 1: rc = launch(k_sto_fast<0, 1>); break;
-    case 2: rc = launch(k_sto_fast<0, 2>); break;
-    case 3: rc = launch(k_sto_fast<1, 0>); break;
-    case 4: rc = launch(k_sto_fast<1, 1>); break;
-    case 5: rc = launch(k_sto_fast<1, 2>); break;
-    case 6: rc = launch(k_sto_fast<2, 0>); break;
-    case 7: rc = launch(k_sto_fast<2, 1>); break;
-    case 8: rc = launch(k_sto_fast<2, 2>); break;
+    case 0: rc = pack_fast ? launch(k_sto_fast<0, 0, true>) : launch(k_sto_fast<0, 0, false>); break;
+    case 1: rc = pack_fast ? launch(k_sto_fast<0, 1, true>) : launch(k_sto_fast<0, 1, false>); break;
+    case 2: rc = pack_fast ? launch(k_sto_fast<0, 2, true>) : launch(k_sto_fast<0, 2, false>); break;
+    case 3: rc = launch(k_sto_fast<1, 0, false>); break;
+    case 4: rc = launch(k_sto_fast<1, 1, false>); break;
+    case 5: rc = launch(k_sto_fast<1, 2, false>); break;
+    case 6: rc = launch(k_sto_fast<2, 0, false>); break;
+    case 7: rc = launch(k_sto_fast<2, 1, false>); break;
+    case 8: rc = launch(k_sto_fast<2, 2, false>); break;
     default: set_error("unknown kernel id"); return 1;
   }
   if (rc == 0) *used = true;

@@ -270,3 +270,31 @@ def test_wide_trees_fall_back_or_run_fast(fs, d):
         close = _rel(a.raw, b.raw) <= 1e-4
         assert close.mean() >= 0.97, (sharing, close.mean())
         assert ((a.path_steps == b.path_steps).mean()) >= 0.97
+
+
+@pytest.mark.parametrize("scene", ["uniform_2e14", "torus_2e18", "winding_2e16", "smooth_2e16"])
+def test_fast_kernels_are_taken(fs, scene, monkeypatch):
+    """FSB_REQUIRE_FAST turns a fallback of the FP32 stochastic path to the generic
+    kernel into an error: the BASELINE-like trees (many level-2 records, as C1's
+    4015) run k_sto_fast / k_sto_warp in both stream modes."""
+    monkeypatch.setenv("FSB_REQUIRE_FAST", "1")
+    if scene == "uniform_2e14":
+        rng = np.random.default_rng(0)
+        s = fs.SourceSet(rng.uniform(-1, 1, (2 ** 14, 3)), np.full(2 ** 14, 1.0 / 2 ** 14))
+        kind = "coulomb"
+    elif scene == "torus_2e18":
+        s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 18, seed=1))
+        kind = "coulomb"
+    elif scene == "winding_2e16":
+        s = scenes.build_sources(dict(kind="mesh_sphere_winding", m=2 ** 16, seed=2, channels=3))
+        kind = "winding_dipole"
+    else:
+        s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 16, seed=3))
+        kind = "smooth_exp"
+    kern = fs.KernelSpec(kind)
+    q = fs.QuerySet(np.random.default_rng(1).uniform(-1, 1, (4096, 3)))
+    t = fs.build_tree(s, 4)
+    for sharing in ("query", "warp"):
+        r = fs.evaluate_field(fs.EstimatorConfig("stochastic", seed=1, precision="f32",
+                                                 rng_sharing=sharing), s, kern, q, tree=t)
+        assert np.isfinite(r.raw).all()
