@@ -262,6 +262,17 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # the headline must run the fast FP32 kernel: a silent fallback is reported
+    os.environ["FSB_REQUIRE_FAST"] = "1"
+    try:
+        step()
+        fast_path = True
+    except Exception as exc:  # pragma: no cover
+        log("WARNING: fast stochastic kernel declined:", exc)
+        fast_path = False
+    finally:
+        del os.environ["FSB_REQUIRE_FAST"]
+    torch.cuda.synchronize()
 
     # ---- launch count of one step (CUPTI via torch.profiler; outside the timed region)
     launches_per_step = None
@@ -332,7 +343,8 @@ def run_ours(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic (reference mesh generators, fixed seeds)",
-           "config": config_block(args.streams), "clocks": clk.summary(), "e2e": e2e}
+           "config": config_block(args.streams), "clocks": clk.summary(), "e2e": e2e,
+           "fast_kernel": fast_path}
     if launches_per_step is not None:
         out["gpu_launches"] = launches_per_step * args.steps
 
