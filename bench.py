@@ -249,6 +249,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     build4_warm_ms = e0.elapsed_time(e1)
 
+    # N > 1: the alternative tree distribution, built on rank 0 and broadcast (NCCL over
+    # NVLink), timed beside the per-rank replica build the step uses
+    tree_dist = None
+    if world > 1:
+        from paper_2506_02219_b200.sharding import broadcast_tree
+        barrier()
+        t0 = time.perf_counter()
+        bt = broadcast_tree(src if rank == 0 else None, 4, src=0)
+        barrier()
+        bcast_ms = (time.perf_counter() - t0) * 1e3
+        del bt
+        tt = torch.tensor([build4_ms, build4_warm_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tree_dist = {"replica_build_ms_max_over_ranks": float(tt[0]),
+                     "replica_build_warm_ms_max_over_ranks": float(tt[1]),
+                     "build_on_rank0_and_broadcast_ms": bcast_ms,
+                     "used": "replica (deterministic per-rank build, no collective)"}
     q_dev = dev.to_device(qs.positions)
     qoff = rank * n  # slab `rank` of a world*n query set: distinct RNG streams per rank
     other = "query" if args.streams == "warp" else "warp"
@@ -345,6 +362,8 @@ def run_ours(args):
            "data": "synthetic (reference mesh generators, fixed seeds)",
            "config": config_block(args.streams), "clocks": clk.summary(), "e2e": e2e,
            "fast_kernel": fast_path}
+    if tree_dist is not None:
+        out["tree_distribution"] = tree_dist
     if launches_per_step is not None:
         out["gpu_launches"] = launches_per_step * args.steps
 

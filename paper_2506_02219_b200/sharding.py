@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["slab", "gather_slabs", "evaluate_field_sharded", "SHUFFLE_WINDOW"]
+__all__ = ["slab", "gather_slabs", "evaluate_field_sharded", "broadcast_tree", "SHUFFLE_WINDOW"]
 
 SHUFFLE_WINDOW = 1 << 16  # positions per window of fsb_shuffle_order (warp-shared mode)
 
@@ -72,3 +72,56 @@ def evaluate_field_sharded(config, sources, kernel, queries, tree=None, group=No
 def _shared(config) -> bool:
     return (getattr(config, "method", "") == "stochastic"
             and getattr(config, "rng_sharing", "query") == "warp")
+
+
+def broadcast_tree(sources, branching_per_dim: int = 2, max_depth: int = 32, src: int = 0,
+                   group=None):
+    """The tree built once on rank `src` and broadcast (NCCL over NVLink with the nccl
+    backend) to every rank -- the alternative to per-rank replica builds.
+
+    Rank `src` builds from `sources` (other ranks may pass None) and exports the ten
+    device core arrays (Octree.core_arrays() minus the unused bbox_min) straight into
+    device buffers; every other rank receives them and assembles its handle with
+    fsb_tree_from_core_arrays (a device-to-device copy; the per-rank packed records are
+    rebuilt lazily from them).  Returns an Octree on every rank; the result is
+    bit-identical to the source rank's tree.
+    """
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from . import _device as dev
+    from . import _lib
+    from .octree import Octree, _DeviceTree, build_tree
+    rank = dist.get_rank(group)
+    device = torch.device("cuda", torch.cuda.current_device())
+    meta = torch.zeros(3, dtype=torch.int64, device=device)
+    tree = None
+    if rank == src:
+        tree = build_tree(sources, branching_per_dim, max_depth)
+        d = tree._device_tree()
+        meta[:] = torch.tensor([d.num_nodes, d.num_points, d.channels], dtype=torch.int64)
+    dist.broadcast(meta, src, group=group)
+    n, m, c = (int(v) for v in meta.cpu())
+    f64, i64 = torch.float64, torch.int64
+    # export order (fsb_tree_export): bbox_min, bbox_max, diameter, aggregate_mass,
+    # aggregate_weight, center_of_mass, child_start, child_count, child_index, begin,
+    # end, depth, permuted_indices, points, masses, weights
+    spec = {2: ((n,), f64), 3: ((n, c), f64), 5: ((n, 3), f64), 6: ((n,), i64), 7: ((n,), i64),
+            8: ((max(n - 1, 1),), i64), 9: ((n,), i64), 10: ((n,), i64), 13: ((m, 3), f64),
+            14: ((m, c), f64)}
+    bufs = {k: torch.empty(shape, dtype=dt, device=device) for k, (shape, dt) in spec.items()}
+    if rank == src:
+        ptrs = (C.c_void_p * 16)(*[dev.ptr(bufs[k]) if k in bufs else None for k in range(16)])
+        _lib.check(_lib.lib().fsb_tree_export(C.c_void_p(tree._device_tree().handle), ptrs,
+                                              C.c_void_p(dev.stream_ptr())))
+    for k in sorted(bufs):
+        dist.broadcast(bufs[k], src, group=group)
+    if rank == src:
+        return tree
+    torch.cuda.synchronize()
+    h = C.c_void_p()
+    order = (2, 3, 5, 6, 7, 8, 9, 10, 13, 14)
+    _lib.check(_lib.lib().fsb_tree_from_core_arrays(
+        *[C.c_void_p(dev.ptr(bufs[k])) for k in order], n, m, c, C.byref(h),
+        C.c_void_p(dev.stream_ptr())))
+    return Octree._from_device(_DeviceTree(h.value), branching_per_dim, max_depth)
