@@ -764,7 +764,6 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
 #define s_t2(i) sh_i2[o_t2 + (i)]
 #define s_b2(i) sh_i[o_b2 + (i)]
 #define s_lut(i) sh_u16[o_lut + (i)]
-#define s_p2(i) sh_f4[o_p2 + (i)]
   const int o_int = o_lut + n1 * (kLut + 1), o_leaf = o_int + n1;  // 2 B subdomain lists
 #define s_int(i) sh_u16[o_int + (i)]
 #define s_leaf(i) sh_u16[o_leaf + (i)]
@@ -1074,7 +1073,6 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
 #undef s_t2
 #undef s_b2
 #undef s_lut
-#undef s_p2
 #undef s_int
 #undef s_leaf
 }
