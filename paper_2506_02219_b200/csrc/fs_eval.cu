@@ -93,8 +93,11 @@ __device__ __forceinline__ double ffr(const typename Prec<F64>::V4& g, double qx
 // accept: skip[i]); a warp processes the union of its lanes' node sequences in
 // increasing preorder index, so every record load is one broadcast transaction
 // while each lane still sees exactly its own sequence (results unchanged).
+#ifndef FSB_BH_MINB
+#define FSB_BH_MINB 1
+#endif
 template <int KID, bool F64, bool VOTE>
-__global__ void __launch_bounds__(128) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
+__global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
                                             const typename Prec<F64>::V4* __restrict__ pa,
                                             const typename Prec<F64>::V4* __restrict__ pb,
                                             uint32_t nn, const double* __restrict__ q, int64_t n,
@@ -226,13 +229,13 @@ struct LoTree {
 };
 
 // _sample_residual, _core.py:159-212 (one path from subdomain a)
-template <int KID, bool F64>
+template <int KID, bool F64, int VARIANT = 0>
 __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int a,
                                                   const int4& tpa, double delta_a,
                                                   uint64_t key_i, uint64_t key_r, int rr_mode,
                                                   double qx, double qy, double qz,
                                                   const KParams& kp, int64_t& steps,
-                                                  int64_t& seen, int variant) {
+                                                  int64_t& seen) {
   int64_t count_a = (int64_t)tpa.w - tpa.z;
   double u0 = uniform_draw(key_i, 0);
   int64_t j = tpa.z + (int64_t)__dmul_rn(u0, (double)count_a);
@@ -241,7 +244,7 @@ __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int
   int4 tp = tpa;
   double prr = 1.0, resid = 0.0;
   uint64_t rctr = 0;
-  if (variant == 1) {
+  if constexpr (VARIANT == 1) {
     // the paper's Alg. 2 (pathSampleEstimator, PAPER.md supplemental): the
     // roulette at T_{I,k} gates the swap at T_{I,k} (the reference commits the
     // swap first); counters: +1 per roulette test, +children per swap
@@ -297,12 +300,15 @@ __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int
 }
 
 // stochastic_batch, _core.py:215-267
-template <int KID, bool F64>
-__global__ void __launch_bounds__(128) k_stochastic(LoTree<KID, F64> T, int root_kids,
+#ifndef FSB_GEN_MINB
+#define FSB_GEN_MINB 12  // 17.9 / 11.8 / 10.7 / 10.6 ms at 1 / 8 / 12 / 16 (C4, FP64)
+#endif
+template <int KID, bool F64, int VARIANT>
+__global__ void __launch_bounds__(128, FSB_GEN_MINB) k_stochastic(LoTree<KID, F64> T, int root_kids,
                                                     const double* __restrict__ q, int64_t n,
                                                     const int32_t* __restrict__ qperm, int S,
                                                     int rr_mode, uint64_t seed, int64_t qoff,
-                                                    int share, int variant, KParams kp,
+                                                    int share, KParams kp,
                                                     typename Prec<F64>::Out* __restrict__ out,
                                                     int64_t* __restrict__ visited,
                                                     int64_t* __restrict__ path_steps,
@@ -336,8 +342,8 @@ __global__ void __launch_bounds__(128) k_stochastic(LoTree<KID, F64> T, int root
       for (int s = 0; s < S; ++s) {
         uint64_t hs = key_fold(ha, (uint64_t)s);
         uint64_t key_i = key_fold(hs, 0), key_r = key_fold(hs, 1);
-        double resid = sample_residual<KID, F64>(T, a, tpa, delta_a, key_i, key_r, rr_mode, qx,
-                                                 qy, qz, kp, steps, seen, variant);
+        double resid = sample_residual<KID, F64, VARIANT>(T, a, tpa, delta_a, key_i, key_r,
+                                                          rr_mode, qx, qy, qz, kp, steps, seen);
         fa = __dadd_rn(fa, resid);
         ++paths;
       }
@@ -392,7 +398,7 @@ __global__ void __launch_bounds__(128) k_moments(LoTree<KID, F64> T, int root_ki
       uint64_t hs = key_fold(key_fold(hq, (uint64_t)a_ord), (uint64_t)r);
       tsum = __dadd_rn(tsum, sample_residual<KID, F64>(T, a, tpa, delta[a_ord], key_fold(hs, 0),
                                                        key_fold(hs, 1), rr_mode, qx, qy, qz, kp,
-                                                       st, se, 0));
+                                                       st, se));
     }
     acc = __dadd_rn(acc, tsum);
     acc2 = __dadd_rn(acc2, __dmul_rn(tsum, tsum));
@@ -891,9 +897,16 @@ int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
   return with_kid(kid, f64, [&](auto K, auto P) {
     constexpr int KID = decltype(K)::value;
     constexpr bool F64 = decltype(P)::value;
-    k_stochastic<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(
-        lo_view<KID, F64>(t), t->root_kids, q, n, qperm, n_samples, rr_mode, seed, query_offset,
-        share, variant, kp, (typename Prec<F64>::Out*)out, visited, path_steps, path_count);
+    auto go = [&](auto kern) {
+      kern<<<grid_for(n, 128), 128, 0, s>>>(lo_view<KID, F64>(t), t->root_kids, q, n, qperm,
+                                           n_samples, rr_mode, seed, query_offset, share, kp,
+                                           (typename Prec<F64>::Out*)out, visited, path_steps,
+                                           path_count);
+    };
+    if (variant)
+      go(k_stochastic<KID, F64, 1>);
+    else
+      go(k_stochastic<KID, F64, 0>);
   });
 }
 
