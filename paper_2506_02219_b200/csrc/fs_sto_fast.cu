@@ -211,6 +211,81 @@ __device__ __forceinline__ void stage_coulomb_pairs(const float4* __restrict__ c
   }
 }
 
+// Winding (dipole) dense part over level-2 records staged as pairs {x0,x1,y0,y1},
+// {z0,z1,m0_0,m0_1}, {m1_0,m1_1,m2_0,m2_1}: (m . (p - q)) r^-3 / (4 pi) on the
+// packed FP32 pipe, the floor as r2 + floor^2 (as the Coulomb form)
+__device__ __forceinline__ double dense_winding_pairs(int o_p2, int np2, float qx, float qy,
+                                                      float qz, float dfloor) {
+  const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy), nz = make_float2(-qz, -qz);
+  const float f2 = dfloor * dfloor;
+  const float2 fl2 = make_float2(f2, f2);
+  auto pair_term = [&](int i, float2 a) {
+    const float4 A = sh_f4[o_p2 + 3 * i], B = sh_f4[o_p2 + 3 * i + 1], M = sh_f4[o_p2 + 3 * i + 2];
+    const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
+    const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
+    const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
+    const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
+    const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+    const float2 ri3 = __fmul2_rn(__fmul2_rn(ri, ri), ri);
+    const float2 dot = __ffma2_rn(make_float2(B.z, B.w), dx,
+                                  __ffma2_rn(make_float2(M.x, M.y), dy,
+                                             __fmul2_rn(make_float2(M.z, M.w), dz)));
+    return __ffma2_rn(dot, ri3, a);
+  };
+  double acc = 0.0;
+  int k = 0;
+  for (; k + kDenseChunk <= np2; k += kDenseChunk) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+#pragma unroll
+    for (int u = 0; u < kDenseChunk; u += 2) {
+      a0 = pair_term(k + u, a0);
+      a1 = pair_term(k + u + 1, a1);
+    }
+    acc += (double)((a0.x + a0.y) + (a1.x + a1.y));
+  }
+  if (k < np2) {
+    float2 a0 = make_float2(0.f, 0.f);
+    for (; k < np2; ++k) a0 = pair_term(k, a0);
+    acc += (double)(a0.x + a0.y);
+  }
+  return acc * kInv4Pi;
+}
+
+__device__ __forceinline__ void stage_winding_pairs(const float4* __restrict__ cm,
+                                                    const float2* __restrict__ m12, int base2,
+                                                    int n2, int o_p2, int tid, int nthreads) {
+  for (int i = tid; i < (n2 + 1) / 2; i += nthreads) {
+    const bool two = 2 * i + 1 < n2;
+    const float4 u = cm[base2 + 2 * i];
+    const float4 v = two ? cm[base2 + 2 * i + 1] : make_float4(u.x, u.y, u.z, 0.f);
+    const float2 wu = m12[base2 + 2 * i];
+    const float2 wv = two ? m12[base2 + 2 * i + 1] : make_float2(0.f, 0.f);
+    sh_f4[o_p2 + 3 * i] = make_float4(u.x, v.x, u.y, v.y);
+    sh_f4[o_p2 + 3 * i + 1] = make_float4(u.z, v.z, u.w, v.w);
+    sh_f4[o_p2 + 3 * i + 2] = make_float4(wu.x, wv.x, wu.y, wv.y);
+  }
+}
+
+// dense part dispatch for the packed kernels (Coulomb: 2, winding: 3 float4 per pair)
+template <int KID>
+__device__ __forceinline__ void stage_pairs(const FastView& V, int n2, int o_p2, int tid,
+                                            int nthreads) {
+  if (KID == KID_WINDING)
+    stage_winding_pairs(V.cm, V.m12, V.base2, n2, o_p2, tid, nthreads);
+  else
+    stage_coulomb_pairs(V.cm, V.base2, n2, o_p2, tid, nthreads);
+}
+template <int KID>
+__device__ __forceinline__ double dense_pairs(int o_p2, int np2, float qx, float qy, float qz,
+                                              float dfloor) {
+  return KID == KID_WINDING ? dense_winding_pairs(o_p2, np2, qx, qy, qz, dfloor)
+                            : dense_coulomb_pairs(o_p2, np2, qx, qy, qz, dfloor);
+}
+template <int KID>
+constexpr int pair_vecs() {
+  return KID == KID_WINDING ? 3 : 2;
+}
+
 // sum of the Coulomb terms of the contiguous children [first, first + count)
 // from the pair-interleaved records (ensure_pairs): one 32-byte load and packed
 // FP32 arithmetic per two children, the floor as r2 + floor^2
@@ -277,7 +352,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
   const int o_hist = 2 * (o_t2 + n2);  // walk starts per level-2 node, then their offsets
   const int o_lut = 2 * (o_hist + n2 + (n2 & 1));
   // Coulomb: level-2 records also as packed pairs (16-B units, after the table)
-  constexpr bool kPack = PACK && KID == KID_COULOMB;
+  constexpr bool kPack = PACK && KID != KID_SMOOTH;
   const int o_p2 = (2 * (o_lut + n1 * (kLut + 1)) + 15) / 16;
 #define s_q(i) sh_f4[(i)]
 #define s_cm1(i) sh_f4[o_cm1 + (i)]
@@ -321,7 +396,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     s_b2(i) = b;
     s_t2(i) = make_int2(tp.y > 0 ? (tp.x | (tp.y << 25)) : 0, tp.w - tp.z);
   }
-  if (kPack && !l2_multi) stage_coulomb_pairs(V.cm, V.base2, n2, o_p2, tid, kBlock);
+  if (kPack && !l2_multi) stage_pairs<KID>(V, n2, o_p2, tid, kBlock);
   if (tid < 4) s_count(tid) = 0;  // [0] queue length, [1] drain head
   s_seen(tid) = 0;
   s_steps(tid) = 0;
@@ -387,7 +462,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
     // sums over 16 records folded into the FP64 accumulator
     double acc = 0.0;
     if (kPack && !l2_multi) {
-      acc = dense_coulomb_pairs(o_p2, (n2 + 1) / 2, qx, qy, qz, kp.dfloor_f);
+      acc = dense_pairs<KID>(o_p2, (n2 + 1) / 2, qx, qy, qz, kp.dfloor_f);
     } else if (!l2_multi) {
       int k = 0;
       for (; k + 16 <= n2; k += 16) {
@@ -749,10 +824,11 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   const int n1 = V.n1, n2 = V.n2;
   // Coulomb: level-2 records also as packed pairs {x0,x1,y0,y1}, {z0,z1,-m0,-m1}
   constexpr bool kPack = KID == KID_COULOMB && FSB_WARP_DENSE2;  // packed walk levels
-  constexpr bool pack = PACK && KID == KID_COULOMB;               // packed dense part
+  constexpr bool pack = PACK && KID != KID_SMOOTH;                // packed dense part
   const int np2 = pack ? (n2 + 1) / 2 : 0;
   const int o_cm1 = 0, o_tp1 = n1, o_cm2 = 2 * n1, o_p2 = 2 * n1 + n2;
-  const int o_w1 = 2 * (2 * n1 + n2 + 2 * np2), o_w2 = o_w1 + (KID == KID_WINDING ? n1 : 0);
+  const int o_w1 = 2 * (2 * n1 + n2 + pair_vecs<KID>() * np2),
+            o_w2 = o_w1 + (KID == KID_WINDING ? n1 : 0);
   const int o_t2 = o_w2 + (KID == KID_WINDING ? n2 : 0);
   const int o_b2 = 2 * (o_t2 + n2);
   const int o_lut = 2 * (o_b2 + n2);
@@ -787,7 +863,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     s_b2(i) = b;
     s_t2(i) = make_int2(tp.y > 0 ? (tp.x | (tp.y << 25)) : 0, tp.w - tp.z);
   }
-  if (pack) stage_coulomb_pairs(V.cm, V.base2, n2, o_p2, tid, kWarpBlock);
+  if (pack) stage_pairs<KID>(V, n2, o_p2, tid, kWarpBlock);
   __syncthreads();
   for (int i = tid; i < n1 * (kLut + 1); i += kWarpBlock) {
     const int a = i / (kLut + 1), b = i - a * (kLut + 1);
@@ -854,7 +930,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     // ---- dense part: every level-2 record (as k_sto_fast) + leaf subdomains
     double acc = 0.0;
     if (pack && !l2_multi) {
-      acc = dense_coulomb_pairs(o_p2, np2, qx, qy, qz, kp.dfloor_f);
+      acc = dense_pairs<KID>(o_p2, np2, qx, qy, qz, kp.dfloor_f);
     } else if (!l2_multi) {
       int k = 0;
       for (; k + 16 <= n2; k += 16) {
@@ -1121,22 +1197,32 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   const size_t n1 = (size_t)V.n1, n2 = (size_t)V.n2;
   // shared memory: the packed pair table is an option, used when it fits
   constexpr size_t kSmemMax = 220 * 1024;
-  const bool can_pack = kid == KID_COULOMB && FSB_WARP_DENSE2;
-  const size_t pairs_bytes = 32 * ((n2 + 1) / 2);
+  const bool can_pack = kid != KID_SMOOTH && FSB_WARP_DENSE2;
+  const size_t pvec = kid == KID_WINDING ? 3 : 2;  // float4 per staged record pair
+  const size_t pairs_bytes = 16 * pvec * ((n2 + 1) / 2);
   size_t smem = 16 * ((size_t)kBlock + 2 * n1 + n2) + 8 * ((wind ? n1 + n2 : 0) + kBlock) +
                 4 * (2 * n2 + 2 * (size_t)kBlock + 6) + 8 * n2 + 2 * n1 * (kLut + 1);
   smem = (smem + 31) & ~(size_t)15;  // (+ alignment slack for the pair table)
-  const bool pack_fast = can_pack && smem + pairs_bytes <= kSmemMax;
+  // resident blocks per SM a shared-memory size allows (228 KB per SM, 1 KB reserved
+  // per block), capped by the register budget: the pair table is used only when it
+  // does not cost occupancy
+  auto fit = [](size_t bytes, int cap) {
+    return std::min<int>(cap, (int)((228 * 1024) / (bytes + 1024)));
+  };
+  // (winding pairs measured slower in the per-query kernel: C2 torus 0.43 -> 0.46 ms)
+  const bool pack_fast = can_pack && kid == KID_COULOMB && smem + pairs_bytes <= kSmemMax &&
+                         fit(smem + pairs_bytes, FSB_STO_MINB) >= fit(smem, FSB_STO_MINB);
   if (pack_fast) smem += pairs_bytes;
   if (n2 >= 65535 || (int64_t)nslot * kBlock >= (1ll << 31) || t->n >= (1ll << 25)) return 0;
   // warp-uniform kernel's layout (sample tables after the level-1/2 records)
   auto warp_smem = [&](bool pk) {
-    return ((16 * (2 * n1 + n2 + (pk ? 2 * ((n2 + 1) / 2) : 0)) +
+    return ((16 * (2 * n1 + n2 + (pk ? pvec * ((n2 + 1) / 2) : 0)) +
              8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 3) + 128) &
             ~(size_t)127) +
            (size_t)(kWarpBlock / 32) * 96 * 16;
   };
-  const bool pack_warp = can_pack && warp_smem(true) <= kSmemMax;
+  const bool pack_warp = can_pack && warp_smem(true) <= kSmemMax &&
+                         fit(warp_smem(true), FSB_WARP_MINB) >= fit(warp_smem(false), FSB_WARP_MINB);
   const size_t wsmem = warp_smem(pack_warp);
   const bool warp_path = share == 5 && (qoff & 31) == 0 && !std::getenv("FSB_STO_WARP_OFF");
   if (warp_path ? wsmem > kSmemMax : smem > kSmemMax) return 0;
@@ -1177,7 +1263,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     return 1;
   }
   if (warp_path) {
-    if (can_pack) {  // pair-interleaved records for the walks
+    if (kid == KID_COULOMB && FSB_WARP_DENSE2) {  // pair-interleaved records for the walks
       FS_TRY(ensure_pairs(t, s));
       V.cmp = t->lo_cmp;
     }
@@ -1215,9 +1301,9 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
       case 0: rc = pack_warp ? launch_w(k_sto_warp<0, 0, true>) : launch_w(k_sto_warp<0, 0, false>); break;
       case 1: rc = pack_warp ? launch_w(k_sto_warp<0, 1, true>) : launch_w(k_sto_warp<0, 1, false>); break;
       case 2: rc = pack_warp ? launch_w(k_sto_warp<0, 2, true>) : launch_w(k_sto_warp<0, 2, false>); break;
-      case 3: rc = launch_w(k_sto_warp<1, 0, false>); break;
-      case 4: rc = launch_w(k_sto_warp<1, 1, false>); break;
-      case 5: rc = launch_w(k_sto_warp<1, 2, false>); break;
+      case 3: rc = pack_warp ? launch_w(k_sto_warp<1, 0, true>) : launch_w(k_sto_warp<1, 0, false>); break;
+      case 4: rc = pack_warp ? launch_w(k_sto_warp<1, 1, true>) : launch_w(k_sto_warp<1, 1, false>); break;
+      case 5: rc = pack_warp ? launch_w(k_sto_warp<1, 2, true>) : launch_w(k_sto_warp<1, 2, false>); break;
       case 6: rc = launch_w(k_sto_warp<2, 0, false>); break;
       case 7: rc = launch_w(k_sto_warp<2, 1, false>); break;
       case 8: rc = launch_w(k_sto_warp<2, 2, false>); break;
