@@ -114,7 +114,10 @@ constexpr int kOwnerBits = kBlock <= 256 ? 8 : (kBlock <= 512 ? 9 : 10);
 // and uint2 {kr.lo, kr.hi} (roulette stream key).  Everything else a walk needs
 // at level 2 (p_rr, ratio, control-variate term) is recomputed from the staged
 // level-1/2 records in shared memory.
-constexpr size_t kWalkBytes = 24;
+#ifndef FSB_KR_RECOMPUTE
+#define FSB_KR_RECOMPUTE 1  // rederive the roulette key in the drain (16-byte walk starts)
+#endif
+constexpr size_t kWalkBytes = FSB_KR_RECOMPUTE ? 16 : 24;
 
 extern __shared__ float4 sh_f4[];
 extern __shared__ int4 sh_i4[];
@@ -371,8 +374,8 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 
   // two walk-start buffers: creation order (qa, qk) and sorted by level-2 node (sa, sk)
   int4* const qa = reinterpret_cast<int4*>(queues + (size_t)blockIdx.x * 2 * V.qcap * kWalkBytes);
-  uint2* const qk = reinterpret_cast<uint2*>(qa + V.qcap);
-  int4* const sa = reinterpret_cast<int4*>(qk + V.qcap);
+  uint2* const qk = reinterpret_cast<uint2*>(qa + V.qcap);  // (unused with FSB_KR_RECOMPUTE)
+  int4* const sa = FSB_KR_RECOMPUTE ? qa + V.qcap : reinterpret_cast<int4*>(qk + V.qcap);
   uint2* const sk = reinterpret_cast<uint2*>(sa + V.qcap);
   const int tid = threadIdx.x;
   const int nslot = n1 * S;
@@ -523,8 +526,12 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
       if (survive<RR>(p, kr, 0)) {  // descends: queue the walk start
         const int pos = atomicAdd(&s_count(0), 1);
         atomicAdd(&s_hist(lo), 1);
+#if FSB_KR_RECOMPUTE
+        qa[pos] = make_int4(tid | (steps << kOwnerBits), a_ord | (sm << 8), lo, j);
+#else
         qa[pos] = make_int4(tid | (steps << kOwnerBits), a_ord, lo, j);
         qk[pos] = make_uint2((uint32_t)kr, (uint32_t)(kr >> 32));
+#endif
         ++steps;
       }
     };
@@ -598,10 +605,9 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
         __syncthreads();
         for (int i = tid; i < cnt; i += kBlock) {
           const int4 wa = qa[i];
-          const uint2 wk = qk[i];
           const int pos = atomicAdd(&s_hist(wa.z), 1);
           sa[pos] = wa;
-          sk[pos] = wk;
+          if (!FSB_KR_RECOMPUTE) sk[pos] = qk[i];
         }
         __syncthreads();
         for (int b = tid; b < n2; b += kBlock) s_hist(b) = 0;
@@ -629,13 +635,21 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
             const int idx = head + __popc(need & ((1u << lane) - 1u));
             if (!act && idx < cnt) {
               const int4 wa = sa[idx];  // consecutive lanes, consecutive records
-              const uint2 wk = sk[idx];
               owner = wa.x & ((1 << kOwnerBits) - 1);
-              const int wa_ord = wa.y, k = wa.z;
+              const int wa_ord = FSB_KR_RECOMPUTE ? (wa.y & 0xff) : wa.y, k = wa.z;
               slot = wa.x >> kOwnerBits;  // creation index among the owner's walks
               jj = wa.w;
               path = V.path[jj];
+#if FSB_KR_RECOMPUTE
+              {  // the roulette stream key of (owner query, a, s), as in the sampling
+                const uint2 hv = s_hq(owner);
+                const uint64_t hq_o = ((uint64_t)hv.y << 32) | hv.x;
+                kr = key_fold(key_fold(key_fold(hq_o, (uint64_t)wa_ord), (uint64_t)(wa.y >> 8)), 1);
+              }
+#else
+              const uint2 wk = sk[idx];
               kr = ((uint64_t)wk.y << 32) | wk.x;
+#endif
               qq = s_q(owner);
               const int4 tpa = s_tp1(wa_ord);
               count_a = tpa.w - tpa.z;
