@@ -27,6 +27,13 @@
 //    creation-ordered slot and owners fold their slots in that ((a, s))
 //    order, so a query's value never depends on which lane served its walks.
 //  * FP32 terms and residuals, FP64 accumulation across chunks/subdomains.
+//
+// k_sto_warp (further down) is the same estimator with the paper's warp-shared
+// RNG streams: 32 queries of a seeded shuffled order share
+// the draws, so sampling is done once per warp and every walk is warp-uniform
+// (broadcast child loads, no queue / sort / result slots).  The Coulomb (and
+// winding) dense parts of both kernels run on the packed FP32 pipe
+// (FADD2/FFMA2, dense_coulomb_pairs / dense_winding_pairs).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
