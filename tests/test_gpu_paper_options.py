@@ -237,3 +237,28 @@ def test_warp_shared_small_and_ragged_query_counts(fs, O, n):
     O.stochastic_ex_batch(*t.core_arrays(), 0, 200.0, 1e-12, q, 1, 0, 5, 0, *ref,
                           keys=O.shared_keys(n, 5, 32 * n))
     np.testing.assert_array_equal(b, ref[0])
+
+
+def test_ex_entry_validates_flags(fs):
+    """fsb_stochastic_batch_ex: unknown flags, or FSB_FLAG_SHUFFLED with an explicit
+    order, are argument errors (status 1, ValueError in Python)."""
+    import ctypes as C
+    import torch
+    from paper_2506_02219_b200 import _device as dev, _lib
+    s = scenes.build_sources(dict(kind="mesh_torus", m=5000, seed=1))
+    t = fs.build_tree(s, 4)
+    h = C.c_void_p(t._device_tree().handle)
+    q = dev.to_device(np.zeros((64, 3)))
+    out = dev.empty(64, torch.float32)
+    order = dev.empty(64, torch.int32)
+    L = _lib.lib()
+    sp = C.c_void_p(dev.stream_ptr())
+
+    def call(order_ptr, flags):
+        return L.fsb_stochastic_batch_ex(h, 0, 200.0, 1e-12, 1, C.c_void_p(dev.ptr(q)), 64,
+                                         order_ptr, 1, 0, 1, 0, 5, flags,
+                                         C.c_void_p(dev.ptr(out)), None, None, None, sp)
+
+    assert call(None, 4) == 1 and b"flags" in L.fsb_last_error()
+    assert call(C.c_void_p(dev.ptr(order)), 2) == 1 and b"order = NULL" in L.fsb_last_error()
+    assert call(None, 2) == 0 and call(None, 3) == 0
