@@ -124,6 +124,21 @@ def test_types_validation_mirrors_reference():
     assert out.min() >= -1 and out.max() <= 1 and scale == 1 / 3
 
 
+def test_paper_option_fields_default_to_the_reference():
+    """The paper's options are opt-in extensions: defaults reproduce the reference,
+    and bad values are rejected like the reference's own config fields."""
+    from paper_2506_02219_b200.estimators import _variant
+    c = fs.EstimatorConfig("stochastic")
+    assert (c.rng_sharing, c.bh_warp_vote, c.path_order) == ("query", False,
+                                                             "swap_then_roulette")
+    assert _variant(c) == 0
+    assert _variant(fs.EstimatorConfig("stochastic", path_order="roulette_then_swap")) == 1
+    with pytest.raises(ValueError):
+        fs.EstimatorConfig("stochastic", rng_sharing="block")
+    with pytest.raises(ValueError):
+        fs.EstimatorConfig("stochastic", path_order="random")
+
+
 # ---------------------------------------------------------------- kernels
 def test_kernel_hand_values():
     coul, wind, sm3 = (fs.KernelSpec("coulomb"), fs.KernelSpec("winding_dipole"),
