@@ -820,7 +820,10 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 //    lane keeps its own roulette state (p depends on the query) and stops
 //    committing once its roulette fails; the walk ends when no lane is alive.
 //    No queue, no sort, no result slots: residuals accumulate in (a, s) order.
-constexpr int kWarpBlock = 256;
+#ifndef FSB_WARP_BLOCK
+#define FSB_WARP_BLOCK 256  // 512 / 1024: 1-1.5 % faster on C4 but fewer blocks for small launches
+#endif
+constexpr int kWarpBlock = FSB_WARP_BLOCK;
 #ifdef FSB_WARP_STATS
 __device__ unsigned long long g_warp_stats[8];
 #define WSTAT(i, v) \
