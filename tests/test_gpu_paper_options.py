@@ -262,3 +262,22 @@ def test_ex_entry_validates_flags(fs):
     assert call(None, 4) == 1 and b"flags" in L.fsb_last_error()
     assert call(C.c_void_p(dev.ptr(order)), 2) == 1 and b"order = NULL" in L.fsb_last_error()
     assert call(None, 2) == 0 and call(None, 3) == 0
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_alg2_host_pipeline_equals_device_path(fs, prec):
+    """path_order="roulette_then_swap" through evaluate_field (pipelined slabs, with and
+    without shared streams) gives the device path's values and counters bit for bit."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200 import _device as dev
+    s = scenes.build_sources(dict(kind="mesh_torus", m=20000, seed=5))
+    kern = fs.KernelSpec("coulomb")
+    q = np.random.default_rng(6).uniform(-0.6, 0.6, (2 * (1 << 16) + 300, 3))
+    t = fs.build_tree(s, 4)
+    for sharing in ("query", "warp"):
+        cfg = fs.EstimatorConfig("stochastic", seed=8, precision=prec, rng_sharing=sharing,
+                                 path_order="roulette_then_swap")
+        ref = evaluate_field_device(cfg, s, kern, dev.to_device(q), t).to_host()
+        r = fs.evaluate_field(cfg, s, kern, fs.QuerySet(q), tree=t, chunks=3)
+        np.testing.assert_array_equal(r.raw, ref.raw)
+        np.testing.assert_array_equal(r.path_steps, ref.path_steps)
