@@ -194,6 +194,9 @@ struct LoTree {
   const int4* __restrict__ topo;
   const V4* __restrict__ pa;
   const V4* __restrict__ pb;
+  // per point: sibling rank per level (ensure_path; null: binary search over begins)
+  const uint64_t* __restrict__ path;
+  int path_bits, path_levels;
 
   __device__ __forceinline__ double agg_term(int r, double qx, double qy, double qz,
                                              const KParams& kp) const {
@@ -226,6 +229,14 @@ struct LoTree {
     }
     return tp.x + lo;
   }
+  // child of the level-`lvl` node `tp` holding point j: from the point's path of
+  // sibling ranks when available (one load per walk instead of a search per level)
+  __device__ __forceinline__ int pick_child(const int4& tp, int64_t j, uint64_t pj,
+                                            int lvl) const {
+    if (path && lvl < path_levels)
+      return tp.x + (int)((pj >> (path_bits * lvl)) & ((1ull << path_bits) - 1ull));
+    return child_of(tp, j);
+  }
 };
 
 // _sample_residual, _core.py:159-212 (one path from subdomain a)
@@ -244,12 +255,14 @@ __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int
   int4 tp = tpa;
   double prr = 1.0, resid = 0.0;
   uint64_t rctr = 0;
+  const uint64_t pj = T.path ? T.path[j] : 0;
+  int lvl = 1;  // subdomains are the root's children
   if constexpr (VARIANT == 1) {
     // the paper's Alg. 2 (pathSampleEstimator, PAPER.md supplemental): the
     // roulette at T_{I,k} gates the swap at T_{I,k} (the reference commits the
     // swap first); counters: +1 per roulette test, +children per swap
     while (tp.y > 0) {
-      int child = T.child_of(tp, j);
+      int child = T.pick_child(tp, j, pj, lvl);
       double rp = ffr<F64>(T.geo[node], qx, qy, qz);
       double rc = ffr<F64>(T.geo[child], qx, qy, qz);
       double p = rr_probability(rp, rc, rr_mode);
@@ -270,11 +283,12 @@ __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int
       node = child;
       tp = T.topo[node];
       ++steps;
+      ++lvl;
     }
     return resid;
   }
   while (tp.y > 0) {
-    int child = T.child_of(tp, j);
+    int child = T.pick_child(tp, j, pj, lvl);
     double delta;
     if (node == a)
       delta = delta_a;
@@ -295,6 +309,7 @@ __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int
     node = child;
     tp = T.topo[node];
     ++steps;
+    ++lvl;
   }
   return resid;
 }
@@ -816,6 +831,9 @@ static LoTree<KID, F64> lo_view(const FsTree* t) {
     T.pb = t->pts32b;
   }
   T.topo = t->lo_topo;
+  T.path = t->pt_path;
+  T.path_bits = t->path_bits;
+  T.path_levels = t->path_levels;
   return T;
 }
 
@@ -893,6 +911,7 @@ int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
     qperm = order.as<int32_t>();
   }
   FS_TRY(ensure_lo(t, f64, s));
+  FS_TRY(ensure_path(t, s));
   KParams kp = make_kp(alpha, dfloor);
   return with_kid(kid, f64, [&](auto K, auto P) {
     constexpr int KID = decltype(K)::value;
@@ -915,6 +934,7 @@ int stochastic_moments(FsTree* t, int kid, double alpha, double dfloor, const do
                        double* var_out, cudaStream_t s) {
   if (n <= 0) return 0;
   FS_TRY(ensure_lo(t, true, s));
+  FS_TRY(ensure_path(t, s));
   KParams kp = make_kp(alpha, dfloor);
   Scratch work;
   FS_TRY(work.alloc(sizeof(double) * n * std::max(1, t->root_kids), s));
