@@ -153,7 +153,7 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
         visited.fill_(len(sources))
     else:
         if tree is None:
-            tree = build_tree(sources, config.resolved_branching, config.max_depth)
+            tree = _tree_for(sources, config.resolved_branching, config.max_depth)
         elif tree.branching_per_dim != config.resolved_branching:
             raise ValueError("prebuilt tree branching factor does not match config")
         h = C.c_void_p(tree._device_tree().handle)
@@ -198,6 +198,30 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
                                     _vp(raw64), _vp(flagged), _sp()))
     return DeviceField(values=values, raw=raw64, flagged=flagged, visited=visited,
                        path_steps=steps, path_count=count, method=config.method)
+
+
+_TREE_CACHE: dict = {}  # the last tree built for an immutable SourceSet
+
+
+def _tree_for(sources: SourceSet, branching: int, max_depth: int):
+    """build_tree for calls without a prebuilt tree, reusing the device tree of the
+    most recent SourceSet (immutable, so the tree is the same bits): repeated
+    evaluate_field calls on one scene pay the build once.  Only the latest
+    SourceSet is kept (weakly): its tree is freed with it or when another scene
+    is evaluated."""
+    import weakref
+    key = (branching, max_depth)
+    ref = _TREE_CACHE.get("src")
+    if ref is not None and ref() is sources and key in _TREE_CACHE["trees"]:
+        return _TREE_CACHE["trees"][key]
+    if ref is None or ref() is not sources:
+        _TREE_CACHE.clear()
+        _TREE_CACHE["src"] = weakref.ref(
+            sources, lambda r: _TREE_CACHE.clear() if _TREE_CACHE.get("src") is r else None)
+        _TREE_CACHE["trees"] = {}
+    tree = build_tree(sources, branching, max_depth)
+    _TREE_CACHE["trees"][key] = tree
+    return tree
 
 
 def _variant(config) -> int:
@@ -278,7 +302,7 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
         args.m, args.c = len(sources), sources.channel_count
     else:
         if tree is None:
-            tree = build_tree(sources, config.resolved_branching, config.max_depth)
+            tree = _tree_for(sources, config.resolved_branching, config.max_depth)
         elif tree.branching_per_dim != config.resolved_branching:
             raise ValueError("prebuilt tree branching factor does not match config")
         h = C.c_void_p(tree._device_tree().handle)

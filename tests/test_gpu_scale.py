@@ -230,3 +230,32 @@ def test_paper_warp_shared_rng_is_unbiased_and_deterministic(fs, prec):
     e_warp = np.median([np.median(np.abs(r - truth)) for r in runs[:16]])
     e_ref = np.median([np.median(np.abs(run(k, "query") - truth)) for k in range(16)])
     assert abs(e_warp - e_ref) <= 0.1 * e_ref
+
+
+def test_tree_reused_for_repeated_calls_on_one_scene(fs, monkeypatch):
+    """evaluate_field without a prebuilt tree builds once per (SourceSet, branching)
+    and reuses it; a new SourceSet gets its own tree; results are unchanged."""
+    from paper_2506_02219_b200 import estimators as E
+    calls = []
+    real = E.build_tree
+
+    def counting(*a, **k):
+        calls.append(1)
+        return real(*a, **k)
+
+    monkeypatch.setattr(E, "build_tree", counting)
+    s = scenes.build_sources(dict(kind="mesh_torus", m=5000, seed=2))
+    q = fs.QuerySet(np.random.default_rng(0).uniform(-0.5, 0.5, (300, 3)))
+    kern = fs.KernelSpec("coulomb")
+    cfg = fs.EstimatorConfig("stochastic", seed=1)
+    a = fs.evaluate_field(cfg, s, kern, q)
+    b = fs.evaluate_field(cfg, s, kern, q)
+    assert len(calls) == 1
+    np.testing.assert_array_equal(a.raw, b.raw)
+    fs.evaluate_field(fs.EstimatorConfig("barnes_hut"), s, kern, q)  # d = 2: another tree
+    assert len(calls) == 2
+    s2 = scenes.build_sources(dict(kind="mesh_torus", m=5000, seed=3))
+    fs.evaluate_field(cfg, s2, kern, q)
+    assert len(calls) == 3
+    ref = fs.evaluate_field(cfg, s, kern, q, tree=fs.build_tree(s, 4))
+    np.testing.assert_array_equal(a.raw, ref.raw)
