@@ -178,17 +178,24 @@ __global__ void k_pack_bh(const double* __restrict__ com, const double* __restri
 }
 
 int ensure_bh(FsTree* t, bool f64, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lk(t->mu);
   const int B = 256;
   if (f64 && !t->bh64) {
-    FS_TRY(dalloc(&t->bh64, t->n, s));
+    BhRec64* rec = nullptr;
+    FS_TRY(dalloc(&rec, t->n, s));
     k_pack_bh<double, double4><<<grid_for(t->n, B), B, 0, s>>>(
         t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->skip, t->n, t->c,
-        reinterpret_cast<double4*>(t->bh64), nullptr);
+        reinterpret_cast<double4*>(rec), nullptr);
+    FS_CK(cudaStreamSynchronize(s));
+    t->bh64 = rec;
   } else if (!f64 && !t->bh32) {
-    FS_TRY(dalloc(&t->bh32, t->n, s));
+    BhRec32* rec = nullptr;
+    FS_TRY(dalloc(&rec, t->n, s));
     k_pack_bh<float, float4><<<grid_for(t->n, B), B, 0, s>>>(
         t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->skip, t->n, t->c,
-        reinterpret_cast<float4*>(t->bh32), nullptr);
+        reinterpret_cast<float4*>(rec), nullptr);
+    FS_CK(cudaStreamSynchronize(s));
+    t->bh32 = rec;
   }
   FS_CK(cudaGetLastError());
   return 0;
@@ -238,29 +245,46 @@ __global__ void k_pack_pts(const double* __restrict__ pts, const double* __restr
 }
 
 int ensure_lo(FsTree* t, bool f64, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lk(t->mu);
   const int B = 256;
-  if (!t->lo_topo) FS_TRY(dalloc(&t->lo_topo, t->n, s));
-  if (f64 && !t->lo_geo64) {
-    FS_TRY(dalloc(&t->lo_geo64, t->n, s));
-    FS_TRY(dalloc(&t->lo_mass64, t->n, s));
-    FS_TRY(dalloc(&t->pts64a, t->m, s));
-    FS_TRY(dalloc(&t->pts64b, t->m, s));
+  if ((f64 && t->lo_geo64) || (!f64 && t->lo_geo32)) return 0;
+  // the topology is shared by both precisions: packed by the first call only
+  int4* topo = nullptr;
+  if (!t->lo_topo) FS_TRY(dalloc(&topo, t->n, s));
+  if (f64) {
+    double4 *geo = nullptr, *mass = nullptr, *pa = nullptr, *pb = nullptr;
+    FS_TRY(dalloc(&geo, t->n, s));
+    FS_TRY(dalloc(&mass, t->n, s));
+    FS_TRY(dalloc(&pa, t->m, s));
+    FS_TRY(dalloc(&pb, t->m, s));
     k_pack_lo<double, double4><<<grid_for(t->n, B), B, 0, s>>>(
         t->lo2pre, t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->fc_lo,
-        t->n, t->c, t->lo_geo64, t->lo_mass64, t->lo_topo);
+        t->n, t->c, geo, mass, topo);
     k_pack_pts<double, double4><<<grid_for(t->m, B), B, 0, s>>>(t->points, t->masses, t->m, t->c,
-                                                                t->pts64a, t->pts64b);
-  } else if (!f64 && !t->lo_geo32) {
-    FS_TRY(dalloc(&t->lo_geo32, t->n, s));
-    FS_TRY(dalloc(&t->lo_mass32, t->n, s));
-    FS_TRY(dalloc(&t->pts32a, t->m, s));
-    FS_TRY(dalloc(&t->pts32b, t->m, s));
+                                                                pa, pb);
+    FS_CK(cudaStreamSynchronize(s));
+    t->lo_geo64 = geo;
+    t->lo_mass64 = mass;
+    t->pts64a = pa;
+    t->pts64b = pb;
+  } else {
+    float4 *geo = nullptr, *mass = nullptr, *pa = nullptr, *pb = nullptr;
+    FS_TRY(dalloc(&geo, t->n, s));
+    FS_TRY(dalloc(&mass, t->n, s));
+    FS_TRY(dalloc(&pa, t->m, s));
+    FS_TRY(dalloc(&pb, t->m, s));
     k_pack_lo<float, float4><<<grid_for(t->n, B), B, 0, s>>>(
         t->lo2pre, t->com, t->diameter, t->agg_mass, t->child_count, t->begin, t->end, t->fc_lo,
-        t->n, t->c, t->lo_geo32, t->lo_mass32, t->lo_topo);
+        t->n, t->c, geo, mass, topo);
     k_pack_pts<float, float4><<<grid_for(t->m, B), B, 0, s>>>(t->points, t->masses, t->m, t->c,
-                                                              t->pts32a, t->pts32b);
+                                                              pa, pb);
+    FS_CK(cudaStreamSynchronize(s));
+    t->lo_geo32 = geo;
+    t->lo_mass32 = mass;
+    t->pts32a = pa;
+    t->pts32b = pb;
   }
+  if (topo) t->lo_topo = topo;
   FS_CK(cudaGetLastError());
   return 0;
 }
@@ -323,6 +347,7 @@ __global__ void k_max_children(const int4* __restrict__ topo, int64_t n, int* __
 }
 
 int ensure_path(FsTree* t, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lk(t->mu);
   if (t->pt_path) return 0;
   FS_TRY(ensure_lo(t, false, s));
   Scratch mx;
@@ -334,13 +359,15 @@ int ensure_path(FsTree* t, cudaStream_t s) {
   FS_CK(cudaStreamSynchronize(s));
   int bits = 1;
   while ((1ll << bits) < kids) ++bits;
-  FS_TRY(dalloc(&t->pt_path, t->m, s));
+  uint64_t* path = nullptr;
+  FS_TRY(dalloc(&path, t->m, s));
+  const int levels = bits <= 16 ? 64 / bits : 0;
+  k_point_path<<<grid_for(t->m, 256), 256, 0, s>>>(t->lo_topo, t->m, bits, levels, path);
+  FS_CK(cudaStreamSynchronize(s));
   t->path_bits = bits;
-  t->path_levels = bits <= 16 ? 64 / bits : 0;
+  t->path_levels = levels;
   t->max_children = kids;
-  k_point_path<<<grid_for(t->m, 256), 256, 0, s>>>(t->lo_topo, t->m, bits, t->path_levels,
-                                                   t->pt_path);
-
+  t->pt_path = path;
   FS_CK(cudaGetLastError());
   return 0;
 }
@@ -355,11 +382,15 @@ __global__ void k_pack_pairs(const float4* __restrict__ cm, int64_t n, float4* _
 }
 
 int ensure_pairs(FsTree* t, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lk(t->mu);
   if (t->lo_cmp) return 0;
   FS_TRY(ensure_fast(t, s));
   const int64_t np = (t->n + 1) / 2;
-  FS_TRY(dalloc(&t->lo_cmp, 2 * np, s));
-  k_pack_pairs<<<grid_for(np, 256), 256, 0, s>>>(t->lo_cm32, t->n, t->lo_cmp);
+  float4* pairs = nullptr;
+  FS_TRY(dalloc(&pairs, 2 * np, s));
+  k_pack_pairs<<<grid_for(np, 256), 256, 0, s>>>(t->lo_cm32, t->n, pairs);
+  FS_CK(cudaStreamSynchronize(s));
+  t->lo_cmp = pairs;
   FS_CK(cudaGetLastError());
   return 0;
 }
@@ -372,11 +403,13 @@ __global__ void k_level_diam(const int64_t* __restrict__ start, int nl,
 }
 
 int ensure_fast(FsTree* t, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lk(t->mu);
   if (t->fast_ready) return 0;
   const int B = 256;
-  FS_TRY(dalloc(&t->lo_cm32, t->n, s));
-  FS_TRY(dalloc(&t->lo_begin, t->n, s));
-  if (t->c >= 3) FS_TRY(dalloc(&t->lo_m12_32, t->n, s));
+  // (an earlier call that failed half-way may have left buffers behind)
+  if (!t->lo_cm32) FS_TRY(dalloc(&t->lo_cm32, t->n, s));
+  if (!t->lo_begin) FS_TRY(dalloc(&t->lo_begin, t->n, s));
+  if (t->c >= 3 && !t->lo_m12_32) FS_TRY(dalloc(&t->lo_m12_32, t->n, s));
   k_pack_fast<<<grid_for(t->n, B), B, 0, s>>>(t->lo2pre, t->com, t->agg_mass, t->begin, t->n, t->c,
                                               t->lo_cm32, t->c >= 3 ? t->lo_m12_32 : nullptr,
                                               t->lo_begin);

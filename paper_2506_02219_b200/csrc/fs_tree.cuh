@@ -6,6 +6,7 @@
 //   * level order (children contiguous): geo + mass + topo (int4) per node
 #pragma once
 #include <atomic>
+#include <mutex>
 #include <cstdint>
 #include <vector>
 #include <cuda_runtime.h>
@@ -47,6 +48,10 @@ struct FsTree {
   float4 *pts32a = nullptr, *pts32b = nullptr;  // permuted points {x,y,z,m0}, {m1,m2,0,0}
   double4 *pts64a = nullptr, *pts64b = nullptr;
   int root_kids = 0;  // child_count[0]
+  // Guards the lazily packed records below (ensure_*): a record pointer is
+  // published only after its pack kernels have completed, so a launch on any
+  // stream or host thread that obtained it through ensure_* reads finished data.
+  std::recursive_mutex mu;
   std::atomic<int> bh_items_hint{0};  // load-balanced BH: items emitted by the last call
 
   // fast FP32 stochastic / BH path (built by ensure_fast)

@@ -14,7 +14,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 import sys
-import time
+import threading
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -200,28 +201,31 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
                        path_steps=steps, path_count=count, method=config.method)
 
 
-_TREE_CACHE: dict = {}  # the last tree built for an immutable SourceSet
+_TREE_CACHE: dict = {}  # the last trees built for an immutable SourceSet, per device
+_TREE_LOCK = threading.Lock()
 
 
 def _tree_for(sources: SourceSet, branching: int, max_depth: int):
     """build_tree for calls without a prebuilt tree, reusing the device tree of the
-    most recent SourceSet (immutable, so the tree is the same bits): repeated
-    evaluate_field calls on one scene pay the build once.  Only the latest
-    SourceSet is kept (weakly): its tree is freed with it or when another scene
-    is evaluated."""
-    import weakref
-    key = (branching, max_depth)
-    ref = _TREE_CACHE.get("src")
-    if ref is not None and ref() is sources and key in _TREE_CACHE["trees"]:
-        return _TREE_CACHE["trees"][key]
-    if ref is None or ref() is not sources:
-        _TREE_CACHE.clear()
-        _TREE_CACHE["src"] = weakref.ref(
-            sources, lambda r: _TREE_CACHE.clear() if _TREE_CACHE.get("src") is r else None)
-        _TREE_CACHE["trees"] = {}
-    tree = build_tree(sources, branching, max_depth)
-    _TREE_CACHE["trees"][key] = tree
-    return tree
+    most recent SourceSet (immutable: SourceSet owns frozen copies of its arrays,
+    so the tree is the same bits): repeated evaluate_field calls on one scene pay
+    the build once.  Only the latest SourceSet is kept (weakly): its trees are
+    freed with it or when another scene is evaluated.  Keyed on the current CUDA
+    device too (a device tree is only valid on the device that built it), and
+    locked so two host threads never build or evict concurrently."""
+    key = (dev.torch().cuda.current_device(), branching, max_depth)
+    with _TREE_LOCK:
+        ref = _TREE_CACHE.get("src")
+        if ref is not None and ref() is sources and key in _TREE_CACHE["trees"]:
+            return _TREE_CACHE["trees"][key]
+        if ref is None or ref() is not sources:
+            _TREE_CACHE.clear()
+            _TREE_CACHE["src"] = weakref.ref(
+                sources, lambda r: _TREE_CACHE.clear() if _TREE_CACHE.get("src") is r else None)
+            _TREE_CACHE["trees"] = {}
+        tree = build_tree(sources, branching, max_depth)
+        _TREE_CACHE["trees"][key] = tree
+        return tree
 
 
 def _variant(config) -> int:
@@ -230,27 +234,30 @@ def _variant(config) -> int:
 
 
 _PINNED: list = []  # (tensor, ndarray) pinned output blocks, reused once unreferenced
+_PINNED_LOCK = threading.Lock()
 
 
 def _pinned_block(nbytes: int):
     """(data pointer, uint8 ndarray) of a pinned host block of >= nbytes.  Result
     arrays are numpy views of the block's ndarray (their .base chain ends there),
     so a block whose ndarray has no other referrers is free and is reused:
-    page-locking fresh memory costs tens of ms per call."""
+    page-locking fresh memory costs tens of ms per call.  Under a lock: the
+    caller's reference exists before another thread can test the block."""
     torch = dev.torch()
-    for t, mem in _PINNED:
-        # referrers: the pool tuple, the loop variable, getrefcount's argument
-        if sys.getrefcount(mem) <= 3 and mem.nbytes >= nbytes:
-            return t.data_ptr(), mem
-    t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-    entry = (t, t.numpy())
-    _PINNED.append(entry)
-    if len(_PINNED) > 4:  # keep the pool small: drop the oldest free block
-        for i, (_, old) in enumerate(_PINNED[:-1]):
-            if sys.getrefcount(old) <= 3:
-                del _PINNED[i]
-                break
-    return entry[0].data_ptr(), entry[1]
+    with _PINNED_LOCK:
+        for t, mem in _PINNED:
+            # referrers: the pool tuple, the loop variable, getrefcount's argument
+            if sys.getrefcount(mem) <= 3 and mem.nbytes >= nbytes:
+                return t.data_ptr(), mem
+        t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        entry = (t, t.numpy())
+        _PINNED.append(entry)
+        if len(_PINNED) > 4:  # keep the pool small: drop the oldest free block
+            for i, (_, old) in enumerate(_PINNED[:-1]):
+                if sys.getrefcount(old) <= 3:
+                    del _PINNED[i]
+                    break
+        return entry[0].data_ptr(), entry[1]
 
 
 def _pipeline_chunks(n: int) -> int:
@@ -307,19 +314,13 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
             raise ValueError("prebuilt tree branching factor does not match config")
         h = C.c_void_p(tree._device_tree().handle)
     # one pinned block for all outputs: 5 x 8-byte columns, then the flags
-    _t0 = time.perf_counter()
     base, mem = _pinned_block(41 * n + 8)
-    _t1 = time.perf_counter()
     ptrs = [base + 8 * n * k for k in range(5)] + [base + 40 * n]
     _lib.check(L.fsb_evaluate_field_host(
         h, C.byref(args), q.ctypes.data_as(C.c_void_p), n,
         C.c_void_p(ptrs[0]), C.c_void_p(ptrs[1]), C.c_void_p(ptrs[5]), C.c_void_p(ptrs[2]),
         C.c_void_p(ptrs[3]), C.c_void_p(ptrs[4]),
         int(chunks if chunks is not None else _pipeline_chunks(n)), _sp()))
-    _t2 = time.perf_counter()
-    if os.environ.get("FSB_PY_TRACE"):
-        print(f"evaluate_field: pinned alloc {(_t1 - _t0) * 1e3:.3f} ms, "
-              f"host pipeline {(_t2 - _t1) * 1e3:.3f} ms", file=sys.stderr)
     cols = [mem[8 * n * k: 8 * n * (k + 1)] for k in range(5)]
     return FieldResult(values=cols[0].view(np.float64), raw=cols[1].view(np.float64),
                        flagged=mem[40 * n: 41 * n].view(bool),

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 import weakref
 from dataclasses import dataclass
 
@@ -24,6 +25,7 @@ __all__ = ["TreeNode", "Octree", "build_tree", "far_field_ratio", "validate_tree
            "dump_outline"]
 
 _DIAM_FLOOR = 1e-12
+_UPLOAD_LOCK = threading.Lock()
 _ARRAY_SLOTS = ("bbox_min", "bbox_max", "diameter", "aggregate_mass", "aggregate_weight",
                 "center_of_mass", "child_start", "child_count", "child_index", "begin", "end",
                 "depth", "permuted_indices", "points", "masses", "weights")
@@ -127,8 +129,11 @@ class Octree:
         """The device handle; host-constructed trees are uploaded once."""
         d = object.__getattribute__(self, "_dev")
         if d is None:
-            d = _upload_core_arrays(self.core_arrays())
-            object.__setattr__(self, "_dev", d)
+            with _UPLOAD_LOCK:  # one upload per tree, even from two host threads
+                d = object.__getattribute__(self, "_dev")
+                if d is None:
+                    d = _upload_core_arrays(self.core_arrays())
+                    object.__setattr__(self, "_dev", d)
         return d
 
     @property

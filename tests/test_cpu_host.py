@@ -215,3 +215,14 @@ def test_estimator_api_params_and_clone():
     p = est.get_params()
     assert p["beta"] == 3.0 and p["seed"] == 4 and p["method"] == "barnes_hut"
     assert clone(est).get_params() == p
+
+
+def test_source_set_owns_its_arrays():
+    """SourceSet keeps frozen copies of its inputs, so a device tree cached for it
+    (evaluate_field without a tree) cannot go stale when the caller later writes
+    its own buffer (the reference freezes the caller's arrays in place)."""
+    pos = np.random.default_rng(0).uniform(-1, 1, (1000, 3))
+    s = fs.SourceSet(pos, np.ones(1000))
+    pos[:] = 0.0
+    assert not np.all(s.positions == 0.0)
+    assert not s.positions.flags.writeable and not s.masses.flags.writeable
