@@ -225,6 +225,16 @@ int fsb_make_queries(int kind, int64_t n, const double *ax0, const double *ax1,
                      const double *ax2, int64_t r1, int64_t r2, const double *geo,
                      const uint64_t *state4, double *out, void *stream);
 
+/* Text writers (host code, no GPU): the reference's field CSV
+ * (scene_io.py:246-262, "index,x,y,z,value,flag" with every float as Python's
+ * "{:.17g}") and points file (scene_io.py:75-80, "x y z m[ my mz]"), byte for
+ * byte, rows formatted on all host threads.  queries (n,3), values (n,),
+ * flagged (n,) uint8; positions (m,3), masses (m,c), c in {1, 3}. */
+int fsb_write_field_csv(const char *path, int64_t n, const double *queries,
+                        const double *values, const uint8_t *flagged);
+int fsb_write_points_file(const char *path, int64_t m, int c, const double *positions,
+                          const double *masses);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,8 @@ SIGNATURES = {
     "fsb_error_stats": [_P, _P, _P, _P, _I64, _P, C.POINTER(_I64), _P],
     "fsb_sample_mesh_surface": [_P, _I64, _P, _P, _I64, _P, _D, _D, _P, _P, _P, _P],
     "fsb_make_queries": [_I, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P],
+    "fsb_write_field_csv": [C.c_char_p, _I64, _P, _P, _P],
+    "fsb_write_points_file": [C.c_char_p, _I64, _I, _P, _P],
 }
 _RESTYPES = {"fsb_last_error": C.c_char_p}
 

@@ -113,7 +113,7 @@ def rmse(estimates, reference, flags=None) -> float:
 # Oracle caching (bench.py:98-136)
 # ---------------------------------------------------------------------------
 
-_ORACLE_CACHE: dict[str, DeviceField] = {}
+_ORACLE_CACHE: dict[str, list] = {}  # key -> [DeviceField, FieldResult or None]
 _CACHE_STATS = {"hits": 0, "misses": 0}
 
 
@@ -127,21 +127,30 @@ def content_hash(sources: SourceSet, kernel: KernelSpec, queries: QuerySet) -> s
     return h.hexdigest()
 
 
-def _oracle_device(sources: SourceSet, kernel: KernelSpec, queries: QuerySet) -> DeviceField:
+def _oracle_entry(sources: SourceSet, kernel: KernelSpec, queries: QuerySet) -> list:
     key = content_hash(sources, kernel, queries)
     if key in _ORACLE_CACHE:
         _CACHE_STATS["hits"] += 1
         return _ORACLE_CACHE[key]
     _CACHE_STATS["misses"] += 1
-    result = evaluate_field_device(EstimatorConfig("brute_force"), sources, kernel, queries)
-    _ORACLE_CACHE[key] = result
-    return result
+    entry = [evaluate_field_device(EstimatorConfig("brute_force"), sources, kernel, queries),
+             None]
+    _ORACLE_CACHE[key] = entry
+    return entry
+
+
+def _oracle_device(sources: SourceSet, kernel: KernelSpec, queries: QuerySet) -> DeviceField:
+    return _oracle_entry(sources, kernel, queries)[0]
 
 
 def oracle_field(sources: SourceSet, kernel: KernelSpec, queries: QuerySet) -> FieldResult:
     """Brute-force reference field (FP64 parity brute force on the GPU), cached on
-    input content; the device copy stays cached for the sweeps."""
-    return _oracle_device(sources, kernel, queries).to_host()
+    input content (bench.py:117-128: a hit returns the same FieldResult object);
+    the device copy stays cached for the sweeps."""
+    entry = _oracle_entry(sources, kernel, queries)
+    if entry[1] is None:
+        entry[1] = entry[0].to_host()
+    return entry[1]
 
 
 def oracle_cache_stats() -> dict[str, int]:

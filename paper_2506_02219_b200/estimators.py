@@ -71,8 +71,22 @@ def _worker_count() -> int:
         n = int(raw)
     except ValueError:
         n = 0
-    cap = os.cpu_count() or 1
-    return cap if n <= 0 else min(n, cap)
+    return _thread_cap() if n <= 0 else min(n, _thread_cap())
+
+
+def _thread_cap() -> int:
+    """The host thread pool size the reference caps at (numba.config.NUMBA_NUM_THREADS:
+    the NUMBA_NUM_THREADS variable, else the CPUs this process may run on)."""
+    try:
+        v = int(os.environ.get("NUMBA_NUM_THREADS", ""))
+        if v > 0:
+            return v
+    except ValueError:
+        pass
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
 
 
 def _check_channels(sources: SourceSet, kernel: KernelSpec) -> None:
