@@ -235,6 +235,12 @@ int fsb_write_field_csv(const char *path, int64_t n, const double *queries,
 int fsb_write_points_file(const char *path, int64_t m, int c, const double *positions,
                           const double *masses);
 
+/* Self-test (synchronous, default stream): the FP64 kernels' branch-free
+ * division / square root against __ddiv_rn / __dsqrt_rn on n pseudo-random
+ * operand pairs.  counts4 (host) = {division fast-path cases, bit mismatches,
+ * square-root fast-path cases, bit mismatches}; both mismatch counts must be 0. */
+int fsb_selftest_fp64(int64_t n, uint64_t seed, unsigned long long *counts4);
+
 #ifdef __cplusplus
 }
 #endif

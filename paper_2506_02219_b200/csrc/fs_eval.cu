@@ -890,7 +890,7 @@ int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
                int64_t* path_count, cudaStream_t s, int share, int flags) {
   if (n <= 0) return 0;
   const int variant = flags & kFlagAlg2;
-  const bool shuffled = (flags & kFlagShuffled) != 0;  // order = shuffle_order(n, seed, qoff)
+  bool shuffled = (flags & kFlagShuffled) != 0;  // order = shuffle_order(n, seed, qoff)
   // the fast FP32 kernels implement the reference variant; Alg. 2 runs the
   // generic per-query kernel in either precision
   if (!f64 && variant == 0 && !std::getenv("FSB_DISABLE_FAST")) {
@@ -905,6 +905,20 @@ int stochastic(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
     }
   }
   Scratch order;  // the generic kernel reads the shuffled order from memory
+  if (shuffled) {
+    FS_TRY(order.alloc(sizeof(int32_t) * (size_t)n, s));
+    FS_TRY(shuffle_order(n, seed, query_offset, order.as<int32_t>(), s));
+    qperm = order.as<int32_t>();
+    shuffled = false;
+  }
+  // FP64 reference variant: the queue kernel (fs_sto64.cu), same bits
+  if (f64 && variant == 0) {
+    bool used = false;
+    FS_TRY(stochastic64(t, kid, alpha, dfloor, q, n, qperm, n_samples, rr_mode, seed,
+                        query_offset, share, (double*)out, visited, path_steps, path_count, s,
+                        &used));
+    if (used) return 0;
+  }
   if (shuffled) {
     FS_TRY(order.alloc(sizeof(int32_t) * (size_t)n, s));
     FS_TRY(shuffle_order(n, seed, query_offset, order.as<int32_t>(), s));

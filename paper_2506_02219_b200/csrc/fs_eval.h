@@ -36,6 +36,10 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
                     const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed,
                     int64_t qoff, int share, float* out, int64_t* visited, int64_t* path_steps,
                     int64_t* path_count, cudaStream_t s, bool* used, bool shuffled = false);
+int stochastic64(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
+                 const int32_t* qperm, int n_samples, int rr_mode, uint64_t seed, int64_t qoff,
+                 int share, double* out, int64_t* visited, int64_t* path_steps,
+                 int64_t* path_count, cudaStream_t s, bool* used);
 int barnes_hut_split(FsTree* t, int kid, double alpha, double dfloor, const double* q, int64_t n,
                      const int32_t* qperm, double beta, float* out, int64_t* visited,
                      cudaStream_t s, bool* done, bool vote = false);

@@ -78,6 +78,7 @@ int ensure_lo(FsTree* t, bool f64, cudaStream_t s);
 int ensure_fast(FsTree* t, cudaStream_t s);
 int ensure_path(FsTree* t, cudaStream_t s);
 int ensure_pairs(FsTree* t, cudaStream_t s);
+int ensure_cm64(FsTree* t, cudaStream_t s);
 constexpr int64_t kShuffleWindow = 1 << 16;  // positions per shuffle window (warp-shared mode)
 int shuffle_order(int64_t n, uint64_t seed, int64_t qoff, int32_t* perm, cudaStream_t s);
 void free_tree(FsTree* t);

@@ -22,7 +22,8 @@ void free_tree(FsTree* t) {
                   t->perm, t->points, t->masses, t->weights, t->lo2pre, t->pre2lo, t->skip,
                   t->fc_lo, t->bh32, t->bh64, t->lo_geo32, t->lo_mass32, t->lo_geo64,
                   t->lo_mass64, t->lo_topo, t->pts32a, t->pts32b, t->pts64a, t->pts64b,
-                  t->lo_cm32, t->lo_m12_32, t->lo_begin, t->pt_path, t->lo_cmp};
+                  t->lo_cm32, t->lo_m12_32, t->lo_begin, t->pt_path, t->lo_cmp, t->lo_cm64,
+                  t->lo_m12_64};
   // the handle's owner may still have work queued on any stream: wait for the
   // device once, then return every array to the pool
   cudaDeviceSynchronize();
@@ -441,10 +442,40 @@ int ensure_fast(FsTree* t, cudaStream_t s) {
     FS_CK(cudaMemcpyAsync(ldiam.data(), ddiam.p, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
   }
   FS_CK(cudaStreamSynchronize(s));
-  for (int l = 0; l < nl; ++l) t->level_diam[l] = (float)ldiam[l];
+  for (int l = 0; l < nl; ++l) {
+    t->level_diam[l] = (float)ldiam[l];
+    t->level_diam64[l] = ldiam[l];
+  }
   t->uniform_diam = res[0] == 0 && t->num_levels <= FsTree::kMaxLevels;
   t->first_multi_level = res[1];
   t->fast_ready = true;
+  FS_CK(cudaGetLastError());
+  return 0;
+}
+
+// ------------------------------------------------ FP64 queue-kernel records
+__global__ void k_pack_cm64(const int32_t* __restrict__ lo2pre, const double* __restrict__ com,
+                            const double* __restrict__ am, int64_t n, int c,
+                            double4* __restrict__ cm, double2* __restrict__ m12) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t i = lo2pre[r];
+  cm[r] = make_double4(com[3 * i], com[3 * i + 1], com[3 * i + 2], am[(int64_t)c * i]);
+  if (m12) m12[r] = make_double2(am[(int64_t)c * i + 1], am[(int64_t)c * i + 2]);
+}
+
+int ensure_cm64(FsTree* t, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lk(t->mu);
+  if (t->lo_cm64) return 0;
+  double4* cm = nullptr;
+  double2* m12 = nullptr;
+  FS_TRY(dalloc(&cm, t->n, s));
+  if (t->c >= 3) FS_TRY(dalloc(&m12, t->n, s));
+  k_pack_cm64<<<grid_for(t->n, 256), 256, 0, s>>>(t->lo2pre, t->com, t->agg_mass, t->n, t->c, cm,
+                                                  m12);
+  FS_CK(cudaStreamSynchronize(s));
+  t->lo_m12_64 = m12;
+  t->lo_cm64 = cm;
   FS_CK(cudaGetLastError());
   return 0;
 }

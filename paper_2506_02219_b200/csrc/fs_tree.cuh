@@ -60,6 +60,10 @@ struct FsTree {
   bool uniform_diam = false;     // every level has one cell diameter (uniform splits)
   int first_multi_level = 1 << 30;  // shallowest level holding a multi-point leaf
   float level_diam[kMaxLevels];
+  double level_diam64[kMaxLevels];  // the same, exact (FP64 queue kernel's _ffr)
+  // FP64 queue kernel (ensure_cm64): {cx, cy, cz, m0} and {m1, m2} per level-order node
+  double4* lo_cm64 = nullptr;
+  double2* lo_m12_64 = nullptr;
   float4* lo_cm32 = nullptr;     // {cx, cy, cz, m0} per level-order node
   float2* lo_m12_32 = nullptr;   // {m1, m2} (winding)
   int32_t* lo_begin = nullptr;   // point-range begin per level-order node

@@ -124,3 +124,21 @@ def test_gpu_evaluate_field_device_tree_matches_reference(fs, entry):
                           src, kern, qs)
     _assert_close(r.raw, A[pre + "sto_d4_S3_rr0_seed11_off0"], entry["kernel"], "sto")
     np.testing.assert_array_equal(r.visited_nodes, A[pre + "sto_d4_S3_rr0_seed11_off0_visited"])
+
+
+@pytest.mark.gpu
+def test_fp64_branch_free_div_sqrt_bitwise_equal_intrinsics():
+    """The FP64 queue kernel's branch-free division / square root (fs_common.cuh
+    ddiv_fast / dsqrt_fast) must equal __ddiv_rn / __dsqrt_rn bit for bit whenever
+    they claim the fast path (else the kernel recomputes with the intrinsic)."""
+    import ctypes as C
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_02219_b200 import _lib
+    counts = (C.c_ulonglong * 4)()
+    for seed in (1, 2, 3):
+        _lib.check(_lib.lib().fsb_selftest_fp64(1 << 24, seed, counts))
+        div_ok, div_bad, sqrt_ok, sqrt_bad = list(counts)
+        assert div_bad == 0 and sqrt_bad == 0, list(counts)
+        assert div_ok > (1 << 23) and sqrt_ok > (1 << 23)  # the fast path is the common case

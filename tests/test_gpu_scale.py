@@ -259,3 +259,33 @@ def test_tree_reused_for_repeated_calls_on_one_scene(fs, monkeypatch):
     assert len(calls) == 3
     ref = fs.evaluate_field(cfg, s, kern, q, tree=fs.build_tree(s, 4))
     np.testing.assert_array_equal(a.raw, ref.raw)
+
+
+@pytest.mark.parametrize("kind", ["coulomb", "winding_dipole", "smooth_exp"])
+def test_fp64_queue_kernel_equals_per_query_kernel(fs, kind, monkeypatch):
+    """The FP64 queue kernel (fs_sto64.cu, level-1/2 staged, walks drained by the
+    block) and the thread-per-query parity kernel give the same bytes: values and
+    all three counters, for every rr mode, S = 1 / 7 / 150 (several drain rounds),
+    per-query and warp-shared streams, and a query offset."""
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    if kind == "winding_dipole":
+        s = scenes.build_sources(dict(kind="mesh_sphere_winding", m=2 ** 15, seed=3))
+    else:
+        s = scenes.build_sources(dict(kind="mesh_torus", m=2 ** 15, seed=3))
+        if kind == "smooth_exp":
+            s = fs.SourceSet(s.positions, np.ones((len(s), 1)))
+    kern = fs.KernelSpec(kind)
+    t = fs.build_tree(s, 4)
+    q = fs.QuerySet(np.random.default_rng(9).uniform(-0.8, 0.8, (1500, 3)))
+    for S, rr, sharing, off in ((1, "paper_ratio", "query", 0), (7, "fixed_half", "query", 77),
+                                (150, "disabled", "query", 0), (1, "paper_ratio", "warp", 0),
+                                (3, "paper_ratio", "query", 5)):
+        cfg = fs.EstimatorConfig("stochastic", seed=11, samples_per_subdomain=S, rr_mode=rr,
+                                 rng_sharing=sharing)
+        monkeypatch.delenv("FSB_STO64_OFF", raising=False)
+        a = evaluate_field_device(cfg, s, kern, q, t, query_offset=off).to_host()
+        monkeypatch.setenv("FSB_STO64_OFF", "1")
+        b = evaluate_field_device(cfg, s, kern, q, t, query_offset=off).to_host()
+        for k in ("raw", "visited_nodes", "path_steps", "path_count"):
+            np.testing.assert_array_equal(getattr(a, k), getattr(b, k),
+                                          err_msg=f"{kind} S={S} {rr} {sharing} {k}")
