@@ -197,6 +197,191 @@ def peaks():
         return {}
 
 
+C5_SOURCES = 2 ** 24
+C5_QUERIES = 10 ** 7
+
+
+def workload_c5(m=C5_SOURCES, n=C5_QUERIES):
+    """BASELINE configs[4] / SURVEY 8(d) C5: the C4 generator at 2^24 samples,
+    default_rng(5).uniform(-1, 1, (10^7, 3)) queries."""
+    from paper_2506_02219_b200 import scenes as S
+    from paper_2506_02219_b200.types import KernelSpec, QuerySet
+    v, f = S.torus(0.25, 0.06)
+    v = S.rotate_x(v, 0.7) + np.array([0.1, 0.05, -0.1])
+    src = S.sample_mesh_surface(v, f, m, seed=7, kernel_kind="coulomb")
+    qs = QuerySet(np.random.default_rng(5).uniform(-1, 1, (n, 3)))
+    return src, qs, KernelSpec("coulomb")
+
+
+def c5_config(world):
+    return {"workload": "C5: coulomb, 2^24 tilted-torus surface samples, 10^7 default_rng(5) "
+                        "uniform [-1,1]^3 queries (BASELINE configs[4])",
+            "sources": C5_SOURCES, "queries": C5_QUERIES, "method": "stochastic S=1 paper_ratio",
+            "rng_streams": STREAM_NOTES["warp"], "branching": {"stochastic": 4, "barnes_hut": 2},
+            "precision": "f32 terms, f64 accumulation",
+            "l2": "inputs larger than L2 (tree ~0.9 GB, queries 240 MB); no flush",
+            "parallelism": (f"strong scaling: {world} rank(s), query slabs on 2^16-position "
+                            f"shuffle windows (query_offset = slab start), replica tree per rank, "
+                            f"all_gather of the FP64 field inside every step")}
+
+
+def run_c5(args, world, rank, local, anchor=False):
+    """C5 strong scaling (SURVEY 8(e)): a fixed 10^7 queries split into `world` slabs;
+    every step evaluates this rank's slab (device-resident queries) and all-gathers
+    the field (FP64 values, NCCL) -- both inside the timed region, max over ranks.
+    Returns the JSON line (rank 0) or, with anchor=True at N=1, a compact object
+    for the C4 line."""
+    import torch
+    import torch.distributed as dist
+    import paper_2506_02219_b200 as fs
+    from paper_2506_02219_b200 import _device as dev
+    from paper_2506_02219_b200.estimators import evaluate_field_device
+    from paper_2506_02219_b200.sharding import SHUFFLE_WINDOW, broadcast_tree, slab
+
+    t0 = time.perf_counter()
+    src, qs, kern = workload_c5()
+    gen_s = time.perf_counter() - t0
+    n = len(qs)
+    a, b = slab(n, rank, world, SHUFFLE_WINDOW)
+    widths = [slab(n, r, world, SHUFFLE_WINDOW)[1] - slab(n, r, world, SHUFFLE_WINDOW)[0]
+              for r in range(world)]
+    width = max(widths)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    t0 = time.perf_counter()
+    tree = fs.build_tree(src, 4)
+    torch.cuda.synchronize()
+    build_ms = (time.perf_counter() - t0) * 1e3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fs.build_tree(src, 4)
+    e1.record()
+    torch.cuda.synchronize()
+    build_warm_ms = e0.elapsed_time(e1)
+    tree_dist = None
+    if world > 1:
+        barrier()
+        t0 = time.perf_counter()
+        bt = broadcast_tree(src if rank == 0 else None, 4, src=0)
+        barrier()
+        bcast_ms = (time.perf_counter() - t0) * 1e3
+        del bt
+        tt = torch.tensor([build_ms, build_warm_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tree_dist = {"replica_build_ms_max_over_ranks": float(tt[0]),
+                     "replica_build_warm_ms_max_over_ranks": float(tt[1]),
+                     "build_on_rank0_and_broadcast_ms": bcast_ms,
+                     "backend": dist.get_backend(),
+                     "used": "replica (deterministic per-rank build, no collective)"}
+    cfg = fs.EstimatorConfig("stochastic", samples_per_subdomain=1, seed=1, precision="f32",
+                             rng_sharing="warp")
+    q_dev = dev.to_device(qs.positions[a:b])
+    full = torch.empty(world * width, dtype=torch.float64, device="cuda")
+    pad = torch.zeros(width, dtype=torch.float64, device="cuda")
+
+    def step():
+        r = evaluate_field_device(cfg, src, kern, q_dev, tree, query_offset=a)
+        if world == 1:
+            return r.values
+        pad[: b - a].copy_(r.values)
+        if dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(full, pad)
+        else:  # (gloo: several ranks sharing one GPU in tests)
+            dist.all_gather(list(full.split(width)), pad)
+        return full
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches = _count_launches(step)
+    with Clocks(local) as clk:
+        barrier()
+        ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev_a.record()
+        clk.active = True
+        for _ in range(args.steps):
+            res = step()
+        ev_b.record()
+        barrier()
+        clk.active = False
+    step_ms = ev_a.elapsed_time(ev_b) / args.steps
+    if world > 1:
+        tt = torch.tensor([step_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms = float(tt.item())
+    value = n / (step_ms * 1e-3)
+    # the gathered field equals one process evaluating all 10^7 queries (rank 0, untimed)
+    same = None
+    if rank == 0:
+        got = torch.cat([res[r * width: r * width + widths[r]] for r in range(world)])
+        if world > 1:
+            ref = evaluate_field_device(cfg, src, kern, dev.to_device(qs.positions), tree)
+            same = bool(torch.equal(got, ref.values))
+        else:
+            same = True
+        sub = np.linspace(0, n - 1, 65536).astype(np.int64)
+        truth = fs.evaluate_field(fs.EstimatorConfig("brute_force", precision="f32"), src, kern,
+                                  fs.QuerySet(qs.positions[sub])).values
+        err = median_rel(got[torch.as_tensor(sub, device="cuda")].cpu().numpy(), truth)
+    # e2e through the public multi-GPU API: host queries in, gathered host field out
+    e2e = None
+    if not anchor:
+        from paper_2506_02219_b200.sharding import evaluate_field_sharded
+        host = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+        host.numpy()[:] = qs.positions
+        qset = fs.QuerySet(host.numpy())
+        if world > 1:
+            fn = lambda: evaluate_field_sharded(cfg, src, kern, qset, tree)  # noqa: E731
+        else:
+            fn = lambda: fs.evaluate_field(cfg, src, kern, qset, tree=tree).values  # noqa: E731
+        for _ in range(max(2, args.warmup)):
+            fn()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            vals = fn()
+        barrier()
+        dt = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            tt = torch.tensor([dt], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": n / dt, "unit": "queries/s", "h2d_bytes_per_step": int((b - a) * 24),
+               "d2h_bytes_per_step": int(vals.nbytes), "ms_per_step": dt * 1e3,
+               "api": ("paper_2506_02219_b200.sharding.evaluate_field_sharded (host slab in, "
+                       "all_gather, host field out)" if world > 1 else
+                       "paper_2506_02219_b200.evaluate_field (host numpy in/out)"),
+               "bytes_note": "per rank per step (h2d: the rank's slab; d2h: the gathered field)"}
+    if anchor:
+        return {"workload": c5_config(1)["workload"], "n_gpus": 1, "ms_per_step": step_ms,
+                "value": value, "unit": "queries/s", "s1_median_rel_err_65536_subset": err,
+                "tree_build_ms": {"first_call": build_ms, "warm": build_warm_ms},
+                "scene_generation_s": gen_s,
+                "note": "C5 at one GPU: the anchor of the strong-scaling curve that "
+                        "bench.py --gpus N (N > 1) measures on C5"}
+    out = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (reference mesh generators, fixed seeds)",
+           "config": c5_config(world), "clocks": clk.summary(), "e2e": e2e,
+           "gathered_equals_single_process": same,
+           "tree_build_ms": {"first_call": build_ms, "warm": build_warm_ms}}
+    if rank == 0:
+        out["accuracy"] = {"s1_median_rel_err": err,
+                           "truth": "GPU brute force (FP32 terms, FP64 accumulation) on 65,536 "
+                                    "queries spread over the 10^7"}
+    if tree_dist is not None:
+        out["tree_distribution"] = tree_dist
+    if launches is not None:
+        out["gpu_launches"] = launches * args.steps
+    return out
+
+
 # ----------------------------------------------------------------- our arm
 def run_ours(args):
     import ctypes as C
@@ -222,6 +407,16 @@ def run_ours(args):
     from paper_2506_02219_b200 import _device as dev
     from paper_2506_02219_b200 import _lib
     from paper_2506_02219_b200.estimators import evaluate_field_device
+
+    wl = args.workload if args.workload != "auto" else ("c4" if world == 1 else "c5")
+    if wl == "c5":
+        out = run_c5(args, world, rank, local)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        return
 
     L = _lib.lib()
     src, qs, kern = workload()
@@ -514,6 +709,31 @@ def run_ours(args):
                      "tools/micro/l2bw.cu (64 MB buffer)")}
         out["tree_build_ms"] = {"d4_first_call": build4_ms, "d2_first_call": build2_ms,
                                 "d4_warm": build4_warm_ms}
+        # the build is HBM-bound -- points/s, and the DRAM bytes of the
+        # build kernels from the committed ncu capture of one warm d = 4 build
+        out["tree_build"] = {"points_per_s_d4_warm": len(src) / (build4_warm_ms * 1e-3),
+                             "from": "device-resident FP64 inputs (the public build_tree adds "
+                                     "the host->device copy)",
+                             "dram_bytes": _profiled_build_traffic()}
+        # the API-default precision (f64, types.py:205): the FP64 parity kernels on the
+        # same workload, bitwise equal to the reference's cores
+        f64 = {}
+        for name, cfg in (("stochastic_s1", fs.EstimatorConfig("stochastic", seed=1)),
+                          ("barnes_hut_beta2", fs.EstimatorConfig("barnes_hut", beta=2.0))):
+            tr = tree4 if name.startswith("sto") else tree2
+            evaluate_field_device(cfg, src, kern, q_dev, tr)
+            torch.cuda.synchronize()
+            ev_a.record()
+            for _ in range(3):
+                r64 = evaluate_field_device(cfg, src, kern, q_dev, tr)
+            ev_b.record()
+            torch.cuda.synchronize()
+            ms = ev_a.elapsed_time(ev_b) / 3
+            f64[name] = {"ms_per_step": ms, "value": n / (ms * 1e-3),
+                         "median_rel_err": median_rel(r64.values.cpu().numpy(), truth_h)}
+        f64["note"] = ("precision='f64' (the reference's default): k_sto64 (FP64 queue kernel) and "
+                       "k_bh<F64>, every operation in the reference's order (bitwise)")
+        out["f64_default_precision"] = f64
 
         # ---- roofline of the stochastic kernel.  Work unit: one
         # node-term evaluation ("interaction": 8 FP32-pipe ops + 1 MUFU.RSQ, 10
@@ -530,7 +750,13 @@ def run_ours(args):
         inter_q = n2 + walk_inter
         samples_q = S * n_int
         ach = inter_q * n / (kern_ms * 1e-3)
-        limit = min(128 * sms * f_mhz * 1e6 / 8, 16 * sms * f_mhz * 1e6 / 1)  # coulomb I=8, U=1
+        nominal = min(128 * sms * f_mhz * 1e6 / 8, 16 * sms * f_mhz * 1e6 / 1)  # coulomb I=8, U=1
+        # measured on this GPU (fsb_micro_peaks): the Coulomb term at its best instruction
+        # mix with every operand on chip, and the MUFU.RSQ rate
+        mp = (C.c_double * 2)()
+        _lib.check(L.fsb_micro_peaks(mp, sp))
+        _lib.check(L.fsb_micro_peaks(mp, sp))
+        limit = float(mp[1])
         # pipe floor with the integer RNG work (6 splitmix64 per sample: 6 IMAD on
         # the FMA-heavy pipe + 14 ALU ops each; once per warp with shared streams):
         # max over FMA / ALU / MUFU pipes
@@ -547,20 +773,54 @@ def run_ours(args):
             "kernel": f"{kname}<coulomb, paper_ratio> (FP32)", "kernel_ms": kern_ms,
             "work": (f"{inter_q:.1f} interactions/query = {n2} dense level-2 records + "
                      f"{walk_inter:.1f} walk children; 10 flops each"),
-            "peak_source": (f"FP32 128/clk/SM over 8 ops, MUFU 16/clk/SM over 1 op, {sms} SMs "
-                            f"x {f_mhz:.0f} MHz (nominal pipe rates; no MEASURED_PEAKS.json "
-                            f"entry for FP32/MUFU)"),
+            "peak_source": ("measured on this GPU in this run: fsb_micro_peaks (csrc/fs_micro.cu, "
+                            "tools/micro/peaks.py) -- Coulomb node terms/s of the packed-FP32 + "
+                            "MUFU.RSQ loop with all operands on chip, x 10 flops (MEASURED_PEAKS."
+                            "json has no FP32/MUFU entry)"),
+            "measured_mufu_rsq_per_s": float(mp[0]),
+            "nominal_peak": nominal * 10 / 1e12, "frac_of_nominal": ach / nominal,
+            "nominal_source": (f"FP32 128/clk/SM over 8 ops, MUFU 16/clk/SM over 1 op, {sms} SMs "
+                               f"x {f_mhz:.0f} MHz"),
             "pipe_floor_ms": floor_ms, "frac_of_pipe_floor": floor_ms / kern_ms,
             "pipe_floor_note": (f"FMA/ALU/MUFU pipe floor incl. {samples_q} samples/query x 6 "
                                 f"splitmix64 mixes; cycles/query fma {fma_cyc:.1f} alu "
                                 f"{alu_cyc:.1f} mufu {mufu_cyc:.1f}")}
         if args.cpu_baseline and world == 1:
             out["cpu_baseline"] = _cpu_baseline(tree4, src, qs, kern, args)
+        if args.c5_anchor and world == 1:
+            out["c5"] = run_c5(args, 1, 0, local, anchor=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def _count_launches(fn):
+    """Kernels of libfastsum_b200.so (fsb:: and its CUB sorts) one call of fn launches
+    (CUPTI via torch.profiler, outside any timed region)."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        return sum(1 for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+                   and ("fsb" in e.name or "cub" in e.name.lower()))
+    except Exception as exc:  # pragma: no cover
+        log("profiler unavailable:", exc)
+        return None
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def _profiled_traffic(kernel_key: str):
@@ -578,6 +838,21 @@ def _profiled_traffic(kernel_key: str):
     return None
 
 
+def _profiled_build_traffic():
+    """Sum of dram__bytes over the build kernels of one warm d = 4 C4 build, from the
+    newest committed profiles/r*_build.json (tools/profile_build.py)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_build.json")), reverse=True):
+        try:
+            with open(path) as f:
+                side = json.load(f)
+            return {"bytes": side["dram_bytes_total"], "kernels": side["kernels"],
+                    "gpu_time_ms": side["gpu_time_ms"], "source": os.path.relpath(path, ROOT)}
+        except (OSError, ValueError, KeyError):
+            continue
+    return None
+
+
 def _level_sizes(tree):
     """(n1, n2, internal level-1 nodes) of the d=4 tree: level-1 nodes, their children."""
     cc = tree.child_count
@@ -589,37 +864,45 @@ def _level_sizes(tree):
 
 def _e2e(args, fs, src, kern, qs, tree, cfg, world, rank):
     """The step through the public API (evaluate_field, host numpy in / out): every
-    rank evaluates its own slab (query_offset = rank * n) from pinned host memory,
-    timed between barriers, max over ranks."""
+    rank evaluates its own slab (query_offset = rank * n), timed between barriers, max
+    over ranks.  The headline input is a QuerySet over page-locked host memory (what a
+    serving caller keeps); a plain (pageable) numpy QuerySet is timed beside it."""
     import torch
     import torch.distributed as dist
     n = len(qs)
     host = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
     host.numpy()[:] = qs.positions
-    qset = fs.QuerySet.__new__(fs.QuerySet)
-    object.__setattr__(qset, "positions", host.numpy())
     off = rank * n
-    r = None
-    for _ in range(max(2, args.warmup)):  # like the timed loop: the previous result stays alive
-        r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / args.steps
-    if world > 1:
-        tt = torch.tensor([dt], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt = float(tt.item())
+
+    def timed(qset):
+        r = None
+        for _ in range(max(2, args.warmup)):  # like the timed loop: the previous result stays alive
+            r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            tt = torch.tensor([dt], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        return dt, r
+
+    dt, r = timed(fs.QuerySet(host.numpy()))
+    dt_pg, _ = timed(fs.QuerySet(np.array(qs.positions)))
     out_bytes = sum(a.nbytes for a in (r.values, r.raw, r.flagged, r.visited_nodes, r.path_steps,
                                        r.path_count))
     return {"value": world * n / dt, "unit": "queries/s",
-            "h2d_bytes_per_step": int(host.numel() * 8), "d2h_bytes_per_step": int(out_bytes),
+            "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(out_bytes),
             "ms_per_step": dt * 1e3,
-            "api": "paper_2506_02219_b200.evaluate_field (host numpy in/out, pipelined slabs)",
+            "api": ("paper_2506_02219_b200.evaluate_field (host numpy in/out, pipelined slabs); "
+                    "QuerySet over page-locked host memory"),
+            "pageable": {"value": world * n / dt_pg, "ms_per_step": dt_pg * 1e3,
+                         "note": "the same call with a plain numpy (pageable) QuerySet"},
             "n_gpus": world, "bytes_note": "per rank per step"}
 
 
@@ -640,6 +923,7 @@ def _cpu_baseline(tree, src, qs, kern, args):
     dt = time.perf_counter() - t0
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": n_sample / dt, "unit": "queries/s", "cores": cores, "kind": "port",
+            "cpu_model": _cpu_model(), "nproc": os.cpu_count(),
             "sample": f"{n_sample} queries of the C4 plane, stochastic S=1 f64 "
                       f"(oracle/fastsum_oracle.c, OpenMP), tree from the GPU build"}
 
@@ -679,6 +963,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference mesh generators, fixed seeds)",
             "config": config_block("query"), "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
+                             "cpu_model": _cpu_model(), "nproc": os.cpu_count(),
                              "sample": f"{n_sample} random queries of the C4 plane per step, "
                                        f"stochastic S=1 f64, oracle/fastsum_oracle.c (OpenMP)"},
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -694,6 +979,11 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-sample", type=int, default=N_SIDE * N_SIDE)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--workload", choices=("auto", "c4", "c5"), default="auto",
+                    help="auto: C4 (the headline, BASELINE configs[3]) on one GPU, C5 strong "
+                         "scaling (configs[4]) on N > 1")
+    ap.add_argument("--no-c5-anchor", dest="c5_anchor", action="store_false",
+                    help="skip the C5 one-GPU anchor in the C4 line")
     ap.add_argument("--streams", choices=("warp", "query"), default="warp",
                     help="RNG streams of the headline step (the other mode is reported beside)")
     args = ap.parse_args()

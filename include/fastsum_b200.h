@@ -241,6 +241,11 @@ int fsb_write_points_file(const char *path, int64_t m, int c, const double *posi
  * square-root fast-path cases, bit mismatches}; both mismatch counts must be 0. */
 int fsb_selftest_fp64(int64_t n, uint64_t seed, unsigned long long *counts4);
 
+/* Measured compute ceilings for the roofline (synchronises): out2 (host) =
+ * {MUFU.RSQ ops/s, Coulomb node-term interactions/s at the packed-FP32 + MUFU
+ * instruction mix with every operand on chip}. */
+int fsb_micro_peaks(double *out2, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

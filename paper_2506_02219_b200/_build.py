@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libfastsum_b200.so")
-SOURCES = ["fs_build.cu", "fs_pack.cu", "fs_eval.cu", "fs_sto_fast.cu", "fs_abi.cu", "fs_host.cu", "fs_stats.cu", "fs_bh_split.cu", "fs_scene.cu", "fs_io.cu", "fs_sto64.cu"]
+SOURCES = ["fs_build.cu", "fs_pack.cu", "fs_eval.cu", "fs_sto_fast.cu", "fs_abi.cu", "fs_host.cu", "fs_stats.cu", "fs_bh_split.cu", "fs_scene.cu", "fs_io.cu", "fs_sto64.cu", "fs_micro.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1,0 +1,122 @@
+// fs_micro.cu -- measured compute ceilings of this GPU for the roofline
+// denominators the driver does not measure (MEASURED_PEAKS.json has HBM and
+// bf16 only):
+//   [0] MUFU.RSQ throughput (independent rsqrt.approx.ftz.f32 chains), ops/s;
+//   [1] the Coulomb node-term interaction at its best instruction mix, terms/s:
+//       the packed-FP32 loop of k_brute32_coulomb2 / the dense parts of the
+//       stochastic kernels (FADD2 x3, FFMA2 x3 + 1 accumulate per two terms,
+//       one MUFU.RSQ per term) over a shared-memory tile with 16 queries per
+//       thread -- every operand on chip, so nothing but the FP32/MUFU pipes and
+//       issue bound it.
+// tools/micro/peaks.cu is the stand-alone copy; bench.py calls fsb_micro_peaks
+// on the bench's own GPU and clocks.
+#include <cstdio>
+
+#include "../../include/fastsum_b200.h"
+#include "fs_common.cuh"
+#include "fs_internal.h"
+
+namespace fsb {
+namespace {
+
+constexpr int kChains = 8;
+
+__global__ void __launch_bounds__(256) k_mufu_rsq(int iters, float seed, float* sink) {
+  float v[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) v[c] = seed + (float)(threadIdx.x + c) * 1e-3f + 1.0f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) v[c] = rsqrt_ftz(v[c]);
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) acc += v[c];
+  if (acc == 12345.f) *sink = acc;
+}
+
+constexpr int kTile = 256, kQpt = 16;
+
+__global__ void __launch_bounds__(256) k_coulomb_terms(int reps, float seed, float* sink) {
+  __shared__ float4 sa[2 * kTile];
+  for (int k = threadIdx.x; k < kTile; k += blockDim.x) {
+    const float x = seed + 0.01f * k, y = 0.5f - 0.003f * k, z = 0.25f + 0.002f * k,
+                m = 1e-3f * (1 + (k & 7));
+    sa[2 * k] = make_float4(x, x, y, y);
+    sa[2 * k + 1] = make_float4(z, z, -m, -m);
+  }
+  __syncthreads();
+  constexpr int P = kQpt / 2;
+  float2 qx[P], qy[P], qz[P], acc[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const float t = (float)(threadIdx.x * kQpt + 2 * k) * 1e-4f;
+    qx[k] = make_float2(-t, -t - 1e-4f);
+    qy[k] = make_float2(-0.3f * t, -0.3f * t);
+    qz[k] = make_float2(0.7f, 0.7f);
+    acc[k] = make_float2(0.f, 0.f);
+  }
+  const float2 fl2 = make_float2(1e-24f, 1e-24f);
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll 4
+    for (int j = 0; j < kTile; ++j) {
+      const float4 a = sa[2 * j], b = sa[2 * j + 1];
+      const float2 sx = make_float2(a.x, a.y), sy = make_float2(a.z, a.w),
+                   sz = make_float2(b.x, b.y), nm = make_float2(b.z, b.w);
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const float2 dx = __fadd2_rn(sx, qx[k]), dy = __fadd2_rn(sy, qy[k]),
+                     dz = __fadd2_rn(sz, qz[k]);
+        const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
+        acc[k] = __ffma2_rn(nm, make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y)), acc[k]);
+      }
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < P; ++k) s += acc[k].x + acc[k].y;
+  if (s == 12345.f) *sink = s;
+}
+
+}  // namespace
+}  // namespace fsb
+
+extern "C" int fsb_micro_peaks(double* out2, void* stream) {
+  using namespace fsb;
+  if (!out2) {
+    set_error("fsb_micro_peaks: null output");
+    return 1;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 148;
+  FS_CK(cudaGetDevice(&dev));
+  FS_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  Scratch sink;
+  FS_TRY(sink.alloc(16, s));
+  cudaEvent_t e0, e1;
+  FS_CK(cudaEventCreate(&e0));
+  FS_CK(cudaEventCreate(&e1));
+  float ms = 0.f;
+  // MUFU: 8 blocks x 256 threads per SM, 8 chains per thread
+  const int grid = sms * 8, iters = 4096;
+  k_mufu_rsq<<<grid, 256, 0, s>>>(64, 1.0f, sink.as<float>());  // warm-up
+  FS_CK(cudaEventRecord(e0, s));
+  k_mufu_rsq<<<grid, 256, 0, s>>>(iters, 1.0f, sink.as<float>());
+  FS_CK(cudaEventRecord(e1, s));
+  FS_CK(cudaEventSynchronize(e1));
+  FS_CK(cudaEventElapsedTime(&ms, e0, e1));
+  out2[0] = (double)grid * 256 * iters * kChains / (ms * 1e-3);
+  // Coulomb terms: 4 blocks per SM (128 registers, as k_brute32_coulomb2)
+  const int grid2 = sms * 4, reps = 64;
+  k_coulomb_terms<<<grid2, 256, 0, s>>>(2, 0.1f, sink.as<float>());
+  FS_CK(cudaEventRecord(e0, s));
+  k_coulomb_terms<<<grid2, 256, 0, s>>>(reps, 0.1f, sink.as<float>());
+  FS_CK(cudaEventRecord(e1, s));
+  FS_CK(cudaEventSynchronize(e1));
+  FS_CK(cudaEventElapsedTime(&ms, e0, e1));
+  out2[1] = (double)grid2 * 256 * kQpt * (double)reps * kTile / (ms * 1e-3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  FS_CK(cudaGetLastError());
+  return 0;
+}

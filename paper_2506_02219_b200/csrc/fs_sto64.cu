@@ -481,10 +481,16 @@ int stochastic64(FsTree* t, int kid, double alpha, double dfloor, const double* 
                  int share, double* out, int64_t* visited, int64_t* path_steps,
                  int64_t* path_count, cudaStream_t s, bool* used) {
   *used = false;
-  if (std::getenv("FSB_STO64_OFF")) return 0;
-  if (t->root_kids <= 0 || t->num_levels > kMaxLevels64 || t->num_levels < 3) return 0;
+  const bool trace = std::getenv("FSB_TRACE_DISPATCH") != nullptr;
+  auto decline = [&](const char* why) {
+    if (trace) fprintf(stderr, "stochastic64: declined (%s)\n", why);
+    return 0;
+  };
+  if (std::getenv("FSB_STO64_OFF")) return decline("FSB_STO64_OFF");
+  if (t->root_kids <= 0 || t->num_levels > kMaxLevels64 || t->num_levels < 3)
+    return decline("tree shape");
   FS_TRY(ensure_fast(t, s));  // per-level diameters, multi-point leaf levels
-  if (!t->uniform_diam) return 0;
+  if (!t->uniform_diam) return decline("non-uniform cell diameters");
   FS_TRY(ensure_lo(t, true, s));  // FP64 points (multi-point leaves), topology
   FS_TRY(ensure_path(t, s));
   FS_TRY(ensure_cm64(t, s));
@@ -502,15 +508,15 @@ int stochastic64(FsTree* t, int kid, double alpha, double dfloor, const double* 
   V.n2 = (int)(t->level_off[3] - t->level_off[2]);
   V.first_multi = t->first_multi_level;
   for (int l = 0; l < kMaxLevels64; ++l) V.diam[l] = l < t->num_levels ? t->level_diam64[l] : 1.0;
-  if (V.base2 != 1 + V.n1) return 0;
+  if (V.base2 != 1 + V.n1) return decline("level layout");
   const int64_t nflat = (int64_t)V.n1 * n_samples;
-  if (nflat + V.n1 >= (1 << 22) || t->n >= (1ll << 30)) return 0;
+  if (nflat + V.n1 >= (1 << 22) || t->n >= (1ll << 30)) return decline("sizes");
   V.qcap = (int)std::min<int64_t>(FSB_S64_QCAP, std::max<int64_t>(kB64, nflat * kB64));
   V.qcap = std::max(V.qcap / kB64, 1) * kB64;
   const bool wind = kid == KID_WINDING;
   const size_t n12 = (size_t)V.n1 + V.n2;
   const size_t smem = 32 * (n12 + kB64) + 16 * n12 + (wind ? 16 * n12 : 0) + 4 * (2 * kB64 + 4);
-  if (smem > 200 * 1024) return 0;
+  if (smem > 200 * 1024) return decline("shared memory");
   KParams kp;
   kp.alpha = alpha;
   kp.dfloor = dfloor;
