@@ -35,7 +35,6 @@
 // winding) dense parts of both kernels run on the packed FP32 pipe
 // (FADD2/FFMA2, dense_coulomb_pairs / dense_winding_pairs).
 #include <algorithm>
-#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -808,523 +807,6 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 #undef s_t2
 }
 
-// ========================================= bucketed walks (per-query streams)
-// k_sto_fast serves a tile's walks right after sampling them, so every SM walks
-// into all level-2 subtrees at once and its drain is bound by scattered child
-// gathers from L2.  The bucketed path regroups the walks across queries:
-//  1. k_sto_bsample: dense part + sampling exactly as k_sto_fast; a walk that
-//     passes the level-1 roulette into an internal level-2 node k is written
-//     (32 B: query coordinates, owner, roulette key, sampled point, (a,
-//     creation index)) to bucket k in HBM at a slot from a warp-aggregated
-//     atomic.  Bucket k holds the expected number of samples that land in k
-//     (n S points(k) / points(a), before any roulette) + 6 sigma + 32; a walk
-//     that finds its bucket full is walked in place (same arithmetic).
-//  2. k_sto_bwalk: CTAs take equal contiguous ranges of the bucket-major walk
-//     list, so an SM serves one or two subtrees at a time and their records
-//     stay in L1; lanes refill independently as in the drain.  Each walk's
-//     residual and counters land in its owner's creation-ordered slot.
-//  3. k_sto_bfold: every query folds its slots in creation ((a, s)) order:
-//     the order, arithmetic and bits of k_sto_fast.
-constexpr int kBktBlock = 256;
-#ifndef FSB_BWALK_MINB
-#define FSB_BWALK_MINB 4
-#endif
-#ifndef FSB_BKT_SAMPLES
-#define FSB_BKT_SAMPLES (1 << 26)  // samples (queries x S x level-1 nodes) per slab
-#endif
-
-// one walk below level 2: the drain's per-lane state
-struct Walk {
-  int4 tp;  // {first child, count, begin, end} of the current node (only end - begin at level 2)
-  uint64_t path, kr;
-  float qx, qy, qz, prr, rp, cvn, resid;
-  int lvl, jj, count_a, seen, steps;
-};
-
-// level-2 start of a walk from the staged level-1/2 records (w.q*, w.kr, w.jj set)
-template <int KID, int RR>
-__device__ __forceinline__ void walk_begin(Walk& w, const FastView& V, int o_cm1, int o_tp1,
-                                           int o_cm2, int o_w2, int o_t2, float id1, float id2,
-                                           const KParams& kp, int a_ord, int k) {
-  w.path = V.path[w.jj];
-  const int4 tpa = sh_i4[o_tp1 + a_ord];
-  w.count_a = tpa.w - tpa.z;
-  const float4 c2 = sh_f4[o_cm2 + k];
-  w.rp = fdist(c2, w.qx, w.qy, w.qz) * id2;
-  w.prr = rr_fast_t<RR>(fdist(sh_f4[o_cm1 + a_ord], w.qx, w.qy, w.qz) * id1, w.rp);
-  w.cvn = fterm<KID>(c2, KID == KID_WINDING ? sh_f2[o_w2 + k] : make_float2(0.f, 0.f), w.qx,
-                     w.qy, w.qz, kp);
-  const int2 t2 = sh_i2[o_t2 + k];
-  w.tp = make_int4(t2.x & 0x1ffffff, (int)((unsigned)t2.x >> 25), 0, t2.y);
-  w.lvl = 2;
-  w.resid = 0.f;
-  w.seen = 0;
-  w.steps = 0;
-}
-
-// one level of a walk (k_sto_fast's drain body): sum the node's contiguous
-// children, pick the child holding the sampled point, commit the swap, roulette.
-// Returns false when the walk ends.
-template <int KID, int RR>
-__device__ __forceinline__ bool walk_level(Walk& w, const FastView& V, const KParams& kp) {
-  const int4 tp = w.tp;
-  if (tp.y <= 0) return false;
-  const float2 w0 = make_float2(0.f, 0.f);
-  const float qx = w.qx, qy = w.qy, qz = w.qz;
-  const bool cmulti = w.lvl + 1 >= V.first_multi;
-  float ks0 = 0.f, ks1 = 0.f;
-  int le = 0, c = 0;
-  if (!cmulti && w.lvl < V.path_levels) {
-    le = 1 + (int)((w.path >> (V.path_bits * w.lvl)) & ((1u << V.path_bits) - 1u));
-    if (tp.x & 1) {
-      ks0 += fterm<KID>(V.cm[tp.x], KID == KID_WINDING ? V.m12[tp.x] : w0, qx, qy, qz, kp);
-      c = 1;
-    }
-    for (; c + 3 < tp.y; c += 4) {
-      const int r = tp.x + c;
-      float4 c0, c1, c2, c3;
-      ld_pair(V.cm + r, c0, c1);
-      ld_pair(V.cm + r + 2, c2, c3);
-      ks0 += fterm<KID>(c0, KID == KID_WINDING ? V.m12[r] : w0, qx, qy, qz, kp);
-      ks1 += fterm<KID>(c1, KID == KID_WINDING ? V.m12[r + 1] : w0, qx, qy, qz, kp);
-      ks0 += fterm<KID>(c2, KID == KID_WINDING ? V.m12[r + 2] : w0, qx, qy, qz, kp);
-      ks1 += fterm<KID>(c3, KID == KID_WINDING ? V.m12[r + 3] : w0, qx, qy, qz, kp);
-    }
-    for (; c < tp.y; ++c)
-      ks0 += fterm<KID>(V.cm[tp.x + c], KID == KID_WINDING ? V.m12[tp.x + c] : w0, qx, qy, qz,
-                        kp);
-  } else if (!cmulti) {
-    for (; c + 1 < tp.y; c += 2) {
-      const int r = tp.x + c;
-      const float4 c0 = V.cm[r], c1 = V.cm[r + 1];
-      const int b0 = V.lb[r], b1 = V.lb[r + 1];
-      const float2 u0 = KID == KID_WINDING ? V.m12[r] : w0;
-      const float2 u1 = KID == KID_WINDING ? V.m12[r + 1] : w0;
-      ks0 += fterm<KID>(c0, u0, qx, qy, qz, kp);
-      ks1 += fterm<KID>(c1, u1, qx, qy, qz, kp);
-      le += (b0 <= w.jj) + (b1 <= w.jj);
-    }
-  }
-  for (; c < tp.y; ++c) {
-    const int r = tp.x + c;
-    const float4 cr = V.cm[r];
-    const float2 wr = KID == KID_WINDING ? V.m12[r] : w0;
-    float v;
-    if (cmulti) {
-      const int4 tc = V.topo[r];
-      v = (tc.y == 0 && tc.w - tc.z > 1) ? leaf_exact<KID>(V, tc.z, tc.w, qx, qy, qz, kp)
-                                         : fterm<KID>(cr, wr, qx, qy, qz, kp);
-    } else {
-      v = fterm<KID>(cr, wr, qx, qy, qz, kp);
-    }
-    ks0 += v;
-    le += V.lb[r] <= w.jj;
-  }
-  const float ks = ks0 + ks1;
-  const int cidx = tp.x + le - 1;
-  const float4 cch = V.cm[cidx];  // L1 hit: just streamed
-  w.seen += tp.y + 1;
-  // swap / (p_agg * p_rr), p_agg = points(node) / points(a)
-  w.resid += (ks - w.cvn) * ((float)w.count_a * rcp_ftz((float)(tp.w - tp.z) * w.prr));
-  const float rc = fdist(cch, qx, qy, qz) * V.inv_diam[min(w.lvl + 1, kFastMaxLevels - 1)];
-  const float p = rr_fast_t<RR>(w.rp, rc);
-  if (!survive<RR>(p, w.kr, (uint64_t)(w.lvl - 1))) return false;  // counter = levels descended
-  ++w.steps;
-  w.cvn = fterm<KID>(cch, KID == KID_WINDING ? V.m12[cidx] : w0, qx, qy, qz, kp);
-  w.prr *= p;
-  w.rp = rc;
-  w.tp = V.topo[cidx];
-  ++w.lvl;
-  return true;
-}
-
-struct BktArgs {
-  unsigned int* fill;  // [n2] walks claimed per level-2 node; [n2] = tile counter
-  float4* rec;         // bucket storage: two float4 per walk
-  uint2* res;          // [seq * nq + t]: {residual bits, seen | steps << 16}
-  double* part;        // [t]: dense part + leaf subdomains
-  int* steps0;         // [t]: samples that passed the level-1 roulette
-  int64_t t0;          // first position of the slab
-  int nq;              // positions in the slab
-  unsigned int rec_cap;  // walks the storage holds
-};
-
-// shared layout common to the bucketed kernels, in units of the element size:
-// 16 B s_cm1[n1], s_tp1[n1], s_cm2[n2]; 8 B s_w1[n1], s_w2[n2] (winding), s_t2[n2];
-// 4 B s_b2[n2] begins, s_bb[n2] bucket bases, s_bc[n2] capacities (then counts)
-struct BktLayout {
-  int o_cm1, o_tp1, o_cm2, o_w1, o_w2, o_t2, o_b2, o_bb, o_bc, e4;
-};
-__host__ __device__ __forceinline__ BktLayout bkt_layout(int n1, int n2, bool wind) {
-  BktLayout L;
-  L.o_cm1 = 0;
-  L.o_tp1 = n1;
-  L.o_cm2 = 2 * n1;
-  L.o_w1 = 2 * (2 * n1 + n2);
-  L.o_w2 = L.o_w1 + (wind ? n1 : 0);
-  L.o_t2 = L.o_w2 + (wind ? n2 : 0);
-  L.o_b2 = 2 * (L.o_t2 + n2);
-  L.o_bb = L.o_b2 + n2;
-  L.o_bc = L.o_bb + n2;
-  L.e4 = L.o_bc + n2;
-  return L;
-}
-
-// exclusive prefix sum of sh_i[o_in .. o_in + n) into sh_i[o_out ..] (may alias
-// nothing else); returns the total.  Contains barriers: call block-uniformly.
-__device__ int block_exclusive_scan(int o_in, int o_out, int n, int tid, int nthreads) {
-  __shared__ int s_wtot[32];
-  const int per = (n + nthreads - 1) / nthreads, b0 = min(tid * per, n), b1 = min(b0 + per, n);
-  int seg = 0;
-  for (int b = b0; b < b1; ++b) seg += sh_i[o_in + b];
-  const int lane = tid & 31, wid = tid >> 5;
-  int incl = seg;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_wtot[wid] = incl;
-  __syncthreads();
-  int run = incl - seg, total = 0;
-  for (int w = 0; w < (nthreads >> 5); ++w) {
-    if (w < wid) run += s_wtot[w];
-    total += s_wtot[w];
-  }
-  for (int b = b0; b < b1; ++b) {
-    const int c = sh_i[o_in + b];
-    sh_i[o_out + b] = run;
-    run += c;
-  }
-  __syncthreads();
-  return total;
-}
-
-// bucket capacity of a level-2 node that expects mu samples
-__device__ __forceinline__ int bucket_cap(double mu) {
-  return (int)ceil(mu + 6.0 * sqrt(mu)) + 32;
-}
-// host bound on the sum of the capacities (sum mu <= nqS n1; Cauchy-Schwarz)
-inline int64_t bucket_total_bound(int64_t nqS, int n1, int n2) {
-  const double mu = (double)nqS * n1;
-  return (int64_t)(mu + 6.0 * std::sqrt((double)n2 * mu)) + 34ll * n2 + 64;
-}
-
-// every CTA derives the same bucket table from the staged level-1/2 topology:
-// capacities into s_bc, bases into s_bb (clamped to the storage)
-__device__ void stage_buckets(const BktLayout& L, int n1, int base2, int n2, double nqS,
-                              unsigned int rec_cap, int tid, int nthreads) {
-  for (int a = tid; a < n1; a += nthreads) {
-    const int4 tpa = sh_i4[L.o_tp1 + a];
-    if (tpa.y <= 0) continue;
-    const double ca = (double)(tpa.w - tpa.z);
-    const int k0 = tpa.x - base2;
-    for (int c = 0; c < tpa.y; ++c) {
-      const int2 t2 = sh_i2[L.o_t2 + k0 + c];
-      sh_i[L.o_bc + k0 + c] = t2.x != 0 ? bucket_cap(nqS * (double)t2.y / ca) : 0;
-    }
-  }
-  __syncthreads();
-  block_exclusive_scan(L.o_bc, L.o_bb, n2, tid, nthreads);
-  for (int k = tid; k < n2; k += nthreads) {
-    const int64_t b = sh_i[L.o_bb + k], e = b + sh_i[L.o_bc + k];
-    if (e > (int64_t)rec_cap) sh_i[L.o_bc + k] = (int)std::max<int64_t>(0, (int64_t)rec_cap - b);
-  }
-  __syncthreads();
-}
-
-// stages level 1 (root's children) and level 2 records + topology
-template <int KID>
-__device__ __forceinline__ void stage_levels12(const FastView& V, const BktLayout& L, int tid,
-                                               int nthreads) {
-  for (int i = tid; i < V.n1; i += nthreads) {
-    sh_f4[L.o_cm1 + i] = V.cm[1 + i];
-    sh_i4[L.o_tp1 + i] = V.topo[1 + i];
-    if (KID == KID_WINDING) sh_f2[L.o_w1 + i] = V.m12[1 + i];
-  }
-  for (int i = tid; i < V.n2; i += nthreads) {
-    sh_f4[L.o_cm2 + i] = V.cm[V.base2 + i];
-    if (KID == KID_WINDING) sh_f2[L.o_w2 + i] = V.m12[V.base2 + i];
-    sh_i[L.o_b2 + i] = V.lb[V.base2 + i];
-    const int4 tp = V.topo[V.base2 + i];
-    sh_i2[L.o_t2 + i] = make_int2(tp.y > 0 ? (tp.x | (tp.y << 25)) : 0, tp.w - tp.z);
-  }
-}
-
-template <int KID, int RR, bool PACK>
-__global__ void __launch_bounds__(kBktBlock, FSB_STO_MINB)
-    k_sto_bsample(const __grid_constant__ FastView V, const double* __restrict__ q,
-                  const int32_t* __restrict__ qperm, int S, uint64_t seed, int64_t qoff,
-                  KParams kp, BktArgs B) {
-  const int n1 = V.n1, n2 = V.n2, tid = threadIdx.x, lane = tid & 31;
-  const BktLayout L = bkt_layout(n1, n2, KID == KID_WINDING);
-  const int o_lut = 2 * L.e4;  // 2-B units
-  constexpr bool kPack = PACK && KID != KID_SMOOTH;
-  const int o_p2 = (2 * (o_lut + n1 * (kLut + 1)) + 15) / 16;
-#define s_cm1(i) sh_f4[L.o_cm1 + (i)]
-#define s_tp1(i) sh_i4[L.o_tp1 + (i)]
-#define s_cm2(i) sh_f4[L.o_cm2 + (i)]
-#define s_w1(i) sh_f2[L.o_w1 + (i)]
-#define s_w2(i) sh_f2[L.o_w2 + (i)]
-#define s_t2(i) sh_i2[L.o_t2 + (i)]
-#define s_b2(i) sh_i[L.o_b2 + (i)]
-#define s_bb(i) sh_i[L.o_bb + (i)]
-#define s_bc(i) sh_i[L.o_bc + (i)]
-#define s_lut(i) sh_u16[o_lut + (i)]
-  stage_levels12<KID>(V, L, tid, kBktBlock);
-  if (kPack) stage_pairs<KID>(V, n2, o_p2, tid, kBktBlock);
-  __syncthreads();
-  for (int i = tid; i < n1 * (kLut + 1); i += kBktBlock) {  // as k_sto_fast
-    const int a = i / (kLut + 1), b = i - a * (kLut + 1);
-    const int4 tpa = s_tp1(a);
-    int c = 0;
-    if (tpa.y > 0) {
-      int jb = tpa.z + (int)(((int64_t)b * (tpa.w - tpa.z)) >> kLutBits);
-      if (jb > tpa.w - 1) jb = tpa.w - 1;
-      const int k0 = tpa.x - V.base2;
-      c = child_search(L.o_b2, k0, tpa.y, jb) - k0;
-    }
-    s_lut(i) = (unsigned short)c;
-  }
-  stage_buckets(L, n1, V.base2, n2, (double)B.nq * S, B.rec_cap, tid, kBktBlock);
-
-  const uint64_t hseed = mix64(seed + kGamma);
-  const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
-  const float2 w0 = make_float2(0.f, 0.f);
-  __shared__ int s_tile;
-  const int ntiles = (B.nq + kBktBlock - 1) / kBktBlock;
-  while (true) {
-    if (tid == 0) s_tile = (int)atomicAdd(&B.fill[n2], 1u);
-    __syncthreads();
-    const int tile = s_tile;
-    if (tile >= ntiles) break;
-    const int tl = tile * kBktBlock + tid;  // position in the slab
-    const bool live = tl < B.nq;
-    const int64_t t = B.t0 + tl;
-    const int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
-    const float qx = live ? (float)q[3 * qi] : 0.f;
-    const float qy = live ? (float)q[3 * qi + 1] : 0.f;
-    const float qz = live ? (float)q[3 * qi + 2] : 0.f;
-    const uint64_t hq = key_fold(hseed, (uint64_t)(qi + qoff));
-
-    // ---- dense part (k_sto_fast's)
-    double acc = 0.0;
-    if (kPack) {
-      acc = dense_pairs<KID>(o_p2, (n2 + 1) / 2, qx, qy, qz, kp.dfloor_f);
-    } else {
-      int k = 0;
-      for (; k + 16 <= n2; k += 16) {
-        float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; u += 4) {
-          p0 += fterm<KID>(s_cm2(k + u), KID == KID_WINDING ? s_w2(k + u) : w0, qx, qy, qz, kp);
-          p1 += fterm<KID>(s_cm2(k + u + 1), KID == KID_WINDING ? s_w2(k + u + 1) : w0, qx, qy,
-                           qz, kp);
-          p2 += fterm<KID>(s_cm2(k + u + 2), KID == KID_WINDING ? s_w2(k + u + 2) : w0, qx, qy,
-                           qz, kp);
-          p3 += fterm<KID>(s_cm2(k + u + 3), KID == KID_WINDING ? s_w2(k + u + 3) : w0, qx, qy,
-                           qz, kp);
-        }
-        acc += (double)((p0 + p1) + (p2 + p3));
-      }
-      float p0 = 0.f;
-      for (; k < n2; ++k)
-        p0 += fterm<KID>(s_cm2(k), KID == KID_WINDING ? s_w2(k) : w0, qx, qy, qz, kp);
-      acc += (double)p0;
-    }
-    int steps = 0;  // samples past the level-1 roulette = creation index of the next walk
-
-    // one sample (a, s): index draw, level-1 step, roulette; a descending walk
-    // goes to its level-2 node's bucket
-    auto sample = [&](int a_ord, int sm, const int4& tpa, int k0, int lut0, float rp_a,
-                      uint64_t ha) {
-      const uint64_t hs = key_fold(ha, (uint64_t)sm);
-      const uint64_t ki = key_fold(hs, 0), kr = key_fold(hs, 1);
-      const uint64_t x = mix64(ki + kGamma);  // uniform_draw(ki, 0), _core.py:166-169
-      const double u0 = __ull2double_rn(x >> 11) * (1.0 / 9007199254740992.0);
-      int j = tpa.z + (int)__dmul_rn(u0, (double)(tpa.w - tpa.z));
-      if (j >= tpa.w) j = tpa.w - 1;
-      const int bkt = (int)(x >> (64 - kLutBits));
-      int c = s_lut(lut0 + bkt);
-      const int ce = s_lut(lut0 + bkt + 1);
-      while (c < ce && (s_b2(k0 + c + 1) & 0x7fffffff) <= j) ++c;
-      const int lo = k0 + c;
-      const float rc = fdist(s_cm2(lo), qx, qy, qz) * id2;
-      const float p = rr_fast_t<RR>(rp_a, rc);
-      const bool desc = live && survive<RR>(p, kr, 0);
-      const bool deep = desc && s_t2(lo).x != 0;
-      const int seq = steps;
-      if (desc) ++steps;
-      const unsigned dm = __ballot_sync(0xffffffffu, deep);
-      if (desc && !deep) B.res[(int64_t)seq * B.nq + tl] = make_uint2(0u, 0u);  // leaf: no walk
-      if (deep) {
-        const unsigned peers = __match_any_sync(dm, lo);
-        const int leader = __ffs(peers) - 1;
-        unsigned base = 0;
-        if (lane == leader) base = atomicAdd(&B.fill[lo], (unsigned)__popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        const unsigned pos = base + __popc(peers & ((1u << lane) - 1u));
-        if (pos < (unsigned)s_bc(lo)) {
-          float4* r = B.rec + 2 * ((size_t)s_bb(lo) + pos);
-          r[0] = make_float4(qx, qy, qz, __int_as_float(tl));
-          r[1] = make_float4(__uint_as_float((uint32_t)kr), __uint_as_float((uint32_t)(kr >> 32)),
-                             __int_as_float(j), __int_as_float(a_ord | (seq << 8)));
-        } else {  // bucket full: walk it here
-          Walk w;
-          w.qx = qx;
-          w.qy = qy;
-          w.qz = qz;
-          w.kr = kr;
-          w.jj = j;
-          walk_begin<KID, RR>(w, V, L.o_cm1, L.o_tp1, L.o_cm2, L.o_w2, L.o_t2, id1, id2, kp, a_ord,
-                              lo);
-          while (walk_level<KID, RR>(w, V, kp)) {
-          }
-          B.res[(int64_t)seq * B.nq + tl] =
-              make_uint2(__float_as_uint(w.resid), (unsigned)w.seen | ((unsigned)w.steps << 16));
-        }
-      }
-    };
-    auto leaf_term = [&](int a_ord, const int4& tpa) {
-      return (double)((tpa.w - tpa.z > 1)
-                          ? leaf_exact<KID>(V, tpa.z, tpa.w, qx, qy, qz, kp)
-                          : fterm<KID>(s_cm1(a_ord), KID == KID_WINDING ? s_w1(a_ord) : w0, qx,
-                                       qy, qz, kp));
-    };
-    for (int a_ord = 0; a_ord < n1; ++a_ord) {  // block-uniform
-      const int4 tpa = s_tp1(a_ord);
-      if (tpa.y == 0) {  // leaf subdomain: exact term, never sampled
-        acc += leaf_term(a_ord, tpa);
-        continue;
-      }
-      const int k0 = tpa.x - V.base2, lut0 = a_ord * (kLut + 1);
-      const float rp_a = fdist(s_cm1(a_ord), qx, qy, qz) * id1;
-      const uint64_t ha = key_fold(hq, (uint64_t)a_ord);
-      for (int s = 0; s < S; ++s) sample(a_ord, s, tpa, k0, lut0, rp_a, ha);
-    }
-    if (live) {
-      B.part[tl] = acc;
-      B.steps0[tl] = steps;
-    }
-    __syncthreads();
-  }
-#undef s_cm1
-#undef s_tp1
-#undef s_cm2
-#undef s_w1
-#undef s_w2
-#undef s_t2
-#undef s_b2
-#undef s_bb
-#undef s_bc
-#undef s_lut
-}
-
-template <int KID, int RR>
-__global__ void __launch_bounds__(kBktBlock, FSB_BWALK_MINB)
-    k_sto_bwalk(const __grid_constant__ FastView V, int S, KParams kp, BktArgs B) {
-  const int n1 = V.n1, n2 = V.n2, tid = threadIdx.x, lane = tid & 31;
-  const BktLayout L = bkt_layout(n1, n2, KID == KID_WINDING);
-  const int o_pref = L.e4;  // 4-B units: n2 + 1 bucket-major prefix of the walk counts
-  stage_levels12<KID>(V, L, tid, kBktBlock);
-  __syncthreads();
-  stage_buckets(L, n1, V.base2, n2, (double)B.nq * S, B.rec_cap, tid, kBktBlock);
-  for (int k = tid; k < n2; k += kBktBlock)
-    sh_i[L.o_bc + k] = min((int)__ldcg(&B.fill[k]), sh_i[L.o_bc + k]);
-  __syncthreads();
-  const int total = block_exclusive_scan(L.o_bc, o_pref, n2, tid, kBktBlock);
-  if (tid == 0) sh_i[o_pref + n2] = total;
-  // this CTA's contiguous share of the bucket-major walk list
-  const int r0 = (int)((int64_t)total * blockIdx.x / gridDim.x);
-  const int r1 = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
-  __shared__ int s_head;
-  if (tid == 0) s_head = 0;
-  __syncthreads();
-  int kcur = 0;  // first bucket with prefix(k + 1) > r0
-  for (int hi = n2; kcur < hi;) {
-    const int mid = (kcur + hi) >> 1;
-    if (sh_i[o_pref + mid + 1] <= r0)
-      kcur = mid + 1;
-    else
-      hi = mid;
-  }
-  const float id1 = V.inv_diam[1], id2 = V.inv_diam[2];
-  Walk w;
-  bool act = false;
-  int owner = 0, seq = 0;
-  while (true) {
-    const unsigned need = __ballot_sync(0xffffffffu, !act);
-    if (need) {
-      int head = 0;
-      if (lane == 0) head = atomicAdd(&s_head, __popc(need));
-      head = __shfl_sync(0xffffffffu, head, 0);
-      const int idx = r0 + head + __popc(need & ((1u << lane) - 1u));
-      if (!act && idx < r1) {
-        while (sh_i[o_pref + kcur + 1] <= idx) ++kcur;
-        float4 a, b;
-        ld_pair(B.rec + 2 * ((size_t)sh_i[L.o_bb + kcur] + (idx - sh_i[o_pref + kcur])), a, b);
-        w.qx = a.x;
-        w.qy = a.y;
-        w.qz = a.z;
-        owner = __float_as_int(a.w);
-        w.kr = ((uint64_t)__float_as_uint(b.y) << 32) | __float_as_uint(b.x);
-        w.jj = __float_as_int(b.z);
-        const unsigned am = __float_as_uint(b.w);
-        seq = (int)(am >> 8);
-        walk_begin<KID, RR>(w, V, L.o_cm1, L.o_tp1, L.o_cm2, L.o_w2, L.o_t2, id1, id2, kp,
-                            (int)(am & 0xff), kcur);
-        act = true;
-      }
-    }
-    if (!__any_sync(0xffffffffu, act)) break;
-    if (!act) continue;
-    if (!walk_level<KID, RR>(w, V, kp)) {
-      B.res[(int64_t)seq * B.nq + owner] =
-          make_uint2(__float_as_uint(w.resid), (unsigned)w.seen | ((unsigned)w.steps << 16));
-      act = false;
-    }
-  }
-}
-
-// every query folds its walks' residuals in creation ((a, s)) order
-__global__ void k_sto_bfold(const int4* __restrict__ topo, int n1, const int32_t* __restrict__ qperm,
-                            int S, BktArgs B, float* __restrict__ out,
-                            int64_t* __restrict__ visited, int64_t* __restrict__ path_steps,
-                            int64_t* __restrict__ path_count) {
-  __shared__ int s_base[2];
-  if (threadIdx.x == 0) {  // query-independent counters (as k_sto_fast)
-    int sb = n1, ni = 0;
-    for (int a = 0; a < n1; ++a) {
-      const int4 tpa = topo[1 + a];
-      if (tpa.y > 0) {
-        sb += S * (tpa.y + 1);
-        ++ni;
-      }
-    }
-    s_base[0] = sb;
-    s_base[1] = ni;
-  }
-  __syncthreads();
-  const int tl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (tl >= B.nq) return;
-  const int st = B.steps0[tl];
-  double deep = 0.0;
-  int seen = s_base[0], steps = st;
-  for (int k2 = 0; k2 < st; ++k2) {
-    const uint2 r = __ldcs(&B.res[(int64_t)k2 * B.nq + tl]);
-    deep += (double)__uint_as_float(r.x);
-    seen += (int)(r.y & 0xffffu);
-    steps += (int)(r.y >> 16);
-  }
-  const double total = B.part[tl] + deep / (double)S;
-  const int64_t t = B.t0 + tl;
-  const int64_t qi = qperm ? (int64_t)qperm[t] : t;
-  out[qi] = (float)total;
-  if (visited) visited[qi] = seen;
-  if (path_steps) path_steps[qi] = steps;
-  if (path_count) path_count[qi] = (int64_t)S * s_base[1];
-}
-
 // ================================================ warp-shared streams (paper)
 // The paper's GPU recipe: the 32 queries of a warp, taken
 // in a seeded shuffled order, share the index and roulette streams (key = the
@@ -1853,76 +1335,6 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     }
     if (rc == 0) *used = true;
     return rc;
-  }
-  // per-query streams, opt-in (FSB_STO_BUCKET=1): the bucketed path (sampling -> level-2
-  // buckets -> walks -> fold); bitwise equal to k_sto_fast, measured slower on C4
-  // (1.29 vs 1.03 ms: the sampling kernel stalls on the bucket atomics)
-  const BktLayout BL = bkt_layout(V.n1, V.n2, wind);
-  const size_t bsmem_a = 16 * (size_t)((2 * (2 * BL.e4 + V.n1 * (kLut + 1)) + 15) / 16) +
-                         (pack_fast ? pairs_bytes : 0);
-  const size_t bsmem_b = 4 * ((size_t)BL.e4 + V.n2 + 1);
-  if (share == 0 && V.first_multi > 2 && V.n1 <= 255 && nslot < (1 << 24) &&
-      bsmem_a <= kSmemMax && bsmem_b <= kSmemMax && std::getenv("FSB_STO_BUCKET")) {
-    const int64_t per = std::max<int64_t>(kBktBlock, (int64_t)FSB_BKT_SAMPLES / nslot);
-    const int nq_max = (int)std::min<int64_t>(n, per);
-    const int64_t cap = bucket_total_bound((int64_t)nq_max * n_samples, V.n1, V.n2);
-    if (cap < (1ll << 31)) {
-      Scratch fill, rec, res, part, st0;
-      FS_TRY(fill.alloc(sizeof(unsigned int) * (V.n2 + 1), s));
-      FS_TRY(rec.alloc(32 * (size_t)cap, s));
-      FS_TRY(res.alloc(8 * (size_t)nq_max * nslot, s));
-      FS_TRY(part.alloc(8 * (size_t)nq_max, s));
-      FS_TRY(st0.alloc(4 * (size_t)nq_max, s));
-      BktArgs BA;
-      BA.fill = fill.as<unsigned int>();
-      BA.rec = rec.as<float4>();
-      BA.res = res.as<uint2>();
-      BA.part = part.as<double>();
-      BA.steps0 = st0.as<int>();
-      BA.rec_cap = (unsigned int)cap;
-      auto run = [&](auto ka, auto kb) -> int {
-        if (bsmem_a > 48 * 1024)
-          FS_CK(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem_a));
-        if (bsmem_b > 48 * 1024)
-          FS_CK(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem_b));
-        int occ_a = 1, occ_b = 1;
-        FS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, ka, kBktBlock, bsmem_a));
-        FS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, kb, kBktBlock, bsmem_b));
-        for (int64_t t0 = 0; t0 < n; t0 += nq_max) {
-          BA.t0 = t0;
-          BA.nq = (int)std::min<int64_t>(nq_max, n - t0);
-          FS_CK(cudaMemsetAsync(BA.fill, 0, sizeof(unsigned int) * (V.n2 + 1), s));
-          const int64_t tiles = (BA.nq + kBktBlock - 1) / kBktBlock;
-          const int64_t ga = std::min<int64_t>(tiles, (int64_t)sms * std::max(occ_a, 1));
-          ka<<<(unsigned)ga, kBktBlock, bsmem_a, s>>>(V, q, qperm, n_samples, seed, qoff, kp, BA);
-          FS_CK(cudaGetLastError());
-          kb<<<(unsigned)(sms * std::max(occ_b, 1)), kBktBlock, bsmem_b, s>>>(V, n_samples, kp, BA);
-          FS_CK(cudaGetLastError());
-          k_sto_bfold<<<grid_for(BA.nq, 256), 256, 0, s>>>(V.topo, V.n1, qperm, n_samples, BA,
-                                                          out, visited, path_steps, path_count);
-          FS_CK(cudaGetLastError());
-        }
-        return 0;
-      };
-#define FSB_BKT(K, R)                                                                      \
-  (pack_fast ? run(k_sto_bsample<K, R, true>, k_sto_bwalk<K, R>)                         \
-             : run(k_sto_bsample<K, R, false>, k_sto_bwalk<K, R>))
-      switch (kid * 3 + rr_mode) {
-        case 0: rc = FSB_BKT(0, 0); break;
-        case 1: rc = FSB_BKT(0, 1); break;
-        case 2: rc = FSB_BKT(0, 2); break;
-        case 3: rc = run(k_sto_bsample<1, 0, false>, k_sto_bwalk<1, 0>); break;
-        case 4: rc = run(k_sto_bsample<1, 1, false>, k_sto_bwalk<1, 1>); break;
-        case 5: rc = run(k_sto_bsample<1, 2, false>, k_sto_bwalk<1, 2>); break;
-        case 6: rc = run(k_sto_bsample<2, 0, false>, k_sto_bwalk<2, 0>); break;
-        case 7: rc = run(k_sto_bsample<2, 1, false>, k_sto_bwalk<2, 1>); break;
-        case 8: rc = run(k_sto_bsample<2, 2, false>, k_sto_bwalk<2, 2>); break;
-        default: set_error("unknown kernel id"); return 1;
-      }
-#undef FSB_BKT
-      if (rc == 0) *used = true;
-      return rc;
-    }
   }
   switch (kid * 3 + rr_mode) {
     case 0: rc = pack_fast ? launch(k_sto_fast<0, 0, true>) : launch(k_sto_fast<0, 0, false>); break;
