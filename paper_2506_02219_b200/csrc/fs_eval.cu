@@ -286,32 +286,33 @@ __device__ __forceinline__ double sample_residual(const LoTree<KID, F64>& T, int
       ++lvl;
     }
     return resid;
+  } else {  // the reference walk (_core.py:177-211)
+    while (tp.y > 0) {
+      int child = T.pick_child(tp, j, pj, lvl);
+      double delta;
+      if (node == a)
+        delta = delta_a;
+      else
+        delta = F64 ? __dsub_rn(T.children_sum(tp, qx, qy, qz, kp), T.agg_term(node, qx, qy, qz, kp))
+                    : T.children_sum(tp, qx, qy, qz, kp) - T.agg_term(node, qx, qy, qz, kp);
+      seen += tp.y;
+      double pagg = __ddiv_rn((double)(tp.w - tp.z), (double)count_a);
+      resid = __dadd_rn(resid, __ddiv_rn(delta, __dmul_rn(pagg, prr)));
+      double rp = ffr<F64>(T.geo[node], qx, qy, qz);
+      double rc = ffr<F64>(T.geo[child], qx, qy, qz);
+      double p = rr_probability(rp, rc, rr_mode);
+      double u = uniform_draw(key_r, rctr);
+      ++rctr;
+      ++seen;
+      if (u >= p) break;
+      prr = __dmul_rn(prr, p);
+      node = child;
+      tp = T.topo[node];
+      ++steps;
+      ++lvl;
+    }
+    return resid;
   }
-  while (tp.y > 0) {
-    int child = T.pick_child(tp, j, pj, lvl);
-    double delta;
-    if (node == a)
-      delta = delta_a;
-    else
-      delta = F64 ? __dsub_rn(T.children_sum(tp, qx, qy, qz, kp), T.agg_term(node, qx, qy, qz, kp))
-                  : T.children_sum(tp, qx, qy, qz, kp) - T.agg_term(node, qx, qy, qz, kp);
-    seen += tp.y;
-    double pagg = __ddiv_rn((double)(tp.w - tp.z), (double)count_a);
-    resid = __dadd_rn(resid, __ddiv_rn(delta, __dmul_rn(pagg, prr)));
-    double rp = ffr<F64>(T.geo[node], qx, qy, qz);
-    double rc = ffr<F64>(T.geo[child], qx, qy, qz);
-    double p = rr_probability(rp, rc, rr_mode);
-    double u = uniform_draw(key_r, rctr);
-    ++rctr;
-    ++seen;
-    if (u >= p) break;
-    prr = __dmul_rn(prr, p);
-    node = child;
-    tp = T.topo[node];
-    ++steps;
-    ++lvl;
-  }
-  return resid;
 }
 
 // stochastic_batch, _core.py:215-267
