@@ -464,6 +464,21 @@ __global__ void k_pack_cm64(const int32_t* __restrict__ lo2pre, const double* __
   if (m12) m12[r] = make_double2(am[(int64_t)c * i + 1], am[(int64_t)c * i + 2]);
 }
 
+// operand ranges of the FP64 division fast path (contrib_parity_fast): bit 0 set
+// when a node coordinate exceeds 2^100 in magnitude (or is not finite), bit 1
+// when a node's first mass channel is outside [2^-800, 2^800] (or zero / NaN)
+__global__ void k_div_range(const double4* __restrict__ cm, int64_t n, unsigned int* flags) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned int f = 0;
+  if (r < n) {
+    const double4 c = cm[r];
+    if (!(fabs(c.x) <= 0x1p100 && fabs(c.y) <= 0x1p100 && fabs(c.z) <= 0x1p100)) f |= 1u;
+    if (!(fabs(c.w) >= 0x1p-800 && fabs(c.w) <= 0x1p800)) f |= 2u;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
 int ensure_cm64(FsTree* t, cudaStream_t s) {
   std::lock_guard<std::recursive_mutex> lk(t->mu);
   if (t->lo_cm64) return 0;
@@ -473,7 +488,15 @@ int ensure_cm64(FsTree* t, cudaStream_t s) {
   if (t->c >= 3) FS_TRY(dalloc(&m12, t->n, s));
   k_pack_cm64<<<grid_for(t->n, 256), 256, 0, s>>>(t->lo2pre, t->com, t->agg_mass, t->n, t->c, cm,
                                                   m12);
+  Scratch fl;
+  FS_TRY(fl.alloc(sizeof(unsigned int), s));
+  FS_CK(cudaMemsetAsync(fl.p, 0, sizeof(unsigned int), s));
+  k_div_range<<<grid_for(t->n, 256), 256, 0, s>>>(cm, t->n, fl.as<unsigned int>());
+  unsigned int flags = 3;
+  FS_CK(cudaMemcpyAsync(&flags, fl.p, sizeof(flags), cudaMemcpyDeviceToHost, s));
   FS_CK(cudaStreamSynchronize(s));
+  t->coords_in_range = (flags & 1u) == 0;
+  t->masses_in_range = (flags & 2u) == 0;
   t->lo_m12_64 = m12;
   t->lo_cm64 = cm;
   FS_CK(cudaGetLastError());

@@ -63,6 +63,7 @@ struct View64 {
   int path_bits, path_levels;
   int n1, base2, n2, first_multi;
   int qcap;
+  bool div_safe;  // masses / coordinates / floor in range: no division range test
   double diam[kMaxLevels64];  // cell diameter per level (exact)
 };
 
@@ -77,7 +78,7 @@ __device__ __forceinline__ double term64(const double4& c, const double2& w, dou
 // of four evaluated through the branch-free division / square root (bitwise
 // the intrinsics'; the rare out-of-range operand is recomputed with them), so
 // four terms are in flight per thread
-template <int KID, class Rec>
+template <int KID, bool CHK, class Rec>
 __device__ __forceinline__ double terms_sum64(double ks, int c, int ce, Rec rec, double qx,
                                               double qy, double qz, const KParams& kp) {
   auto slow = [&](int i) {
@@ -91,7 +92,7 @@ __device__ __forceinline__ double terms_sum64(double ks, int c, int ce, Rec rec,
       double4 cm;
       double2 w;
       rec(i, cm, w);
-      return contrib_parity_fast<KID>(cm.w, w.x, w.y, cm.x, cm.y, cm.z, qx, qy, qz, kp, ok);
+      return contrib_parity_fast<KID, CHK>(cm.w, w.x, w.y, cm.x, cm.y, cm.z, qx, qy, qz, kp, ok);
     };
     for (; c + 4 <= ce; c += 4) {
       bool o0, o1, o2, o3;
@@ -201,6 +202,12 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
       qz = q[3 * qi + 2];
     }
     s_q[tid] = make_double4(qx, qy, qz, 0.0);
+    // the division range test can be dropped when every query of the tile is
+    // bounded (|q| <= 2^100) on a div_safe tree (contrib_parity_fast)
+    const bool tile_safe =
+        __syncthreads_and(V.div_safe &&
+                          (!live || (fabs(qx) <= 0x1p100 && fabs(qy) <= 0x1p100 &&
+                                     fabs(qz) <= 0x1p100)));
     const uint64_t hq =
         key_fold(hseed, share ? (uint64_t)((t + qoff) >> share) : (uint64_t)(qi + qoff));
     int seen = 0, steps = 0;
@@ -217,7 +224,7 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
       const int f1 = min(f0 + rmax, nflat);
       if (live) {
         for (int f = f0; f < f1; ++f) {
-          const int a_ord = f / S, sm = f - a_ord * S;
+          const int a_ord = S == 1 ? f : f / S, sm = f - a_ord * S;
           if (a_ord != a_cur) {  // a new subdomain: dense part (_core.py:237-250)
             a_cur = a_ord;
             ++seen;
@@ -236,13 +243,12 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
             double ks = 0.0;  // _children_term_sum over the level-2 children
             const int c0 = tpa.x - 1, ce = c0 + tpa.y;
             if (!multi12) {
-              ks = terms_sum64<KID>(
-                  ks, c0, ce,
-                  [&](int i, double4& cm, double2& w) {
-                    cm = s_cm[i];
-                    w = KID == KID_WINDING ? s_w[i] : w0;
-                  },
-                  qx, qy, qz, kp);
+              auto rec = [&](int i, double4& cm, double2& w) {
+                cm = s_cm[i];
+                w = KID == KID_WINDING ? s_w[i] : w0;
+              };
+              ks = tile_safe ? terms_sum64<KID, false>(ks, c0, ce, rec, qx, qy, qz, kp)
+                             : terms_sum64<KID, true>(ks, c0, ce, rec, qx, qy, qz, kp);
             } else {
               for (int c = c0; c < ce; ++c) {
                 double v;
@@ -276,8 +282,9 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
               hi = mid;
           }
           seen += tpa.y;
-          const double pagg = __ddiv_rn((double)count_a, (double)count_a);
-          const double resid = __dadd_rn(0.0, __ddiv_rn(delta_a, __dmul_rn(pagg, 1.0)));
+          // _core.py:196-200 at node == a: p_agg = count_a / count_a = 1 and p_rr = 1,
+          // so delta / (p_agg * p_rr) = delta exactly
+          const double resid = __dadd_rn(0.0, delta_a);
           const double rc = ffr64(s_cm[lo], d2, qx, qy, qz);
           const double p = rr_probability(rp_a, rc, RR);
           const double u = uniform_draw(kr, 0);
@@ -364,13 +371,12 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
             const bool cmulti = lvl + 1 >= V.first_multi;
             double ks = 0.0;
             if (!cmulti) {
-              ks = terms_sum64<KID>(
-                  ks, tp.x, tp.x + tp.y,
-                  [&](int i, double4& cm, double2& w) {
-                    cm = V.cm[i];
-                    w = KID == KID_WINDING ? V.m12[i] : w0;
-                  },
-                  wx, wy, wz, kp);
+              auto rec = [&](int i, double4& cm, double2& w) {
+                cm = V.cm[i];
+                w = KID == KID_WINDING ? V.m12[i] : w0;
+              };
+              ks = tile_safe ? terms_sum64<KID, false>(ks, tp.x, tp.x + tp.y, rec, wx, wy, wz, kp)
+                             : terms_sum64<KID, true>(ks, tp.x, tp.x + tp.y, rec, wx, wy, wz, kp);
             } else {
               for (int c = tp.x; c < tp.x + tp.y; ++c) {
                 double v;
@@ -442,7 +448,7 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
               acc = __dadd_rn(acc, v[k]);
             } else {
               ++n_int;
-              acc = __dadd_rn(acc, __dadd_rn(v[k], __ddiv_rn(__dadd_rn(0.0, r[k]), 1.0)));
+              acc = __dadd_rn(acc, __dadd_rn(v[k], __dadd_rn(0.0, r[k])));  // fa / S, S = 1
             }
           }
         }
@@ -507,6 +513,13 @@ int stochastic64(FsTree* t, int kid, double alpha, double dfloor, const double* 
   V.base2 = (int)t->level_off[2];
   V.n2 = (int)(t->level_off[3] - t->level_off[2]);
   V.first_multi = t->first_multi_level;
+  // the division's range test is provably true when |coordinates| <= 2^100 (so
+  // r <= 2^102), dfloor in [2^-100, 2^100] and, for Coulomb (-m0 / r), |m0| in
+  // [2^-800, 2^800]: every quotient is a normal number and every operand finite
+  // (winding divides the constant 1 / (4 pi) by r^3)
+  V.div_safe = t->coords_in_range && (kid != KID_COULOMB || t->masses_in_range) &&
+               dfloor >= 0x1p-100 && dfloor <= 0x1p100 &&
+               !std::getenv("FSB_S64_DIVCHECK");
   for (int l = 0; l < kMaxLevels64; ++l) V.diam[l] = l < t->num_levels ? t->level_diam64[l] : 1.0;
   if (V.base2 != 1 + V.n1) return decline("level layout");
   const int64_t nflat = (int64_t)V.n1 * n_samples;

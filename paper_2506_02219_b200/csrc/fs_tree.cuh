@@ -63,6 +63,9 @@ struct FsTree {
   double level_diam64[kMaxLevels];  // the same, exact (FP64 queue kernel's _ffr)
   // FP64 queue kernel (ensure_cm64): {cx, cy, cz, m0} and {m1, m2} per level-order node
   double4* lo_cm64 = nullptr;
+  // operand ranges of the FP64 division fast path (ensure_cm64): node coordinates
+  // within 2^100, first mass channel within [2^-800, 2^800]
+  bool coords_in_range = false, masses_in_range = false;
   double2* lo_m12_64 = nullptr;
   float4* lo_cm32 = nullptr;     // {cx, cy, cz, m0} per level-order node
   float2* lo_m12_32 = nullptr;   // {m1, m2} (winding)
