@@ -721,14 +721,15 @@ def run_ours(args):
         for name, cfg in (("stochastic_s1", fs.EstimatorConfig("stochastic", seed=1)),
                           ("barnes_hut_beta2", fs.EstimatorConfig("barnes_hut", beta=2.0))):
             tr = tree4 if name.startswith("sto") else tree2
-            evaluate_field_device(cfg, src, kern, q_dev, tr)
+            for _ in range(3):  # first calls pack the FP64 records and grow the memory pool
+                evaluate_field_device(cfg, src, kern, q_dev, tr)
             torch.cuda.synchronize()
             ev_a.record()
-            for _ in range(3):
+            for _ in range(5):
                 r64 = evaluate_field_device(cfg, src, kern, q_dev, tr)
             ev_b.record()
             torch.cuda.synchronize()
-            ms = ev_a.elapsed_time(ev_b) / 3
+            ms = ev_a.elapsed_time(ev_b) / 5
             f64[name] = {"ms_per_step": ms, "value": n / (ms * 1e-3),
                          "median_rel_err": median_rel(r64.values.cpu().numpy(), truth_h)}
         f64["note"] = ("precision='f64' (the reference's default): k_sto64 (FP64 queue kernel) and "
@@ -773,8 +774,8 @@ def run_ours(args):
             "kernel": f"{kname}<coulomb, paper_ratio> (FP32)", "kernel_ms": kern_ms,
             "work": (f"{inter_q:.1f} interactions/query = {n2} dense level-2 records + "
                      f"{walk_inter:.1f} walk children; 10 flops each"),
-            "peak_source": ("measured on this GPU in this run: fsb_micro_peaks (csrc/fs_micro.cu, "
-                            "tools/micro/peaks.py) -- Coulomb node terms/s of the packed-FP32 + "
+            "peak_source": ("measured on this GPU in this run: fsb_micro_peaks (csrc/fs_micro.cu) "
+                            "-- Coulomb node terms/s of the packed-FP32 + "
                             "MUFU.RSQ loop with all operands on chip, x 10 flops (MEASURED_PEAKS."
                             "json has no FP32/MUFU entry)"),
             "measured_mufu_rsq_per_s": float(mp[0]),

@@ -8,8 +8,7 @@
 //       one MUFU.RSQ per term) over a shared-memory tile with 16 queries per
 //       thread -- every operand on chip, so nothing but the FP32/MUFU pipes and
 //       issue bound it.
-// tools/micro/peaks.cu is the stand-alone copy; bench.py calls fsb_micro_peaks
-// on the bench's own GPU and clocks.
+// bench.py calls fsb_micro_peaks on the bench's own GPU and clocks.
 #include <cstdio>
 
 #include "../../include/fastsum_b200.h"
