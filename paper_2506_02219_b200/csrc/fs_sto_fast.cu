@@ -59,6 +59,7 @@ struct FastView {
   int n1, base2, n2, first_multi;
   int per_chunk;                   // (a, s) samples per thread between drains
   int qcap;                        // queued walk starts per block
+  int kid_pairs;                   // (warp kernel) staged child pairs per warp: max over nodes
   float inv_diam[kFastMaxLevels];  // 1 / max(diam_level, 1e-12)
 };
 
@@ -835,6 +836,62 @@ __device__ unsigned long long g_warp_stats[8];
 #define FSB_WARP_MINB 4
 #endif
 
+#ifndef FSB_WARP_STAGE_KIDS
+#define FSB_WARP_STAGE_KIDS 1  // stage a walk level's child pairs in shared memory
+#endif
+
+// The children [first, first + count) of a walk-level node as the global pair
+// records covering them (pairs p0 .. p0 + np - 1 of ensure_pairs' table), loaded
+// by the warp's lanes at once (one 32-byte load per lane) into the warp's
+// shared buffer -- one L2 round trip per level instead of one per two pair
+// loads -- with the masses of the halves outside the range zeroed.  Returns np.
+__device__ __forceinline__ int stage_kid_pairs(float4* __restrict__ buf,
+                                               const float4* __restrict__ cmp, int first,
+                                               int count, int lane) {
+  const int p0 = first >> 1, np = ((first + count - 1) >> 1) - p0 + 1;
+  __syncwarp();  // the previous level's readers are done
+  for (int k = lane; k < np; k += 32) {
+    float4 A, B;
+    ld_pair(cmp + 2 * (p0 + k), A, B);
+    if (k == 0 && (first & 1)) B.z = 0.f;                     // record first - 1
+    if (k == np - 1 && ((first + count) & 1)) B.w = 0.f;      // record first + count
+    buf[2 * k] = A;
+    buf[2 * k + 1] = B;
+  }
+  __syncwarp();
+  return np;
+}
+// Coulomb sum over the staged pairs (broadcast LDS), packed FP32, the floor as
+// r2 + floor^2 (children_coulomb_pairs' arithmetic per pair)
+__device__ __forceinline__ float staged_kid_sum(const float4* __restrict__ buf, int np, float qx,
+                                                float qy, float qz, float dfloor) {
+  const float2 nx = make_float2(-qx, -qx), ny = make_float2(-qy, -qy), nz = make_float2(-qz, -qz);
+  const float f2 = dfloor * dfloor;
+  const float2 fl2 = make_float2(f2, f2);
+  auto pair_acc = [&](int k, float2 acc2) {
+    const float4 A = buf[2 * k], B = buf[2 * k + 1];
+    const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nx);
+    const float2 dy = __fadd2_rn(make_float2(A.z, A.w), ny);
+    const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nz);
+    const float2 r2 = __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __ffma2_rn(dz, dz, fl2)));
+    const float2 ri = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+    return __ffma2_rn(make_float2(B.z, B.w), ri, acc2);
+  };
+  float2 a2 = make_float2(0.f, 0.f), b2 = a2;
+  int k = 0;
+  for (; k + 1 < np; k += 2) {
+    a2 = pair_acc(k, a2);
+    b2 = pair_acc(k + 1, b2);
+  }
+  if (k < np) a2 = pair_acc(k, a2);
+  return (a2.x + a2.y) + (b2.x + b2.y);
+}
+// {cx, cy, cz, m0} of the staged record at offset i from pair p0's first record
+__device__ __forceinline__ float4 staged_kid(const float4* __restrict__ buf, int i) {
+  const float4 A = buf[2 * (i >> 1)], B = buf[2 * (i >> 1) + 1];
+  return (i & 1) ? make_float4(A.y, A.w, B.y, -B.w) : make_float4(A.x, A.z, B.x, -B.z);
+}
+
 template <int KID, int RR, bool PACK>
 __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
     k_sto_warp(const __grid_constant__ FastView V, const double* __restrict__ q, int64_t n,
@@ -848,6 +905,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   const int n1 = V.n1, n2 = V.n2;
   // Coulomb: level-2 records also as packed pairs {x0,x1,y0,y1}, {z0,z1,-m0,-m1}
   constexpr bool kPack = KID == KID_COULOMB && FSB_WARP_DENSE2;  // packed walk levels
+  constexpr bool kStageKids = kPack && FSB_WARP_STAGE_KIDS;
   constexpr bool pack = PACK && KID != KID_SMOOTH;                // packed dense part
   const int np2 = pack ? (n2 + 1) / 2 : 0;
   const int o_cm1 = 0, o_tp1 = n1, o_cm2 = 2 * n1, o_p2 = 2 * n1 + n2;
@@ -872,6 +930,9 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   const int o_smp = (o_leaf + n1 + 7) / 8;
   const int tid = threadIdx.x, lane = tid & 31;
   int4* const s_smp = reinterpret_cast<int4*>(sh_i4 + o_smp) + (tid >> 5) * 96;
+  // per-warp staging of a walk level's child pairs (Coulomb): 2 float4 per pair
+  float4* const s_kid =
+      sh_f4 + o_smp + (kWarpBlock / 32) * 96 + (tid >> 5) * 2 * (kStageKids ? V.kid_pairs : 0);
   for (int i = tid; i < n1; i += kWarpBlock) {
     s_cm1(i) = V.cm[1 + i];
     s_tp1(i) = V.topo[1 + i];
@@ -1086,7 +1147,12 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             le = 1 + (int)((path >> (V.path_bits * lvl)) & ((1u << V.path_bits) - 1u));
             tpn = V.topo[tp.x + le - 1];
           }
-          if (kPack && use_path) {
+          float4 cch;
+          if (kStageKids && use_path) {
+            const int np = stage_kid_pairs(s_kid, V.cmp, tp.x, tp.y, lane);
+            ks0 = staged_kid_sum(s_kid, np, qx, qy, qz, kp.dfloor_f);
+            cch = staged_kid(s_kid, (tp.x & 1) + le - 1);  // the picked child, staged
+          } else if (kPack && use_path) {
             ks0 = children_coulomb_pairs(V.cmp, V.cm, tp.x, tp.y, qx, qy, qz, kp);
           } else if (use_path) {
             if (tp.x & 1) {
@@ -1125,7 +1191,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             }
           }
           const int cidx = tp.x + le - 1;
-          const float4 cch = V.cm[cidx];  // one of the children just summed: L1 hit
+          if (!(kStageKids && use_path)) cch = V.cm[cidx];  // one of the children just summed
           if (!use_path) tpn = V.topo[cidx];
           if (alive) {  // swap / (p_agg * p_rr), p_agg = points(node) / points(a)
             seen += tp.y + 1;
@@ -1202,6 +1268,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   if (t->max_children >= 128 || t->n >= (1ll << 25)) return 0;
   V.path = t->pt_path;
   V.cmp = nullptr;
+  V.kid_pairs = t->max_children / 2 + 2;
   V.path_bits = t->path_bits;
   V.path_levels = t->path_levels;
   V.n1 = t->root_kids;
@@ -1243,7 +1310,10 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
     return ((16 * (2 * n1 + n2 + (pk ? pvec * ((n2 + 1) / 2) : 0)) +
              8 * ((wind ? n1 + n2 : 0) + n2) + 4 * n2 + 2 * n1 * (kLut + 3) + 128) &
             ~(size_t)127) +
-           (size_t)(kWarpBlock / 32) * 96 * 16;
+           (size_t)(kWarpBlock / 32) * 96 * 16 +
+           (kid == KID_COULOMB && FSB_WARP_DENSE2 && FSB_WARP_STAGE_KIDS
+                ? (size_t)(kWarpBlock / 32) * 32 * V.kid_pairs
+                : 0);
   };
   const bool pack_warp = can_pack && warp_smem(true) <= kSmemMax &&
                          fit(warp_smem(true), FSB_WARP_MINB) >= fit(warp_smem(false), FSB_WARP_MINB);
