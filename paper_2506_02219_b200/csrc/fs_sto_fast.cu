@@ -59,7 +59,7 @@ struct FastView {
   int n1, base2, n2, first_multi;
   int per_chunk;                   // (a, s) samples per thread between drains
   int qcap;                        // queued walk starts per block
-  int kid_pairs;                   // (warp kernel) staged child pairs per warp: max over nodes
+  int stage_kids;                  // (warp kernel) every node has <= 64 children: stage them
   float inv_diam[kFastMaxLevels];  // 1 / max(diam_level, 1e-12)
 };
 
@@ -839,6 +839,7 @@ __device__ unsigned long long g_warp_stats[8];
 #ifndef FSB_WARP_STAGE_KIDS
 #define FSB_WARP_STAGE_KIDS 1  // stage a walk level's child pairs in shared memory
 #endif
+constexpr int kKidPairs = 33;  // staged pairs per warp: up to 64 children (d <= 4)
 
 // The children [first, first + count) of a walk-level node as the global pair
 // records covering them (pairs p0 .. p0 + np - 1 of ensure_pairs' table), loaded
@@ -908,8 +909,10 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   constexpr bool kStageKids = kPack && FSB_WARP_STAGE_KIDS;
   constexpr bool pack = PACK && KID != KID_SMOOTH;                // packed dense part
   const int np2 = pack ? (n2 + 1) / 2 : 0;
-  const int o_cm1 = 0, o_tp1 = n1, o_cm2 = 2 * n1, o_p2 = 2 * n1 + n2;
-  const int o_w1 = 2 * (2 * n1 + n2 + pair_vecs<KID>() * np2),
+  // (16-B units) the warps' child-pair buffers first, then the level-1/2 tables
+  constexpr int kKidBuf = kStageKids ? (kWarpBlock / 32) * 2 * kKidPairs : 0;
+  const int o_cm1 = kKidBuf, o_tp1 = o_cm1 + n1, o_cm2 = o_tp1 + n1, o_p2 = o_cm2 + n2;
+  const int o_w1 = 2 * (o_p2 + pair_vecs<KID>() * np2),
             o_w2 = o_w1 + (KID == KID_WINDING ? n1 : 0);
   const int o_t2 = o_w2 + (KID == KID_WINDING ? n2 : 0);
   const int o_b2 = 2 * (o_t2 + n2);
@@ -931,8 +934,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
   const int tid = threadIdx.x, lane = tid & 31;
   int4* const s_smp = reinterpret_cast<int4*>(sh_i4 + o_smp) + (tid >> 5) * 96;
   // per-warp staging of a walk level's child pairs (Coulomb): 2 float4 per pair
-  float4* const s_kid =
-      sh_f4 + o_smp + (kWarpBlock / 32) * 96 + (tid >> 5) * 2 * (kStageKids ? V.kid_pairs : 0);
+  float4* const s_kid = sh_f4 + (tid >> 5) * 2 * kKidPairs;
   for (int i = tid; i < n1; i += kWarpBlock) {
     s_cm1(i) = V.cm[1 + i];
     s_tp1(i) = V.topo[1 + i];
@@ -1148,7 +1150,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             tpn = V.topo[tp.x + le - 1];
           }
           float4 cch;
-          if (kStageKids && use_path) {
+          if (kStageKids && V.stage_kids && use_path) {
             const int np = stage_kid_pairs(s_kid, V.cmp, tp.x, tp.y, lane);
             ks0 = staged_kid_sum(s_kid, np, qx, qy, qz, kp.dfloor_f);
             cch = staged_kid(s_kid, (tp.x & 1) + le - 1);  // the picked child, staged
@@ -1191,7 +1193,7 @@ __global__ void __launch_bounds__(kWarpBlock, FSB_WARP_MINB)
             }
           }
           const int cidx = tp.x + le - 1;
-          if (!(kStageKids && use_path)) cch = V.cm[cidx];  // one of the children just summed
+          if (!(kStageKids && V.stage_kids && use_path)) cch = V.cm[cidx];  // one of the children just summed
           if (!use_path) tpn = V.topo[cidx];
           if (alive) {  // swap / (p_agg * p_rr), p_agg = points(node) / points(a)
             seen += tp.y + 1;
@@ -1268,7 +1270,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
   if (t->max_children >= 128 || t->n >= (1ll << 25)) return 0;
   V.path = t->pt_path;
   V.cmp = nullptr;
-  V.kid_pairs = t->max_children / 2 + 2;
+  V.stage_kids = t->max_children <= 2 * (kKidPairs - 1);
   V.path_bits = t->path_bits;
   V.path_levels = t->path_levels;
   V.n1 = t->root_kids;
@@ -1312,7 +1314,7 @@ int stochastic_fast(FsTree* t, int kid, double alpha, double dfloor, const doubl
             ~(size_t)127) +
            (size_t)(kWarpBlock / 32) * 96 * 16 +
            (kid == KID_COULOMB && FSB_WARP_DENSE2 && FSB_WARP_STAGE_KIDS
-                ? (size_t)(kWarpBlock / 32) * 32 * V.kid_pairs
+                ? (size_t)(kWarpBlock / 32) * 32 * kKidPairs
                 : 0);
   };
   const bool pack_warp = can_pack && warp_smem(true) <= kSmemMax &&
