@@ -26,12 +26,12 @@ C oracle port, all host threads) on the same workload, bounded sample/step.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -80,12 +80,33 @@ def config_block(streams="warp"):
             "parallelism": "query slabs (replica tree per rank)"}
 
 
+_NVML_POLLER = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM), flush=True)
+w = sys.stdout.write
+while True:
+    try:
+        w("%d %d %d\n" % (time.time_ns(), nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                           nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+    except Exception:
+        break
+    time.sleep(0.001)
+"""
+
+
 class Clocks:
     """SM clock + throttle-reason sampling DURING the timed region.
 
-    NVML is polled from a thread every ~1 ms (the timed region of a default run
-    is only tens of ms, too short for ``nvidia-smi -lms``); ``nvidia-smi`` runs
-    beside it as the recipe's clocks line and is used when NVML is missing.
+    NVML is polled every ~1 ms by a separate Python process (the timed region of
+    a default run is only tens of ms, too short for ``nvidia-smi -lms``); its
+    timestamped samples are kept when they fall between the moments ``active``
+    is switched on and off.  A separate process keeps the poller off this
+    process's GIL, so it never delays the enqueue of the timed steps.
+    ``nvidia-smi`` runs beside it as the recipe's clocks line and is used when
+    NVML is missing.
     """
 
     REASONS = (("hw_slowdown", 0x8), ("sw_power_cap", 0x4), ("hw_thermal_slowdown", 0x40),
@@ -96,33 +117,36 @@ class Clocks:
         self.samples = []  # (sm_mhz, reasons bitmask)
         self.sm_max = None
         self.smi_lines = []
-        self._stop = threading.Event()
-        self._thread = None
+        self._poller = None
         self._proc = None
-        self.active = False  # set only while the timed region runs
+        self._windows = []  # [t_on, t_off) in time.time_ns()
+        self._active = False
 
-    def _poll(self, nv, h):
-        while not self._stop.is_set():
-            if not self.active:
-                time.sleep(0.0002)
-                continue
-            try:
-                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
-                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
-            except Exception:  # pragma: no cover
-                break
-            time.sleep(0.001)
+    @property
+    def active(self):
+        return self._active
+
+    @active.setter
+    def active(self, on):  # set only while the timed region runs
+        if on and not self._active:
+            self._windows.append([time.time_ns(), None])
+        elif not on and self._active:
+            self._windows[-1][1] = time.time_ns()
+        self._active = bool(on)
 
     def __enter__(self):
         try:
-            import pynvml as nv
-            nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.sm_max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            self._thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
-            self._thread.start()
-        except Exception:
-            self._thread = None
+            self._poller = subprocess.Popen([sys.executable, "-c", _NVML_POLLER, str(self.gpu)],
+                                            stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                            text=True)
+            first = self._poller.stdout.readline().split()  # running before the region starts
+            if len(first) == 2 and first[0] == "max":
+                self.sm_max = int(first[1])
+            else:
+                self._poller.kill()
+                self._poller = None
+        except OSError:
+            self._poller = None
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu),
@@ -130,22 +154,36 @@ class Clocks:
                  "clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown", "--format=csv,noheader,nounits",
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # its start-up queries the driver heavily: let it reach its polling loop
+            # (first line) before the timed region begins
+            first = self._proc.stdout.readline()
+            if first.strip():
+                self.smi_lines.append(first.strip())
         except OSError:
             self._proc = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        if self._thread is not None:
-            self._thread.join(timeout=2)
-        if self._proc is not None:
-            self._proc.terminate()
+        self.active = False
+        for proc in (self._poller, self._proc):
+            if proc is None:
+                continue
+            proc.terminate()
             try:
-                out, _ = self._proc.communicate(timeout=5)
+                out, _ = proc.communicate(timeout=5)
             except subprocess.TimeoutExpired:
-                self._proc.kill()
+                proc.kill()
                 out = ""
-            self.smi_lines = [ln for ln in out.splitlines() if ln.strip()]
+            if proc is self._proc:
+                self.smi_lines += [ln for ln in out.splitlines() if ln.strip()]
+                continue
+            for ln in out.splitlines():
+                parts = ln.split()
+                if len(parts) != 3:
+                    continue
+                t = int(parts[0])
+                if any(a <= t < (b if b is not None else t + 1) for a, b in self._windows):
+                    self.samples.append((int(parts[1]), int(parts[2])))
 
     def summary(self):
         sm, mask = [], 0
@@ -154,7 +192,7 @@ class Clocks:
             for _, r in self.samples:
                 mask |= int(r)
             reasons = sorted(nm for nm, bit in self.REASONS if mask & bit)
-            src = "nvml (1 ms poll during the timed region)"
+            src = "nvml (1 ms poll by a separate process during the timed region)"
             mx = float(self.sm_max) if self.sm_max else None
         else:
             reasons, mx = set(), None
@@ -173,6 +211,18 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
                 "sm_mhz_min": float(min(sm)) if sm else None, "reasons": reasons,
                 "samples": len(sm), "source": src}
+
+
+class quiet:
+    """No garbage-collector pause inside a timed measurement."""
+
+    def __enter__(self):
+        self.was = gc.isenabled()
+        gc.disable()
+
+    def __exit__(self, *exc):
+        if self.was:
+            gc.enable()
 
 
 def median_rel(est, ref):
@@ -302,14 +352,33 @@ def run_c5(args, world, rank, local, anchor=False):
     with Clocks(local) as clk:
         barrier()
         ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # an untimed ~10 ms spin before the start event lets the host enqueue several
+        # steps ahead, so a host-side hiccup early in the loop cannot idle the GPU
+        # inside the timed region (which still holds exactly K steps)
+        torch.cuda._sleep(20_000_000)
+        gc.disable()  # no collector pause while the steps are enqueued
         ev_a.record()
         clk.active = True
+        marks, host_t = [], [time.perf_counter()]
         for _ in range(args.steps):
             res = step()
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append(e)
+            host_t.append(time.perf_counter())
         ev_b.record()
         barrier()
+        gc.enable()
         clk.active = False
     step_ms = ev_a.elapsed_time(ev_b) / args.steps
+    # per-step GPU intervals and host enqueue times of the timed loop (diagnostic:
+    # a gap in the GPU intervals with a long host interval is a host-side stall)
+    gpu_iv = [ev_a.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i])
+                                               for i in range(1, len(marks))]
+    host_iv = [1e3 * (host_t[i + 1] - host_t[i]) for i in range(len(host_t) - 1)]
+    step_spread = {"gpu_ms_min": min(gpu_iv), "gpu_ms_median": float(np.median(gpu_iv)),
+                   "gpu_ms_max": max(gpu_iv), "host_enqueue_ms_max": max(host_iv),
+                   "host_enqueue_ms_median": float(np.median(host_iv))}
     if world > 1:
         tt = torch.tensor([step_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -366,6 +435,7 @@ def run_c5(args, world, rank, local, anchor=False):
                         "bench.py --gpus N (N > 1) measures on C5"}
     out = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+           "step_spread": step_spread,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic (reference mesh generators, fixed seeds)",
            "config": c5_config(world), "clocks": clk.summary(), "e2e": e2e,
@@ -488,7 +558,30 @@ def run_ours(args):
         del os.environ["FSB_REQUIRE_FAST"]
     torch.cuda.synchronize()
 
-    # ---- launch count of one step (CUPTI via torch.profiler; outside the timed region)
+    # ---- timed region: K steps, barrier + sync both sides, max over ranks
+    with Clocks(local) as clk:
+        barrier()
+        ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # an untimed ~10 ms spin before the start event lets the host enqueue several
+        # steps ahead, so a host-side hiccup early in the loop cannot idle the GPU
+        # inside the timed region (which still holds exactly K steps)
+        torch.cuda._sleep(20_000_000)
+        gc.disable()  # no collector pause while the steps are enqueued
+        ev_a.record()
+        clk.active = True
+        marks, host_t = [], [time.perf_counter()]
+        for _ in range(args.steps):
+            res = step()
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append(e)
+            host_t.append(time.perf_counter())
+        ev_b.record()
+        barrier()
+        gc.enable()
+        clk.active = False
+    # ---- launch count of one step (CUPTI via torch.profiler), after the timed
+    # region: a CUPTI session before it could leave work behind
     launches_per_step = None
     try:
         from torch.profiler import ProfilerActivity, profile
@@ -502,21 +595,15 @@ def run_ours(args):
     except Exception as exc:  # pragma: no cover
         log("profiler unavailable:", exc)
 
-    # ---- timed region: K steps, barrier + sync both sides, max over ranks
-    with Clocks(local) as clk:
-        barrier()
-        ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev_a.record()
-        switch = sys.getswitchinterval()
-        sys.setswitchinterval(2e-4)  # let the clock poller run between launches
-        clk.active = True
-        for _ in range(args.steps):
-            res = step()
-        ev_b.record()
-        barrier()
-        clk.active = False
-        sys.setswitchinterval(switch)
     step_ms = ev_a.elapsed_time(ev_b) / args.steps
+    # per-step GPU intervals and host enqueue times of the timed loop (diagnostic:
+    # a gap in the GPU intervals with a long host interval is a host-side stall)
+    gpu_iv = [ev_a.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i])
+                                               for i in range(1, len(marks))]
+    host_iv = [1e3 * (host_t[i + 1] - host_t[i]) for i in range(len(host_t) - 1)]
+    step_spread = {"gpu_ms_min": min(gpu_iv), "gpu_ms_median": float(np.median(gpu_iv)),
+                   "gpu_ms_max": max(gpu_iv), "host_enqueue_ms_max": max(host_iv),
+                   "host_enqueue_ms_median": float(np.median(host_iv))}
     # the same steps with L2 flushed before each (a 256 MB write, outside each
     # step's own event pair): reported beside the headline, which runs warm
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -555,11 +642,13 @@ def run_ours(args):
     kernel_only()
     torch.cuda.synchronize()
     reps = max(3, args.steps)
-    ev_a.record()
-    for _ in range(reps):
-        kernel_only()
-    ev_b.record()
-    torch.cuda.synchronize()
+    with quiet():
+        torch.cuda._sleep(20_000_000)  # untimed: the host enqueues ahead
+        ev_a.record()
+        for _ in range(reps):
+            kernel_only()
+        ev_b.record()
+        torch.cuda.synchronize()
     kern_ms = ev_a.elapsed_time(ev_b) / reps
     visited_mean = float(vis.double().mean().item())
 
@@ -568,6 +657,7 @@ def run_ours(args):
 
     out = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+           "step_spread": step_spread,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic (reference mesh generators, fixed seeds)",
            "config": config_block(args.streams), "clocks": clk.summary(), "e2e": e2e,
@@ -596,11 +686,13 @@ def run_ours(args):
         for _ in range(args.warmup):
             r_o = step(other)
         torch.cuda.synchronize()
-        ev_a.record()
-        for _ in range(args.steps):
-            r_o = step(other)
-        ev_b.record()
-        torch.cuda.synchronize()
+        with quiet():
+            torch.cuda._sleep(20_000_000)  # untimed: the host enqueues ahead
+            ev_a.record()
+            for _ in range(args.steps):
+                r_o = step(other)
+            ev_b.record()
+            torch.cuda.synchronize()
         other_ms = ev_a.elapsed_time(ev_b) / args.steps
         err_other = median_rel(r_o.values.cpu().numpy(), truth_h)
         sweep = []
@@ -611,10 +703,11 @@ def run_ours(args):
                 r = evaluate_field_device(cfg, src, kern, q_dev, tree2)
             torch.cuda.synchronize()
             t_w = (time.perf_counter() - t_w) * 1e3
-            ev_a.record()
-            r = evaluate_field_device(cfg, src, kern, q_dev, tree2)
-            ev_b.record()
-            torch.cuda.synchronize()
+            with quiet():
+                ev_a.record()
+                r = evaluate_field_device(cfg, src, kern, q_dev, tree2)
+                ev_b.record()
+                torch.cuda.synchronize()
             ms = ev_a.elapsed_time(ev_b)
             if os.environ.get("FSB_BENCH_DEBUG"):
                 log(f"  (warm-up call {t_w:.2f} ms)")
@@ -637,10 +730,11 @@ def run_ours(args):
                 cfg = fs.EstimatorConfig("barnes_hut", beta=p["beta"], precision="f32")
                 evaluate_field_device(cfg, src, kern, q_dev, tree2)
                 torch.cuda.synchronize()
-                ev_a.record()
-                evaluate_field_device(cfg, src, kern, q_dev, tree2)
-                ev_b.record()
-                torch.cuda.synchronize()
+                with quiet():
+                    ev_a.record()
+                    evaluate_field_device(cfg, src, kern, q_dev, tree2)
+                    ev_b.record()
+                    torch.cuda.synchronize()
                 wc.append({"beta": p["beta"], "ms": ev_a.elapsed_time(ev_b),
                            "median_rel_err": p["median_rel_err"]})
         finally:
@@ -652,10 +746,11 @@ def run_ours(args):
             cfg = fs.EstimatorConfig("barnes_hut", beta=beta, precision="f32", bh_warp_vote=True)
             evaluate_field_device(cfg, src, kern, q_dev, tree2)
             torch.cuda.synchronize()
-            ev_a.record()
-            r = evaluate_field_device(cfg, src, kern, q_dev, tree2)
-            ev_b.record()
-            torch.cuda.synchronize()
+            with quiet():
+                ev_a.record()
+                r = evaluate_field_device(cfg, src, kern, q_dev, tree2)
+                ev_b.record()
+                torch.cuda.synchronize()
             err = median_rel(r.values.cpu().numpy(), truth_h)
             vote.append({"beta": beta, "ms": ev_a.elapsed_time(ev_b), "median_rel_err": err})
             log(f"BH (warp vote) beta={beta}: {vote[-1]['ms']:.2f} ms, median rel err {err:.3e}")
@@ -712,8 +807,10 @@ def run_ours(args):
         # the build is HBM-bound -- points/s, and the DRAM bytes of the
         # build kernels from the committed ncu capture of one warm d = 4 build
         out["tree_build"] = {"points_per_s_d4_warm": len(src) / (build4_warm_ms * 1e-3),
-                             "from": "device-resident FP64 inputs (the public build_tree adds "
-                                     "the host->device copy)",
+                             "from": ("the public build_tree on the same SourceSet: its FP64 "
+                                      "arrays' device copies are cached (octree.device_sources), "
+                                      "so a warm build reads device-resident inputs; the first "
+                                      "call includes their 168 MB host->device copy"),
                              "dram_bytes": _profiled_build_traffic()}
         # the API-default precision (f64, types.py:205): the FP64 parity kernels on the
         # same workload, bitwise equal to the reference's cores
@@ -726,10 +823,11 @@ def run_ours(args):
             torch.cuda.synchronize()
             calls = []
             for _ in range(5):
-                ev_a.record()
-                r64 = evaluate_field_device(cfg, src, kern, q_dev, tr)
-                ev_b.record()
-                torch.cuda.synchronize()
+                with quiet():
+                    ev_a.record()
+                    r64 = evaluate_field_device(cfg, src, kern, q_dev, tr)
+                    ev_b.record()
+                    torch.cuda.synchronize()
                 calls.append(ev_a.elapsed_time(ev_b))
             ms = float(np.median(calls))
             f64[name] = {"ms_per_step": ms, "value": n / (ms * 1e-3), "calls_ms": calls,
@@ -885,11 +983,12 @@ def _e2e(args, fs, src, kern, qs, tree, cfg, world, rank):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
-        torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) / args.steps
+        with quiet():
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
+            torch.cuda.synchronize()
+            dt = (time.perf_counter() - t0) / args.steps
         if world > 1:
             tt = torch.tensor([dt], device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)

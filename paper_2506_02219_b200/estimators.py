@@ -24,7 +24,7 @@ from . import _core
 from . import _device as dev
 from . import _lib
 from .kernels import contribution_rows, kernel_id, node_contribution
-from .octree import Octree, TreeNode, build_tree, far_field_ratio
+from .octree import Octree, TreeNode, build_tree, device_sources, far_field_ratio
 from .rng import RngStreams
 from .types import EstimatorConfig, KernelSpec, QuerySet, SourceSet
 
@@ -160,7 +160,7 @@ def evaluate_field_device(config: EstimatorConfig, sources: SourceSet, kernel: K
     alpha, dfloor = float(kernel.alpha), float(kernel.distance_floor)
     if config.method == "brute_force":
         if source_buffers is None:
-            source_buffers = (dev.to_device(sources.positions), dev.to_device(sources.masses))
+            source_buffers = device_sources(sources)[:2]
         pts, ms = source_buffers
         _lib.check(L.fsb_brute_force_batch(kid, alpha, dfloor, prec, _vp(pts), _vp(ms),
                                            len(sources), sources.channel_count, _vp(q), n,
@@ -317,7 +317,7 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
     h = None
     keep = []
     if config.method == "brute_force":
-        pts, ms = dev.to_device(sources.positions), dev.to_device(sources.masses)
+        pts, ms = device_sources(sources)[:2]
         keep += [pts, ms]
         args.src_pts, args.src_ms = dev.ptr(pts), dev.ptr(ms)
         args.m, args.c = len(sources), sources.channel_count
