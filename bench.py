@@ -213,6 +213,31 @@ class Clocks:
                 "samples": len(sm), "source": src}
 
 
+class Gate:
+    """Holds the current stream behind a one-thread gate kernel (fsb_gate) while the
+    host enqueues a timed region, then opens it, so the region's steps run back to
+    back on the GPU however long the host takes to enqueue them.  Used where every
+    step is stream-ordered (one rank, or NCCL); the kernel gives up after ~2 s, so a
+    host-side synchronisation inside a step cannot deadlock it."""
+
+    def __init__(self, enabled=True):
+        import torch
+        self.enabled = enabled
+        self.flag = torch.zeros(1, dtype=torch.int32, pin_memory=True) if enabled else None
+
+    def close(self):
+        if self.enabled:
+            import ctypes as C
+            from paper_2506_02219_b200 import _device as dev, _lib
+            self.flag[0] = 0
+            _lib.check(_lib.lib().fsb_gate(C.c_void_p(self.flag.data_ptr()), 4_000_000_000,
+                                           C.c_void_p(dev.stream_ptr())))
+
+    def open(self):
+        if self.enabled:
+            self.flag[0] = 1
+
+
 class quiet:
     """No garbage-collector pause inside a timed measurement."""
 
@@ -349,13 +374,14 @@ def run_c5(args, world, rank, local, anchor=False):
         step()
     barrier()
     launches = _count_launches(step)
+    gate = Gate(world == 1 or dist.get_backend() == "nccl")
     with Clocks(local) as clk:
         barrier()
         ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        # an untimed ~10 ms spin before the start event lets the host enqueue several
-        # steps ahead, so a host-side hiccup early in the loop cannot idle the GPU
-        # inside the timed region (which still holds exactly K steps)
-        torch.cuda._sleep(20_000_000)
+        # the start event, the K steps and the end event are enqueued behind a gate
+        # that opens once they all are: a host-side stall while enqueueing cannot
+        # idle the GPU inside the timed region (which holds exactly K steps)
+        gate.close()  # the region runs once every step is enqueued
         gc.disable()  # no collector pause while the steps are enqueued
         ev_a.record()
         clk.active = True
@@ -367,6 +393,7 @@ def run_c5(args, world, rank, local, anchor=False):
             marks.append(e)
             host_t.append(time.perf_counter())
         ev_b.record()
+        gate.open()
         barrier()
         gc.enable()
         clk.active = False
@@ -559,13 +586,14 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, barrier + sync both sides, max over ranks
+    gate = Gate(world == 1 or dist.get_backend() == "nccl")
     with Clocks(local) as clk:
         barrier()
         ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        # an untimed ~10 ms spin before the start event lets the host enqueue several
-        # steps ahead, so a host-side hiccup early in the loop cannot idle the GPU
-        # inside the timed region (which still holds exactly K steps)
-        torch.cuda._sleep(20_000_000)
+        # the start event, the K steps and the end event are enqueued behind a gate
+        # that opens once they all are: a host-side stall while enqueueing cannot
+        # idle the GPU inside the timed region (which holds exactly K steps)
+        gate.close()  # the region runs once every step is enqueued
         gc.disable()  # no collector pause while the steps are enqueued
         ev_a.record()
         clk.active = True
@@ -577,6 +605,7 @@ def run_ours(args):
             marks.append(e)
             host_t.append(time.perf_counter())
         ev_b.record()
+        gate.open()
         barrier()
         gc.enable()
         clk.active = False
@@ -643,11 +672,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     reps = max(3, args.steps)
     with quiet():
-        torch.cuda._sleep(20_000_000)  # untimed: the host enqueues ahead
+        gate.close()
         ev_a.record()
         for _ in range(reps):
             kernel_only()
         ev_b.record()
+        gate.open()
         torch.cuda.synchronize()
     kern_ms = ev_a.elapsed_time(ev_b) / reps
     visited_mean = float(vis.double().mean().item())
@@ -687,11 +717,12 @@ def run_ours(args):
             r_o = step(other)
         torch.cuda.synchronize()
         with quiet():
-            torch.cuda._sleep(20_000_000)  # untimed: the host enqueues ahead
+            gate.close()
             ev_a.record()
             for _ in range(args.steps):
                 r_o = step(other)
             ev_b.record()
+            gate.open()
             torch.cuda.synchronize()
         other_ms = ev_a.elapsed_time(ev_b) / args.steps
         err_other = median_rel(r_o.values.cpu().numpy(), truth_h)

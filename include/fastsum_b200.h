@@ -246,6 +246,11 @@ int fsb_selftest_fp64(int64_t n, uint64_t seed, unsigned long long *counts4);
  * instruction mix with every operand on chip}. */
 int fsb_micro_peaks(double *out2, void *stream);
 
+/* Benchmark utility (no reference counterpart): hold `stream` until the host
+ * writes a nonzero value to *flag (page-locked host memory) or max_cycles SM
+ * cycles pass, so that work enqueued behind it runs back to back. */
+int fsb_gate(const int *flag, int64_t max_cycles, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

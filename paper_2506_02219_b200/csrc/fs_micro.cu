@@ -119,3 +119,28 @@ extern "C" int fsb_micro_peaks(double* out2, void* stream) {
   FS_CK(cudaGetLastError());
   return 0;
 }
+
+// ---- timing gate: a one-thread kernel that holds its stream until the host
+// writes a nonzero value to `flag` (page-locked host memory, read through UVA),
+// or until max_cycles SM cycles have passed.  bench.py enqueues the start event,
+// the K timed steps and the end event behind it, then opens the gate: the steps
+// run back to back on the GPU whatever the host does while enqueueing them (a
+// host-side synchronisation inside a step only delays the region by the timeout).
+namespace {
+__global__ void k_gate(const volatile int* flag, long long max_cycles) {
+  const long long t0 = clock64();
+  while (*flag == 0 && clock64() - t0 < max_cycles) {
+  }
+}
+}  // namespace
+
+extern "C" int fsb_gate(const int* flag, int64_t max_cycles, void* stream) {
+  using namespace fsb;
+  if (!flag || max_cycles < 0) {
+    set_error("fsb_gate: bad arguments");
+    return 1;
+  }
+  k_gate<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flag, (long long)max_cycles);
+  FS_CK(cudaGetLastError());
+  return 0;
+}
