@@ -11,7 +11,7 @@ def fmt(x, f="{:.3f}"):
 
 
 rows = [json.loads(line) for line in open(sys.argv[1]) if line.strip()]
-print("# Round 1 -- secondary configs on one B200 (tools/configs.py)\n")
+print(f"# {sys.argv[2] if len(sys.argv) > 2 else 'Round 1'} -- secondary configs on one B200 (tools/configs.py)\n")
 print("S=1 stochastic (FP32, paper_ratio, seed 1, d=4) with the reference's per-query RNG streams and with")
 print("the paper's warp-shared streams, vs the GPU deterministic BH (FP32, load-balanced, d=2) swept over")
 print("beta and log-log interpolated to each S=1 error (PAPER.md:312). Times are device-resident steps")
