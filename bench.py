@@ -1028,10 +1028,15 @@ def _e2e(args, fs, src, kern, qs, tree, cfg, world, rank):
 
     dt, r = timed(fs.QuerySet(host.numpy()))
     dt_pg, _ = timed(fs.QuerySet(np.array(qs.positions)))
-    out_bytes = sum(a.nbytes for a in (r.values, r.raw, r.flagged, r.visited_nodes, r.path_steps,
-                                       r.path_count))
+    # bytes that cross PCIe: values, raw, visited, path_steps (stochastic, non-smooth
+    # kernel); flagged (all false) and path_count (query-independent) are written on
+    # the host by fsb_evaluate_field_host while the pipeline runs
+    out_bytes = sum(a.nbytes for a in (r.values, r.raw, r.visited_nodes, r.path_steps))
+    result_bytes = sum(a.nbytes for a in (r.values, r.raw, r.flagged, r.visited_nodes,
+                                          r.path_steps, r.path_count))
     return {"value": world * n / dt, "unit": "queries/s",
             "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(out_bytes),
+            "result_bytes_per_step": int(result_bytes),
             "ms_per_step": dt * 1e3,
             "api": ("paper_2506_02219_b200.evaluate_field (host numpy in/out, pipelined slabs); "
                     "QuerySet over page-locked host memory"),

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "../../include/fastsum_b200.h"
@@ -25,11 +26,6 @@ namespace fsb {
 int query_order(const double* q, int64_t n, int32_t* perm, cudaStream_t s);
 
 namespace {
-
-__global__ void k_fill_i64(int64_t* __restrict__ a, int64_t n, int64_t v) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) a[i] = v;
-}
 
 // Streams and events of the host pipeline, created once per (thread, device)
 // and reused: creating them per call costs more than a small evaluation.
@@ -117,6 +113,20 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   }
   cut[chunks] = n;
   const bool counters = a->method == FSB_METHOD_STOCHASTIC;
+  // Constant columns need no PCIe transfer: they are written on the host while
+  // the pipeline runs -- path_count (n_samples x internal subdomains for the
+  // stochastic method, _core.py:215-267, else 0), path_steps (0 unless
+  // stochastic), flagged (false unless smooth_exp, kernels.py:110-122) and, for
+  // brute force, visited (the source count): 41 -> 32 bytes per query cross PCIe
+  // for the stochastic method.  (raw equals values unless smooth_exp, but a host
+  // copy of 8 B/query measured slower than its PCIe transfer.)
+  const bool smooth = a->smooth != 0;
+  int64_t count_value = 0;
+  if (counters && t) {
+    int ni = 0;
+    FS_TRY(internal_level1(t, s, &ni));
+    count_value = (int64_t)a->n_samples * ni;
+  }
   // Slabs alternate between two compute streams so that one slab's last
   // blocks overlap the next slab's first ones (no launch tail per slab).
   for (int k = 0; k < chunks; ++k) {
@@ -142,8 +152,7 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
     switch (a->method) {
       case FSB_METHOD_BRUTE_FORCE:
         FS_TRY(brute_force(a->kid, a->alpha, a->dfloor, !f32, a->src_pts, a->src_ms, a->m, a->c,
-                           qs, m, r, cs));
-        k_fill_i64<<<grid_for(m, 256), 256, 0, cs>>>(v, m, a->m);
+                           qs, m, r, cs));  // (visited = m for every query: filled on the host)
         break;
       case FSB_METHOD_BARNES_HUT: {
         int32_t* pp = nullptr;
@@ -165,10 +174,6 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
                           pc, cs, shared ? a->rng_group_log2 : 0,
                           (a->path_variant ? kFlagAlg2 : 0) | (shared ? kFlagShuffled : 0)));
     }
-    if (!counters) {
-      FS_CK(cudaMemsetAsync(ps, 0, sizeof(int64_t) * (size_t)m, cs));
-      FS_CK(cudaMemsetAsync(pc, 0, sizeof(int64_t) * (size_t)m, cs));
-    }
     double* vd = val.as<double>() + lo;
     double* r64 = raw_h ? raw64.as<double>() + lo : nullptr;
     uint8_t* fd = flg.as<uint8_t>() + lo;
@@ -183,12 +188,18 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
     };
     FS_TRY(d2h(values + lo, vd, sizeof(double) * (size_t)m));
     if (raw_h) FS_TRY(d2h(raw_h + lo, r64, sizeof(double) * (size_t)m));
-    FS_TRY(d2h(flagged ? flagged + lo : nullptr, fd, (size_t)m));
-    FS_TRY(d2h(visited ? visited + lo : nullptr, v, sizeof(int64_t) * (size_t)m));
-    FS_TRY(d2h(path_steps ? path_steps + lo : nullptr, ps, sizeof(int64_t) * (size_t)m));
-    FS_TRY(d2h(path_count ? path_count + lo : nullptr, pc, sizeof(int64_t) * (size_t)m));
+    if (smooth) FS_TRY(d2h(flagged ? flagged + lo : nullptr, fd, (size_t)m));
+    if (a->method != FSB_METHOD_BRUTE_FORCE)
+      FS_TRY(d2h(visited ? visited + lo : nullptr, v, sizeof(int64_t) * (size_t)m));
+    if (counters)
+      FS_TRY(d2h(path_steps ? path_steps + lo : nullptr, ps, sizeof(int64_t) * (size_t)m));
     FS_TRY(mark(st.d2h));
   }
+  // host-derived constant columns, written while the enqueued pipeline runs
+  if (path_count) std::fill(path_count, path_count + n, count_value);
+  if (path_steps && !counters) std::fill(path_steps, path_steps + n, (int64_t)0);
+  if (flagged && !smooth) std::memset(flagged, 0, (size_t)n);
+  if (visited && a->method == FSB_METHOD_BRUTE_FORCE) std::fill(visited, visited + n, a->m);
   // device buffers are freed on `s` after the last D2H copy
   cudaEvent_t done;
   FS_TRY(st.event(&done));

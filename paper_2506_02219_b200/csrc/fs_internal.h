@@ -79,6 +79,9 @@ int ensure_fast(FsTree* t, cudaStream_t s);
 int ensure_path(FsTree* t, cudaStream_t s);
 int ensure_pairs(FsTree* t, cudaStream_t s);
 int ensure_cm64(FsTree* t, cudaStream_t s);
+// internal children of the root (the subdomains that are sampled): every query's
+// stochastic path count is n_samples times this (_core.py:215-267); read once
+int internal_level1(FsTree* t, cudaStream_t s, int* out);
 constexpr int64_t kShuffleWindow = 1 << 16;  // positions per shuffle window (warp-shared mode)
 int shuffle_order(int64_t n, uint64_t seed, int64_t qoff, int32_t* perm, cudaStream_t s);
 void free_tree(FsTree* t);

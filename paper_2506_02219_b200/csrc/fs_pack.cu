@@ -479,6 +479,24 @@ __global__ void k_div_range(const double4* __restrict__ cm, int64_t n, unsigned 
   if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
 }
 
+int internal_level1(FsTree* t, cudaStream_t s, int* out) {
+  std::lock_guard<std::recursive_mutex> lk(t->mu);
+  if (t->internal_kids < 0) {
+    int cnt = 0;
+    if (t->root_kids > 0) {
+      if (!t->lo_topo) FS_TRY(ensure_lo(t, false, s));  // level-order topology
+      std::vector<int4> tp((size_t)t->root_kids);
+      FS_CK(cudaMemcpyAsync(tp.data(), t->lo_topo + 1, sizeof(int4) * tp.size(),
+                            cudaMemcpyDeviceToHost, s));
+      FS_CK(cudaStreamSynchronize(s));
+      for (const int4& v : tp) cnt += v.y > 0;
+    }
+    t->internal_kids = cnt;
+  }
+  *out = t->internal_kids;
+  return 0;
+}
+
 int ensure_cm64(FsTree* t, cudaStream_t s) {
   std::lock_guard<std::recursive_mutex> lk(t->mu);
   if (t->lo_cm64) return 0;

@@ -48,6 +48,7 @@ struct FsTree {
   float4 *pts32a = nullptr, *pts32b = nullptr;  // permuted points {x,y,z,m0}, {m1,m2,0,0}
   double4 *pts64a = nullptr, *pts64b = nullptr;
   int root_kids = 0;  // child_count[0]
+  int internal_kids = -1;  // root children with children (internal_level1), -1 = not yet read
   // Guards the lazily packed records below (ensure_*): a record pointer is
   // published only after its pack kernels have completed, so a launch on any
   // stream or host thread that obtained it through ensure_* reads finished data.
