@@ -329,9 +329,9 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
         const int cnt = s_ctl[0];
         bool act = false;
         int owner = 0, slot = 0, node = 0, lvl = 2, wseen = 0, wsteps = 0;
-        int64_t jj = 0, count_a = 1;
+        int jj = 0, count_a = 1;  // (point indices and counts fit 32 bits)
         uint64_t path = 0, kr = 0;
-        double resid = 0.0, prr = 1.0, rp = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
+        double resid = 0.0, prr = 1.0, rp = 0.0;
         int4 tp = make_int4(0, 0, 0, 0);
         while (true) {
           const unsigned need = __ballot_sync(0xffffffffu, !act);
@@ -351,12 +351,8 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
               prr = __hiloint2double(r1.w, r1.z);
               rp = __hiloint2double(r2.y, r2.x);
               kr = ((uint64_t)(uint32_t)r2.w << 32) | (uint32_t)r2.z;
-              const double4 qq = s_q[owner];
-              wx = qq.x;
-              wy = qq.y;
-              wz = qq.z;
               const int4 ta = s_tp[slot / S];
-              count_a = (int64_t)ta.w - ta.z;
+              count_a = ta.w - ta.z;
               tp = s_tp[node - 1];  // level 2: staged
               path = V.path ? V.path[jj] : 0;
               lvl = 2;
@@ -369,6 +365,9 @@ __global__ void __launch_bounds__(kB64, FSB_S64_MINB)
           if (!act) continue;
           bool cont = false;
           if (tp.y > 0) {  // _core.py:177-211 at a node below the subdomain
+            // the owner's query, re-read from shared memory (fewer live registers)
+            const double4 qq = s_q[owner];
+            const double wx = qq.x, wy = qq.y, wz = qq.z;
             int child;
             if (V.path && lvl < V.path_levels) {
               child = tp.x + (int)((path >> (V.path_bits * lvl)) & ((1ull << V.path_bits) - 1ull));
