@@ -334,12 +334,16 @@ def run_c5(args, world, rank, local, anchor=False):
     tree = fs.build_tree(src, 4)
     torch.cuda.synchronize()
     build_ms = (time.perf_counter() - t0) * 1e3
+    tmp = fs.build_tree(src, 4)  # (grows the memory pool for a second tree; freed)
+    del tmp
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    fs.build_tree(src, 4)
+    tmp = fs.build_tree(src, 4)
     e1.record()
     torch.cuda.synchronize()
     build_warm_ms = e0.elapsed_time(e1)
+    del tmp
     tree_dist = None
     if world > 1:
         barrier()
@@ -537,13 +541,19 @@ def run_ours(args):
     tree2 = fs.build_tree(src, 2)
     torch.cuda.synchronize()
     build2_ms = (time.perf_counter() - t0) * 1e3
-    # warm builds (first call includes lazy module load / allocator growth)
+    # warm build: the first calls include lazy module loading and the growth of the
+    # memory pool (a third tree while two are alive maps new memory), so one more
+    # tree is built and freed first and the next build is timed
+    tmp = fs.build_tree(src, 4)
+    del tmp
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    fs.build_tree(src, 4)
+    tmp = fs.build_tree(src, 4)
     e1.record()
     torch.cuda.synchronize()
     build4_warm_ms = e0.elapsed_time(e1)
+    del tmp
 
     # N > 1: the alternative tree distribution, built on rank 0 and broadcast (NCCL over
     # NVLink), timed beside the per-rank replica build the step uses
@@ -840,10 +850,11 @@ def run_ours(args):
         # the build is HBM-bound -- points/s, and the DRAM bytes of the
         # build kernels from the committed ncu capture of one warm d = 4 build
         out["tree_build"] = {"points_per_s_d4_warm": len(src) / (build4_warm_ms * 1e-3),
-                             "from": ("the public build_tree on the same SourceSet: its FP64 "
-                                      "arrays' device copies are cached (octree.device_sources), "
-                                      "so a warm build reads device-resident inputs; the first "
-                                      "call includes their 168 MB host->device copy"),
+                             "from": ("the public build_tree on the same SourceSet with the "
+                                      "memory pool grown: its FP64 arrays' device copies are "
+                                      "cached (octree.device_sources), so a warm build reads "
+                                      "device-resident inputs; the first call includes their "
+                                      "168 MB host->device copy, module loading and pool growth"),
                              "dram_bytes": _profiled_build_traffic()}
         # the API-default precision (f64, types.py:205): the FP64 parity kernels on the
         # same workload, bitwise equal to the reference's cores
