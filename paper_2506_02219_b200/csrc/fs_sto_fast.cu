@@ -14,11 +14,11 @@
 //    node, + {m1, m2} for winding) and every thread streams them with
 //    broadcast LDS: an FP32 + MUFU.RSQ loop, "brute force over staged nodes".
 //  * Sampling.  Per (a, s): the splitmix64 index draw, the level-1 step from
-//    shared memory (binary search of the sampled point index over the
-//    children's begins, far-field ratios from per-level cell diameters: cells
-//    are uniform splits, octree.py:225), the roulette.
+//    shared memory (a bucket table on the index draw's top bits plus a short
+//    scan over the children's begins; far-field ratios from per-level cell
+//    diameters: cells are uniform splits, octree.py:225), the roulette.
 //  * Deeper steps (~1/3 of samples descend below level 2) would leave most
-//    lanes idle if walked in place.  Descending samples are queued (24 B walk
+//    lanes idle if walked in place.  Descending samples are queued (16 B walk
 //    starts per block in global memory, L2-resident), counting-sorted by
 //    level-2 node, and served after the sampling loop by lanes that refill
 //    independently from the queue and carry each walk to completion (the
@@ -31,8 +31,9 @@
 // k_sto_warp (further down) is the same estimator with the paper's warp-shared
 // RNG streams: 32 queries of a seeded shuffled order share
 // the draws, so sampling is done once per warp and every walk is warp-uniform
-// (broadcast child loads, no queue / sort / result slots).  The Coulomb (and
-// winding) dense parts of both kernels run on the packed FP32 pipe
+// (no queue / sort / result slots; a walk level's child pairs are loaded by the
+// warp's lanes at once into shared memory and summed from there).  The Coulomb
+// (and winding) dense parts of both kernels run on the packed FP32 pipe
 // (FADD2/FFMA2, dense_coulomb_pairs / dense_winding_pairs).
 #include <algorithm>
 #include <cstdio>
