@@ -202,6 +202,7 @@ const char* fsb_last_error(void) { return fsb::g_last_error.c_str(); }
 int fsb_brute_force_batch(int kid, double alpha, double dfloor, int precision, const double* pts,
                           const double* ms, int64_t m, int c, const double* queries, int64_t n,
                           void* out, void* stream) {
+  FSB_RANGE("fsb_brute_force_batch");
   if (int rc = check_common(kid, precision, n)) return rc;
   if (m < 1 || (kid == 1 ? c != 3 : c < 1)) {
     set_error("bad source count / channel count (m=%lld c=%d)", (long long)m, c);
@@ -214,6 +215,7 @@ int fsb_brute_force_batch(int kid, double alpha, double dfloor, int precision, c
 int fsb_brute_force_f32acc64(int kid, double alpha, double dfloor, const double* pts,
                              const double* ms, int64_t m, int c, const double* queries, int64_t n,
                              double* out, void* stream) {
+  FSB_RANGE("fsb_brute_force_f32acc64");
   if (int rc = check_common(kid, 1, n)) return rc;
   if (n == 0) return 0;
   return fsb::brute_force_f32_acc64(kid, alpha, dfloor, pts, ms, m, c, queries, n, out, S(stream));
@@ -222,6 +224,7 @@ int fsb_brute_force_f32acc64(int kid, double alpha, double dfloor, const double*
 int fsb_build_tree(const double* positions, const double* masses, const double* weights,
                    int64_t m, int c, int branching_per_dim, int max_depth, fsb_tree** out,
                    void* stream) {
+  FSB_RANGE("fsb_build_tree");
   if (!out) {
     set_error("null output handle");
     return 1;
@@ -241,6 +244,7 @@ int fsb_tree_from_core_arrays(const double* diameter, const double* aggregate_ma
                               const int64_t* begin, const int64_t* end, const double* points,
                               const double* masses, int64_t num_nodes, int64_t num_points,
                               int channels, fsb_tree** out, void* stream) {
+  FSB_RANGE("fsb_tree_from_core_arrays");
   if (!out) {
     set_error("null output handle");
     return 1;
@@ -270,6 +274,7 @@ int fsb_tree_info(const fsb_tree* tree, int64_t* info) {
 }
 
 int fsb_tree_export(const fsb_tree* tree, void* const* dst, void* stream) {
+  FSB_RANGE("fsb_tree_export");
   ABI_TREE(tree);
   const fsb::FsTree* t = tree->t;
   if (!t->owns_export) {
@@ -302,6 +307,7 @@ int fsb_tree_free(fsb_tree* tree) {
 int fsb_barnes_hut_batch(fsb_tree* tree, int kid, double alpha, double dfloor, int precision,
                          const double* queries, int64_t n, const int32_t* qperm, double beta,
                          void* out, int64_t* visited, void* stream) {
+  FSB_RANGE("fsb_barnes_hut_batch");
   ABI_TREE(tree);
   if (int rc = check_common(kid, precision, n)) return rc;
   if (!(beta > 0)) {
@@ -316,6 +322,7 @@ int fsb_barnes_hut_vote_batch(fsb_tree* tree, int kid, double alpha, double dflo
                               int precision, const double* queries, int64_t n,
                               const int32_t* order, double beta, void* out, int64_t* visited,
                               void* stream) {
+  FSB_RANGE("fsb_barnes_hut_vote_batch");
   ABI_TREE(tree);
   if (int rc = check_common(kid, precision, n)) return rc;
   if (!(beta > 0)) {
@@ -331,6 +338,7 @@ int fsb_stochastic_batch(fsb_tree* tree, int kid, double alpha, double dfloor, i
                          int64_t n_samples, int rr_mode, uint64_t seed, int64_t query_offset,
                          void* out, int64_t* visited, int64_t* path_steps, int64_t* path_count,
                          void* stream) {
+  FSB_RANGE("fsb_stochastic_batch");
   ABI_TREE(tree);
   if (int rc = check_common(kid, precision, n)) return rc;
   if (n_samples < 1 || n_samples > (1LL << 30)) {
@@ -351,6 +359,7 @@ int fsb_stochastic_batch_ex(fsb_tree* tree, int kid, double alpha, double dfloor
                             int64_t n_samples, int rr_mode, uint64_t seed, int64_t query_offset,
                             int group_log2, int flags, void* out, int64_t* visited,
                             int64_t* path_steps, int64_t* path_count, void* stream) {
+  FSB_RANGE("fsb_stochastic_batch_ex");
   ABI_TREE(tree);
   if (int rc = check_common(kid, precision, n)) return rc;
   if (n_samples < 1 || n_samples > (1LL << 30) || rr_mode < 0 || rr_mode > 2 || group_log2 < 0 ||
@@ -370,6 +379,7 @@ int fsb_stochastic_batch_ex(fsb_tree* tree, int kid, double alpha, double dfloor
 int fsb_stochastic_moments_batch(fsb_tree* tree, int kid, double alpha, double dfloor,
                                  const double* queries, int64_t n, int64_t n_reps, int rr_mode,
                                  uint64_t seed, double* mean_out, double* var_out, void* stream) {
+  FSB_RANGE("fsb_stochastic_moments_batch");
   ABI_TREE(tree);
   if (int rc = check_common(kid, 0, n)) return rc;
   if (n_reps < 1 || rr_mode < 0 || rr_mode > 2) {
@@ -383,6 +393,7 @@ int fsb_stochastic_moments_batch(fsb_tree* tree, int kid, double alpha, double d
 int fsb_telescoping_batch(fsb_tree* tree, int kid, double alpha, double dfloor, int precision,
                           const double* queries, int64_t n, void* out, int64_t* visited,
                           void* stream) {
+  FSB_RANGE("fsb_telescoping_batch");
   ABI_TREE(tree);
   if (int rc = check_common(kid, precision, n)) return rc;
   return fsb::telescoping(tree->t, kid, alpha, dfloor, precision == 0, queries, n, out, visited,
@@ -390,6 +401,7 @@ int fsb_telescoping_batch(fsb_tree* tree, int kid, double alpha, double dfloor, 
 }
 
 int fsb_query_order(const double* queries, int64_t n, int32_t* perm_out, void* stream) {
+  FSB_RANGE("fsb_query_order");
   if (n < 0) {
     set_error("negative query count");
     return 1;
@@ -399,6 +411,7 @@ int fsb_query_order(const double* queries, int64_t n, int32_t* perm_out, void* s
 
 int fsb_shuffle_order(int64_t n, uint64_t seed, int64_t query_offset, int32_t* perm_out,
                       void* stream) {
+  FSB_RANGE("fsb_shuffle_order");
   if (n < 0 || (n > 0 && !perm_out)) {
     set_error("bad shuffle arguments");
     return 1;
@@ -408,6 +421,7 @@ int fsb_shuffle_order(int64_t n, uint64_t seed, int64_t query_offset, int32_t* p
 
 int fsb_post_transform(const void* raw, int raw_is_f32, int64_t n, int smooth, double alpha,
                        double* values, double* raw64, uint8_t* flagged, void* stream) {
+  FSB_RANGE("fsb_post_transform");
   if (n < 0) {
     set_error("negative count");
     return 1;

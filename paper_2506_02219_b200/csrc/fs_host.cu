@@ -227,6 +227,7 @@ extern "C" int fsb_evaluate_field_host(fsb_tree* tree, const fsb_eval_args* a,
                                        double* raw, uint8_t* flagged, int64_t* visited,
                                        int64_t* path_steps, int64_t* path_count, int chunks,
                                        void* stream) {
+  FSB_RANGE("fsb_evaluate_field_host");
   using fsb::set_error;
   if (!a || !values || (n > 0 && !queries)) {
     set_error("null argument");

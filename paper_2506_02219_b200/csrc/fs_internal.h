@@ -3,12 +3,24 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "fs_tree.cuh"
 
 namespace fsb {
 
 void set_error(const char* fmt, ...);
+
+// Scoped NVTX range around a C-ABI entry point (header-only NVTX3: a no-op
+// unless a profiling tool is attached), so Nsight timelines and ncu's
+// --nvtx-include filters see the library's calls by name.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define FSB_RANGE(name) ::fsb::NvtxRange fsb_nvtx_range_(name)
 
 #define FS_CK(expr)                                                                   \
   do {                                                                                \
