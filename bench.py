@@ -299,7 +299,8 @@ def c5_config(world):
             "l2": "inputs larger than L2 (tree ~0.9 GB, queries 240 MB); no flush",
             "parallelism": (f"strong scaling: {world} rank(s), query slabs on 2^16-position "
                             f"shuffle windows (query_offset = slab start), replica tree per rank, "
-                            f"all_gather of the FP64 field inside every step")}
+                            f"all_gather of the field inside every step (FP32 values, "
+                            f"widened to FP64 after the collective: the same bits)")}
 
 
 def run_c5(args, world, rank, local, anchor=False):
@@ -362,19 +363,21 @@ def run_c5(args, world, rank, local, anchor=False):
     cfg = fs.EstimatorConfig("stochastic", samples_per_subdomain=1, seed=1, precision="f32",
                              rng_sharing="warp")
     q_dev = dev.to_device(qs.positions[a:b])
-    full = torch.empty(world * width, dtype=torch.float64, device="cuda")
-    pad = torch.zeros(width, dtype=torch.float64, device="cuda")
+    # the FP32 path's values are FP32 results widened to FP64: gathered as FP32 (4 B
+    # per query) and widened after the collective -- the same bits
+    full = torch.empty(world * width, dtype=torch.float32, device="cuda")
+    pad = torch.zeros(width, dtype=torch.float32, device="cuda")
 
     def step():
         r = evaluate_field_device(cfg, src, kern, q_dev, tree, query_offset=a)
         if world == 1:
             return r.values
-        pad[: b - a].copy_(r.values)
+        pad[: b - a].copy_(r.values)  # exact: the values are FP32 numbers
         if dist.get_backend() == "nccl":
             dist.all_gather_into_tensor(full, pad)
         else:  # (gloo: several ranks sharing one GPU in tests)
             dist.all_gather(list(full.split(width)), pad)
-        return full
+        return full.double()
 
     for _ in range(args.warmup):
         step()

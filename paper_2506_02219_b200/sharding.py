@@ -60,13 +60,20 @@ def evaluate_field_sharded(config, sources, kernel, queries, tree=None, group=No
     rank = dist.get_rank(group)
     n = len(queries)
     a, b = slab(n, rank, world, SHUFFLE_WINDOW if _shared(config) else 1)
+    import torch
+    # precision="f32" values of the non-smooth kernels are FP32 results widened to
+    # FP64 (the post-transform is the identity): gathered as FP32, 4 B per query
+    # (SURVEY 5), and widened after the collective -- the same bits
+    narrow = config.precision == "f32" and kernel.kind != "smooth_exp"
     if b > a:
         local = evaluate_field_device(config, sources, kernel, QuerySet(queries.positions[a:b]),
                                       tree, query_offset=a).values
     else:  # more ranks than slabs: this rank contributes nothing
-        import torch
         local = torch.empty(0, dtype=torch.float64, device="cuda")
-    return gather_slabs(local, n, group, SHUFFLE_WINDOW if _shared(config) else 1).cpu().numpy()
+    if narrow:
+        local = local.to(torch.float32)
+    full = gather_slabs(local, n, group, SHUFFLE_WINDOW if _shared(config) else 1)
+    return full.to(torch.float64).cpu().numpy()
 
 
 def _shared(config) -> bool:
