@@ -20,7 +20,11 @@ struct NvtxRange {
   NvtxRange(const NvtxRange&) = delete;
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
+#ifdef FSB_NO_NVTX
+#define FSB_RANGE(name) ((void)0)
+#else
 #define FSB_RANGE(name) ::fsb::NvtxRange fsb_nvtx_range_(name)
+#endif
 
 #define FS_CK(expr)                                                                   \
   do {                                                                                \
