@@ -131,9 +131,12 @@ def test_fast_kernel_tracks_fp64_parity_kernel(fs, case, kind, rr):
                                                  seed=13, precision="f64"), s, kern, q, tree=t)
         fin = np.isfinite(b.raw)
         close = _rel(a.raw[fin], b.raw[fin]) <= 1e-4
-        assert close.mean() >= 0.97, (S, close.mean())
+        assert close.mean() >= 0.99, (S, close.mean())
         same = (a.path_steps == b.path_steps) & (a.visited_nodes == b.visited_nodes)
-        assert same.mean() >= 0.97, (S, same.mean())
+        assert same.mean() >= 0.99, (S, same.mean())
+        # where no decision flipped the difference is FP32 rounding of the terms and
+        # residuals (tools/flip_probe.py: at most 1.7e-4 over these scenes)
+        assert _rel(a.raw[fin & same], b.raw[fin & same]).max(initial=0.0) <= 2e-3, S
         np.testing.assert_array_equal(a.path_count, b.path_count)
         if rr == "disabled":  # no roulette: no decision can flip
             assert same.all()
@@ -189,9 +192,10 @@ def test_warp_kernel_tracks_fp64_shared_kernel(fs, case, kind, rr):
             a, b = res["f32"], res["f64"]
             fin = np.isfinite(b[0])
             close = _rel(a[0][fin], b[0][fin]) <= 1e-4
-            assert close.mean() >= 0.97, (S, off, close.mean())
+            assert close.mean() >= 0.99, (S, off, close.mean())
             same = (a[1] == b[1]) & (a[2] == b[2])
-            assert same.mean() >= 0.97, (S, off, same.mean())
+            assert same.mean() >= 0.99, (S, off, same.mean())
+            assert _rel(a[0][fin & same], b[0][fin & same]).max(initial=0.0) <= 2e-3, (S, off)
             np.testing.assert_array_equal(a[3], b[3])
             if rr == "disabled":
                 assert same.all()
