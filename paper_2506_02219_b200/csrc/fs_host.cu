@@ -68,15 +68,19 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   const bool f32 = a->precision == 1;
   const size_t rsz = f32 ? sizeof(float) : sizeof(double);
   // device buffers (stream-ordered pool allocations on the compute stream)
-  Scratch qd, raw, val, raw64, flg, vis, stp, cnt, perm;
+  // the four 8-byte result columns (values, raw, visited, path_steps) are rows
+  // of one block with pitch 8 n, so a slab's columns leave in one 2-D copy when
+  // the host columns are equally spaced too (evaluate_field's pinned block)
+  Scratch qd, raw, cols, flg, cnt, perm;
   FS_TRY(qd.alloc(sizeof(double) * 3 * (size_t)n, s));
   FS_TRY(raw.alloc(rsz * (size_t)n, s));
-  FS_TRY(val.alloc(sizeof(double) * (size_t)n, s));
-  if (raw_h) FS_TRY(raw64.alloc(sizeof(double) * (size_t)n, s));
+  FS_TRY(cols.alloc(sizeof(double) * 4 * (size_t)n, s));
   FS_TRY(flg.alloc((size_t)n, s));
-  FS_TRY(vis.alloc(sizeof(int64_t) * (size_t)n, s));
-  FS_TRY(stp.alloc(sizeof(int64_t) * (size_t)n, s));
   FS_TRY(cnt.alloc(sizeof(int64_t) * (size_t)n, s));
+  double* const val_d = cols.as<double>();
+  double* const raw64_d = val_d + n;
+  int64_t* const vis_d = reinterpret_cast<int64_t*>(val_d + 2 * n);
+  int64_t* const stp_d = reinterpret_cast<int64_t*>(val_d + 3 * n);
   const bool shared = a->method == FSB_METHOD_STOCHASTIC && a->rng_group_log2 > 0;
   if (a->method == FSB_METHOD_BARNES_HUT && a->query_order)
     FS_TRY(perm.alloc(sizeof(int32_t) * (size_t)n, s));
@@ -127,6 +131,24 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
     FS_TRY(internal_level1(t, s, &ni));
     count_value = (int64_t)a->n_samples * ni;
   }
+  // the device->host columns of a slab: values, raw, then visited (not brute
+  // force: host-filled) and path_steps (stochastic only); `rows` > 0 when the
+  // caller's columns are equally spaced (pitch hpitch), so one 2-D copy moves them
+  int rows = 0;
+  ptrdiff_t hpitch = 0;
+  if (raw_h) {
+    hpitch = reinterpret_cast<const char*>(raw_h) - reinterpret_cast<const char*>(values);
+    const bool has_vis = a->method != FSB_METHOD_BRUTE_FORCE;
+    auto at = [&](int k, const void* p) {
+      return p && reinterpret_cast<const char*>(p) ==
+                      reinterpret_cast<const char*>(values) + k * hpitch;
+    };
+    if (hpitch >= (ptrdiff_t)(sizeof(double) * n)) {  // rows do not overlap
+      rows = 2;
+      if (has_vis) rows = at(2, visited) ? 3 : 0;
+      if (rows == 3 && counters) rows = at(3, path_steps) ? 4 : 0;
+    }
+  }
   // Slabs alternate between two compute streams so that one slab's last
   // blocks overlap the next slab's first ones (no launch tail per slab).
   for (int k = 0; k < chunks; ++k) {
@@ -146,8 +168,8 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
     FS_TRY(mark(cs));
 
     void* r = static_cast<char*>(raw.p) + rsz * (size_t)lo;
-    int64_t* v = vis.as<int64_t>() + lo;
-    int64_t* ps = stp.as<int64_t>() + lo;
+    int64_t* v = vis_d + lo;
+    int64_t* ps = stp_d + lo;
     int64_t* pc = cnt.as<int64_t>() + lo;
     switch (a->method) {
       case FSB_METHOD_BRUTE_FORCE:
@@ -174,8 +196,8 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
                           pc, cs, shared ? a->rng_group_log2 : 0,
                           (a->path_variant ? kFlagAlg2 : 0) | (shared ? kFlagShuffled : 0)));
     }
-    double* vd = val.as<double>() + lo;
-    double* r64 = raw_h ? raw64.as<double>() + lo : nullptr;
+    double* vd = val_d + lo;
+    double* r64 = raw_h ? raw64_d + lo : nullptr;
     uint8_t* fd = flg.as<uint8_t>() + lo;
     FS_TRY(post_transform(r, f32 ? 1 : 0, m, a->smooth, a->alpha, vd, r64, fd, cs));
     FS_TRY(mark(cs));
@@ -186,13 +208,19 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
       if (dst) FS_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st.d2h));
       return 0;
     };
-    FS_TRY(d2h(values + lo, vd, sizeof(double) * (size_t)m));
-    if (raw_h) FS_TRY(d2h(raw_h + lo, r64, sizeof(double) * (size_t)m));
+    if (rows > 0) {  // values, raw[, visited[, path_steps]]: one 2-D copy
+      FS_CK(cudaMemcpy2DAsync(values + lo, (size_t)hpitch, vd, sizeof(double) * (size_t)n,
+                              sizeof(double) * (size_t)m, (size_t)rows, cudaMemcpyDeviceToHost,
+                              st.d2h));
+    } else {
+      FS_TRY(d2h(values + lo, vd, sizeof(double) * (size_t)m));
+      if (raw_h) FS_TRY(d2h(raw_h + lo, r64, sizeof(double) * (size_t)m));
+      if (a->method != FSB_METHOD_BRUTE_FORCE)
+        FS_TRY(d2h(visited ? visited + lo : nullptr, v, sizeof(int64_t) * (size_t)m));
+      if (counters)
+        FS_TRY(d2h(path_steps ? path_steps + lo : nullptr, ps, sizeof(int64_t) * (size_t)m));
+    }
     if (smooth) FS_TRY(d2h(flagged ? flagged + lo : nullptr, fd, (size_t)m));
-    if (a->method != FSB_METHOD_BRUTE_FORCE)
-      FS_TRY(d2h(visited ? visited + lo : nullptr, v, sizeof(int64_t) * (size_t)m));
-    if (counters)
-      FS_TRY(d2h(path_steps ? path_steps + lo : nullptr, ps, sizeof(int64_t) * (size_t)m));
     FS_TRY(mark(st.d2h));
   }
   // host-derived constant columns, written while the enqueued pipeline runs
