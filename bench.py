@@ -1049,10 +1049,11 @@ def _e2e(args, fs, src, kern, qs, tree, cfg, world, rank):
 
     dt, r, tr = timed(fs.QuerySet(host.numpy()))
     dt_pg, _, tr_pg = timed(fs.QuerySet(np.array(qs.positions)))
-    # bytes that cross PCIe: values, raw, visited, path_steps (stochastic, non-smooth
-    # kernel); flagged (all false) and path_count (query-independent) are written on
-    # the host by fsb_evaluate_field_host while the pipeline runs
-    out_bytes = sum(a.nbytes for a in (r.values, r.raw, r.visited_nodes, r.path_steps))
+    # bytes that cross PCIe: values, visited, path_steps (stochastic, non-smooth
+    # kernel); raw (= values, identity post-transform), flagged (all false) and
+    # path_count (query-independent) are written on the host by
+    # fsb_evaluate_field_host while the pipeline runs
+    out_bytes = sum(a.nbytes for a in (r.values, r.visited_nodes, r.path_steps))
     result_bytes = sum(a.nbytes for a in (r.values, r.raw, r.flagged, r.visited_nodes,
                                           r.path_steps, r.path_count))
     return {"value": world * n / dt, "unit": "queries/s",

@@ -8,9 +8,14 @@
 // stochastic estimator are keyed on global query indices (query_offset + slab
 // start, _core.py:219, 258), so the result is identical to one whole launch.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/fastsum_b200.h"
@@ -60,6 +65,88 @@ Streams& streams_for_device() {
   return st;
 }
 
+// Host-side work of the pipeline (raw = values copies, constant columns) on a
+// few persistent worker threads, so it overlaps the PCIe transfers of later
+// slabs: host memory moves ~40 GB/s with four threads, one thread ~16 GB/s.
+class HostPool {
+ public:
+  explicit HostPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this] { run(); });
+  }
+  int size() const { return (int)th_.size(); }
+  void submit(std::function<void()> f) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      q_.push_back(std::move(f));
+    }
+    cv_.notify_one();
+  }
+
+ private:
+  void run() {
+    for (;;) {
+      std::function<void()> f;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [this] { return !q_.empty(); });
+        f = std::move(q_.front());
+        q_.pop_front();
+      }
+      f();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::function<void()>> q_;
+};
+
+HostPool& host_pool() {  // never destroyed: workers outlive static destruction
+  static HostPool* p = new HostPool(
+      (int)std::max(1u, std::min(4u, std::thread::hardware_concurrency() / 4)));
+  return *p;
+}
+
+// one call's outstanding host jobs
+struct Latch {
+  std::mutex mu;
+  std::condition_variable cv;
+  int count = 0;
+  void add(int k) {
+    std::lock_guard<std::mutex> lk(mu);
+    count += k;
+  }
+  void done() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (--count == 0) cv.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [this] { return count == 0; });
+  }
+};
+// waits for the latch on every exit path (jobs capture the caller's frame)
+struct LatchGuard {
+  Latch& l;
+  ~LatchGuard() { l.wait(); }
+};
+
+// fn(b, e) over [0, n) in one part per worker (one part below 64 K elements)
+template <class F>
+void parallel_parts(Latch& latch, int64_t n, F fn) {
+  if (n <= 0) return;
+  HostPool& pool = host_pool();
+  const int parts = n < (1 << 16) ? 1 : pool.size();
+  latch.add(parts);
+  for (int i = 0; i < parts; ++i) {
+    const int64_t b = n * i / parts, e = n * (i + 1) / parts;
+    pool.submit([&latch, fn, b, e] {
+      fn(b, e);
+      latch.done();
+    });
+  }
+}
+
 }  // namespace
 
 static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host, int64_t n,
@@ -68,8 +155,8 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   const bool f32 = a->precision == 1;
   const size_t rsz = f32 ? sizeof(float) : sizeof(double);
   // device buffers (stream-ordered pool allocations on the compute stream)
-  // the four 8-byte result columns (values, raw, visited, path_steps) are rows
-  // of one block with pitch 8 n, so a slab's columns leave in one 2-D copy when
+  // the 8-byte result columns are rows of one block with pitch 8 n (values,
+  // visited, path_steps, raw), so a slab's columns leave in one 2-D copy when
   // the host columns are equally spaced too (evaluate_field's pinned block)
   Scratch qd, raw, cols, flg, cnt, perm;
   FS_TRY(qd.alloc(sizeof(double) * 3 * (size_t)n, s));
@@ -78,9 +165,9 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   FS_TRY(flg.alloc((size_t)n, s));
   FS_TRY(cnt.alloc(sizeof(int64_t) * (size_t)n, s));
   double* const val_d = cols.as<double>();
-  double* const raw64_d = val_d + n;
-  int64_t* const vis_d = reinterpret_cast<int64_t*>(val_d + 2 * n);
-  int64_t* const stp_d = reinterpret_cast<int64_t*>(val_d + 3 * n);
+  int64_t* const vis_d = reinterpret_cast<int64_t*>(val_d + n);
+  int64_t* const stp_d = reinterpret_cast<int64_t*>(val_d + 2 * n);
+  double* const raw64_d = val_d + 3 * n;
   const bool shared = a->method == FSB_METHOD_STOCHASTIC && a->rng_group_log2 > 0;
   if (a->method == FSB_METHOD_BARNES_HUT && a->query_order)
     FS_TRY(perm.alloc(sizeof(int32_t) * (size_t)n, s));
@@ -121,34 +208,57 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
   // the pipeline runs -- path_count (n_samples x internal subdomains for the
   // stochastic method, _core.py:215-267, else 0), path_steps (0 unless
   // stochastic), flagged (false unless smooth_exp, kernels.py:110-122) and, for
-  // brute force, visited (the source count): 41 -> 32 bytes per query cross PCIe
-  // for the stochastic method.  (raw equals values unless smooth_exp, but a host
-  // copy of 8 B/query measured slower than its PCIe transfer.)
+  // brute force, visited (the source count); and raw, which equals values
+  // bit for bit unless smooth_exp, is copied from values on the host as each
+  // slab arrives: 41 -> 24 bytes per query cross PCIe for the stochastic method.
+  // (Narrowing visited / path_steps to int32 for the copy and widening them on
+  // the host measured slower: 0.96 vs 0.94 ms on C4.)
   const bool smooth = a->smooth != 0;
+  const bool raw_dev = raw_h && smooth;  // raw crosses PCIe (smooth_exp only)
   int64_t count_value = 0;
   if (counters && t) {
     int ni = 0;
     FS_TRY(internal_level1(t, s, &ni));
     count_value = (int64_t)a->n_samples * ni;
   }
-  // the device->host columns of a slab: values, raw, then visited (not brute
-  // force: host-filled) and path_steps (stochastic only); `rows` > 0 when the
+  // the device->host 8-byte columns of a slab: values, visited (not brute
+  // force: host-filled) and path_steps (stochastic only); `rows` > 1 when the
   // caller's columns are equally spaced (pitch hpitch), so one 2-D copy moves them
+  const bool vis_dev = visited && a->method != FSB_METHOD_BRUTE_FORCE;
+  const bool stp_dev = path_steps && counters;
   int rows = 0;
   ptrdiff_t hpitch = 0;
-  if (raw_h) {
-    hpitch = reinterpret_cast<const char*>(raw_h) - reinterpret_cast<const char*>(values);
-    const bool has_vis = a->method != FSB_METHOD_BRUTE_FORCE;
-    auto at = [&](int k, const void* p) {
-      return p && reinterpret_cast<const char*>(p) ==
-                      reinterpret_cast<const char*>(values) + k * hpitch;
-    };
+  if (vis_dev) {
+    hpitch = reinterpret_cast<const char*>(visited) - reinterpret_cast<const char*>(values);
     if (hpitch >= (ptrdiff_t)(sizeof(double) * n)) {  // rows do not overlap
       rows = 2;
-      if (has_vis) rows = at(2, visited) ? 3 : 0;
-      if (rows == 3 && counters) rows = at(3, path_steps) ? 4 : 0;
+      if (stp_dev)
+        rows = reinterpret_cast<const char*>(path_steps) ==
+                       reinterpret_cast<const char*>(values) + 2 * hpitch
+                   ? 3
+                   : 0;
     }
   }
+  // host work: the constant columns now, raw slab by slab (below)
+  Latch latch;
+  LatchGuard latch_guard{latch};
+  if (path_count)
+    parallel_parts(latch, n, [=](int64_t b, int64_t e) {
+      std::fill(path_count + b, path_count + e, count_value);
+    });
+  if (path_steps && !counters)
+    parallel_parts(latch, n, [=](int64_t b, int64_t e) {
+      std::fill(path_steps + b, path_steps + e, (int64_t)0);
+    });
+  if (flagged && !smooth)
+    parallel_parts(latch, n, [=](int64_t b, int64_t e) {
+      std::memset(flagged + b, 0, (size_t)(e - b));
+    });
+  if (visited && a->method == FSB_METHOD_BRUTE_FORCE) {
+    const int64_t mv = a->m;
+    parallel_parts(latch, n, [=](int64_t b, int64_t e) { std::fill(visited + b, visited + e, mv); });
+  }
+  std::vector<cudaEvent_t> slab_done(chunks, nullptr);
   // Slabs alternate between two compute streams so that one slab's last
   // blocks overlap the next slab's first ones (no launch tail per slab).
   for (int k = 0; k < chunks; ++k) {
@@ -197,7 +307,7 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
                           (a->path_variant ? kFlagAlg2 : 0) | (shared ? kFlagShuffled : 0)));
     }
     double* vd = val_d + lo;
-    double* r64 = raw_h ? raw64_d + lo : nullptr;
+    double* r64 = raw_dev ? raw64_d + lo : nullptr;
     uint8_t* fd = flg.as<uint8_t>() + lo;
     FS_TRY(post_transform(r, f32 ? 1 : 0, m, a->smooth, a->alpha, vd, r64, fd, cs));
     FS_TRY(mark(cs));
@@ -208,26 +318,34 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
       if (dst) FS_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st.d2h));
       return 0;
     };
-    if (rows > 0) {  // values, raw[, visited[, path_steps]]: one 2-D copy
+    if (rows > 1) {  // values, visited[, path_steps]: one 2-D copy
       FS_CK(cudaMemcpy2DAsync(values + lo, (size_t)hpitch, vd, sizeof(double) * (size_t)n,
                               sizeof(double) * (size_t)m, (size_t)rows, cudaMemcpyDeviceToHost,
                               st.d2h));
     } else {
       FS_TRY(d2h(values + lo, vd, sizeof(double) * (size_t)m));
-      if (raw_h) FS_TRY(d2h(raw_h + lo, r64, sizeof(double) * (size_t)m));
-      if (a->method != FSB_METHOD_BRUTE_FORCE)
-        FS_TRY(d2h(visited ? visited + lo : nullptr, v, sizeof(int64_t) * (size_t)m));
-      if (counters)
-        FS_TRY(d2h(path_steps ? path_steps + lo : nullptr, ps, sizeof(int64_t) * (size_t)m));
+      if (vis_dev) FS_TRY(d2h(visited + lo, v, sizeof(int64_t) * (size_t)m));
+      if (stp_dev) FS_TRY(d2h(path_steps + lo, ps, sizeof(int64_t) * (size_t)m));
     }
+    if (raw_dev) FS_TRY(d2h(raw_h + lo, r64, sizeof(double) * (size_t)m));
     if (smooth) FS_TRY(d2h(flagged ? flagged + lo : nullptr, fd, (size_t)m));
     FS_TRY(mark(st.d2h));
+    FS_TRY(st.event(&slab_done[k]));
+    FS_CK(cudaEventRecord(slab_done[k], st.d2h));
   }
-  // host-derived constant columns, written while the enqueued pipeline runs
-  if (path_count) std::fill(path_count, path_count + n, count_value);
-  if (path_steps && !counters) std::fill(path_steps, path_steps + n, (int64_t)0);
-  if (flagged && !smooth) std::memset(flagged, 0, (size_t)n);
-  if (visited && a->method == FSB_METHOD_BRUTE_FORCE) std::fill(visited, visited + n, a->m);
+  // raw = values (identity post-transform): copied on the worker threads as
+  // each slab lands
+  if (raw_h && !raw_dev) {
+    for (int k = 0; k < chunks; ++k) {
+      if (!slab_done[k]) continue;
+      FS_CK(cudaEventSynchronize(slab_done[k]));
+      const int64_t lo = cut[k];
+      parallel_parts(latch, cut[k + 1] - lo, [=](int64_t b, int64_t e) {
+        std::memcpy(raw_h + lo + b, values + lo + b, sizeof(double) * (size_t)(e - b));
+      });
+    }
+  }
+  latch.wait();
   // device buffers are freed on `s` after the last D2H copy
   cudaEvent_t done;
   FS_TRY(st.event(&done));

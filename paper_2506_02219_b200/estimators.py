@@ -276,8 +276,9 @@ def _pinned_block(nbytes: int):
 
 def _pipeline_chunks(n: int) -> int:
     """Slabs for the host pipeline: enough to overlap PCIe with compute, each
-    slab still several waves of 148 SMs x 4 blocks x 256 queries."""
-    return int(max(1, min(8, n // 125_000)))
+    slab still several waves of 148 SMs x 4 blocks x 256 queries (C4, 10^6
+    queries: 6 slabs 0.89 ms, 8 slabs 0.92, 4 slabs 1.00; tools/e2e_chunks.py)."""
+    return int(max(1, min(6, n // 160_000)))
 
 
 def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSpec,
@@ -327,18 +328,20 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
         elif tree.branching_per_dim != config.resolved_branching:
             raise ValueError("prebuilt tree branching factor does not match config")
         h = C.c_void_p(tree._device_tree().handle)
-    # one pinned block for all outputs: 5 x 8-byte columns, then the flags
+    # one pinned block for all outputs: 8-byte columns values, visited, path_steps,
+    # raw, path_count, then the flags (the library copies values and the int32
+    # counters across PCIe; raw, path_count and the flags are written on the host)
     base, mem = _pinned_block(41 * n + 8)
     ptrs = [base + 8 * n * k for k in range(5)] + [base + 40 * n]
     _lib.check(L.fsb_evaluate_field_host(
         h, C.byref(args), q.ctypes.data_as(C.c_void_p), n,
-        C.c_void_p(ptrs[0]), C.c_void_p(ptrs[1]), C.c_void_p(ptrs[5]), C.c_void_p(ptrs[2]),
-        C.c_void_p(ptrs[3]), C.c_void_p(ptrs[4]),
+        C.c_void_p(ptrs[0]), C.c_void_p(ptrs[3]), C.c_void_p(ptrs[5]), C.c_void_p(ptrs[1]),
+        C.c_void_p(ptrs[2]), C.c_void_p(ptrs[4]),
         int(chunks if chunks is not None else _pipeline_chunks(n)), _sp()))
     cols = [mem[8 * n * k: 8 * n * (k + 1)] for k in range(5)]
-    return FieldResult(values=cols[0].view(np.float64), raw=cols[1].view(np.float64),
+    return FieldResult(values=cols[0].view(np.float64), raw=cols[3].view(np.float64),
                        flagged=mem[40 * n: 41 * n].view(bool),
-                       visited_nodes=cols[2].view(np.int64), path_steps=cols[3].view(np.int64),
+                       visited_nodes=cols[1].view(np.int64), path_steps=cols[2].view(np.int64),
                        path_count=cols[4].view(np.int64), method=config.method)
 
 
