@@ -14,6 +14,7 @@
 #include <cstring>
 #include <deque>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -54,6 +55,18 @@ struct Streams {
     *out = ev[used++];
     return 0;
   }
+  // page-locked staging of pageable query arrays (grown, kept)
+  double* qstage = nullptr;
+  size_t qstage_bytes = 0;
+  int query_staging(size_t bytes) {
+    if (bytes <= qstage_bytes) return 0;
+    if (qstage) FS_CK(cudaFreeHost(qstage));
+    qstage = nullptr;
+    qstage_bytes = 0;
+    FS_CK(cudaHostAlloc(reinterpret_cast<void**>(&qstage), bytes, cudaHostAllocDefault));
+    qstage_bytes = bytes;
+    return 0;
+  }
 };
 
 Streams& streams_for_device() {
@@ -64,6 +77,10 @@ Streams& streams_for_device() {
   st.used = 0;
   return st;
 }
+
+#ifndef FSB_STAGE_PAGEABLE
+#define FSB_STAGE_PAGEABLE 1  // pageable queries: staged by the worker threads
+#endif
 
 // Host-side work of the pipeline (raw = values copies, constant columns) on a
 // few persistent worker threads, so it overlaps the PCIe transfers of later
@@ -125,11 +142,24 @@ struct Latch {
     cv.wait(lk, [this] { return count == 0; });
   }
 };
-// waits for the latch on every exit path (jobs capture the caller's frame)
+// waits for the latches on every exit path (jobs capture the caller's frame)
 struct LatchGuard {
-  Latch& l;
-  ~LatchGuard() { l.wait(); }
+  Latch* l;
+  size_t count;
+  ~LatchGuard() {
+    for (size_t i = 0; i < count; ++i) l[i].wait();
+  }
 };
+
+// true when p is ordinary pageable host memory (not page-locked / registered)
+bool pageable(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // (older drivers: unregistered pointers are an error)
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
 
 // fn(b, e) over [0, n) in one part per worker (one part below 64 K elements)
 template <class F>
@@ -239,9 +269,25 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
                    : 0;
     }
   }
-  // host work: the constant columns now, raw slab by slab (below)
-  Latch latch;
-  LatchGuard latch_guard{latch};
+  // host work on the worker threads: a pageable query array copied slab by
+  // slab into page-locked staging (first: the copies wait on it; the driver's
+  // own staging of pageable copies is single-threaded and synchronous), the
+  // constant columns, raw as slabs land
+  std::unique_ptr<Latch[]> latches(new Latch[chunks + 1]);
+  LatchGuard latch_guard{latches.get(), (size_t)chunks + 1};
+  Latch& latch = latches[chunks];
+  const double* q_src = q_host;
+  if (FSB_STAGE_PAGEABLE && pageable(q_host)) {
+    FS_TRY(st.query_staging(sizeof(double) * 3 * (size_t)n));
+    double* const qs_h = st.qstage;
+    q_src = qs_h;
+    for (int k = 0; k < chunks; ++k) {
+      const int64_t lo = cut[k];
+      parallel_parts(latches[k], cut[k + 1] - lo, [=](int64_t b, int64_t e) {
+        std::memcpy(qs_h + 3 * (lo + b), q_host + 3 * (lo + b), sizeof(double) * 3 * (size_t)(e - b));
+      });
+    }
+  }
   if (path_count)
     parallel_parts(latch, n, [=](int64_t b, int64_t e) {
       std::fill(path_count + b, path_count + e, count_value);
@@ -270,7 +316,8 @@ static int evaluate_host(FsTree* t, const fsb_eval_args* a, const double* q_host
     FS_TRY(st.event(&out_ready));
     double* qs = qd.as<double>() + 3 * lo;
     FS_TRY(mark(st.h2d));
-    FS_CK(cudaMemcpyAsync(qs, q_host + 3 * lo, sizeof(double) * 3 * (size_t)m,
+    latches[k].wait();  // (staged queries: this slab's copy is done)
+    FS_CK(cudaMemcpyAsync(qs, q_src + 3 * lo, sizeof(double) * 3 * (size_t)m,
                           cudaMemcpyHostToDevice, st.h2d));
     FS_TRY(mark(st.h2d));
     FS_CK(cudaEventRecord(in_done, st.h2d));
