@@ -241,6 +241,13 @@ int fsb_write_points_file(const char *path, int64_t m, int c, const double *posi
  * square-root fast-path cases, bit mismatches}; both mismatch counts must be 0. */
 int fsb_selftest_fp64(int64_t n, uint64_t seed, unsigned long long *counts4);
 
+/* Self-test (synchronous): the FP64 Barnes-Hut acceptance shortcut (d2 against
+ * (beta dm)^2 (1 +- 2^-46), the exact _ffr(q, node) >= beta inside the band;
+ * _core.py:44-52, 117) against the reference's test on n query/node pairs placed
+ * within a few ulps to 1e-9 of the acceptance sphere and at random.  counts2
+ * (host) = {cases, mismatches}; mismatches must be 0. */
+int fsb_selftest_bh_far(int64_t n, uint64_t seed, unsigned long long *counts2);
+
 /* Measured compute ceilings for the roofline (synchronises): out2 (host) =
  * {MUFU.RSQ ops/s, Coulomb node-term interactions/s at the packed-FP32 + MUFU
  * instruction mix with every operand on chip}. */

@@ -66,6 +66,7 @@ SIGNATURES = {
     "fsb_write_field_csv": [C.c_char_p, _I64, _P, _P, _P],
     "fsb_write_points_file": [C.c_char_p, _I64, _I, _P, _P],
     "fsb_selftest_fp64": [_I64, C.c_uint64, _P],
+    "fsb_selftest_bh_far": [_I64, C.c_uint64, _P],
     "fsb_micro_peaks": [_P, _P],
     "fsb_gate": [_P, C.c_int64, _P],
 }

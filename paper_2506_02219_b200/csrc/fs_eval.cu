@@ -86,6 +86,41 @@ __device__ __forceinline__ double ffr(const typename Prec<F64>::V4& g, double qx
     return ffr_f32(g.x, g.y, g.z, g.w, (float)qx, (float)qy, (float)qz);
 }
 
+// _ffr(q, node) >= beta exactly as _core.py:44-52 decides it, without the square
+// root and division for all but a vanishing band: RN(RN(sqrt(d2)) / dm) >= beta
+// is monotone in d2, so d2 >= (beta dm)^2 (1 + 2^-46) proves "far" and
+// d2 <= (beta dm)^2 (1 - 2^-46) proves "near" (the bound's own rounding is
+// <= 2^-51 relative); inside the band, or when (beta dm)^2 is not a normal
+// double, the reference's sequence decides.
+__device__ __forceinline__ bool far_parity(double cx, double cy, double cz, double diam,
+                                           double qx, double qy, double qz, double beta) {
+  const double dx = __dsub_rn(qx, cx), dy = __dsub_rn(qy, cy), dz = __dsub_rn(qz, cz);
+  const double d2 =
+      __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  const double dm = diam < kDiamFloor ? kDiamFloor : diam;
+  const double p = __dmul_rn(beta, dm), p2 = __dmul_rn(p, p);
+  if (p2 >= 0x1p-1000 && p2 <= 0x1p1000) {
+    if (d2 >= __dmul_rn(p2, 1.0 + 0x1p-46)) return true;
+    if (d2 <= __dmul_rn(p2, 1.0 - 0x1p-46)) return false;
+  }
+  return __ddiv_rn(__dsqrt_rn(d2), dm) >= beta;
+}
+
+// FP64 term through the branch-free IEEE fast paths (bit-identical whenever
+// they apply, else the intrinsic sequence)
+template <int KID>
+__device__ __forceinline__ double term_parity(double m0, double m1, double m2, double px,
+                                              double py, double pz, double qx, double qy,
+                                              double qz, const KParams& kp) {
+  if constexpr (KID == KID_SMOOTH) {
+    return contrib_parity<KID>(m0, m1, m2, px, py, pz, qx, qy, qz, kp);
+  } else {
+    bool ok;
+    const double v = contrib_parity_fast<KID, true>(m0, m1, m2, px, py, pz, qx, qy, qz, kp, ok);
+    return ok ? v : contrib_parity<KID>(m0, m1, m2, px, py, pz, qx, qy, qz, kp);
+  }
+}
+
 // ====================================================================== BH
 // barnes_hut_batch (_core.py:101-129).  The reference pops an explicit stack
 // with children pushed in reverse, i.e. it walks the accepted frontier in DFS
@@ -95,6 +130,12 @@ __device__ __forceinline__ double ffr(const typename Prec<F64>::V4& g, double qx
 // while each lane still sees exactly its own sequence (results unchanged).
 #ifndef FSB_BH_MINB
 #define FSB_BH_MINB 1
+#endif
+#ifndef FSB_BH_FAR_FAST
+#define FSB_BH_FAR_FAST 1  // FP64 acceptance test without sqrt / division (exact)
+#endif
+#ifndef FSB_BH_TERM_FAST
+#define FSB_BH_TERM_FAST 1  // FP64 terms through the branch-free fast paths
 #endif
 template <int KID, bool F64, bool VOTE>
 __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
@@ -141,7 +182,11 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
         bool leaf = skip == cur + 1;
         bool far;
         if constexpr (F64) {
+#if FSB_BH_FAR_FAST
+          far = far_parity(g.x, g.y, g.z, g.w, qx, qy, qz, beta);  // exact _ffr >= beta
+#else
           far = ffr<F64>(g, qx, qy, qz) >= beta;  // exact _ffr (_core.py:44-52)
+#endif
         } else {
           // FP32 mode: ||q - c||^2 >= (beta * max(diam, 1e-12))^2, no sqrt / division
           float dx = (float)qx - g.x, dy = (float)qy - g.y, dz = (float)qz - g.z;
@@ -168,6 +213,8 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
               e = __float_as_int(mm.y);
             }
             v = leaf_points_sum<KID, F64>(pa, pb, b, e, qx, qy, qz, kp);
+          } else if constexpr (F64 && FSB_BH_TERM_FAST) {
+            v = term_parity<KID>(mm.x, mm.y, mm.z, g.x, g.y, g.z, qx, qy, qz, kp);
           } else {
             v = term<KID, F64>(g, mm, qx, qy, qz, kp);
           }
@@ -975,3 +1022,60 @@ int telescoping(FsTree* t, int kid, double alpha, double dfloor, bool f64, const
 }
 
 }  // namespace fsb
+
+namespace fsb {
+// self-test of far_parity against the reference's acceptance test
+// (_ffr(q, node) >= beta, _core.py:44-52 / 117) on operands that put the query
+// within a few ulps to 1e-9 of the acceptance sphere, plus general positions and
+// degenerate diameters / betas
+__global__ void k_bh_far_selftest(int64_t n, uint64_t seed, unsigned long long* counts) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t h = mix64(seed + (uint64_t)i * kGamma);
+  auto u01 = [&]() {
+    h = mix64(h + kGamma);
+    return (double)(h >> 11) * 0x1p-53;
+  };
+  const double cx = 2.0 * u01() - 1.0, cy = 2.0 * u01() - 1.0, cz = 2.0 * u01() - 1.0;
+  const int kind = (int)(i & 7);
+  double diam = kind == 6 ? 1e-13 * u01() : ldexp(0.5 + u01(), -(int)(h & 15));
+  double beta = kind == 7 ? ldexp(1.0 + u01(), (int)(h >> 60) * 80 - 600) : 0.25 + 16.0 * u01();
+  // a direction, then a distance on the sphere of radius beta * max(diam, 1e-12)
+  // perturbed by a few ulps (kinds 0-2), up to 1e-9 relative (3-4), or anywhere (5+)
+  double ux = 2.0 * u01() - 1.0, uy = 2.0 * u01() - 1.0, uz = 2.0 * u01() - 1.0;
+  const double un = sqrt(ux * ux + uy * uy + uz * uz) + 1e-300;
+  ux /= un;
+  uy /= un;
+  uz /= un;
+  const double dm = diam < kDiamFloor ? kDiamFloor : diam;
+  double t = beta * dm;
+  if (kind <= 2)
+    t *= 1.0 + (double)((int)(h & 63) - 32) * 0x1p-52;
+  else if (kind <= 4)
+    t *= 1.0 + (2.0 * u01() - 1.0) * 1e-9;
+  else
+    t *= 4.0 * u01();
+  const double qx = cx + t * ux, qy = cy + t * uy, qz = cz + t * uz;
+  const bool fast = far_parity(cx, cy, cz, diam, qx, qy, qz, beta);
+  const bool exact = ffr_parity(cx, cy, cz, diam, qx, qy, qz) >= beta;
+  atomicAdd(&counts[0], 1ull);
+  if (fast != exact) atomicAdd(&counts[1], 1ull);
+}
+}  // namespace fsb
+
+// counts2 (host) = {cases, mismatches} of the exact-acceptance shortcut
+extern "C" int fsb_selftest_bh_far(int64_t n, uint64_t seed, unsigned long long* counts2) {
+  using namespace fsb;
+  FSB_RANGE("fsb_selftest_bh_far");
+  if (n < 1 || !counts2) {
+    set_error("fsb_selftest_bh_far: bad arguments");
+    return 1;
+  }
+  Scratch c;
+  FS_TRY(c.alloc(2 * sizeof(unsigned long long), nullptr));
+  FS_CK(cudaMemset(c.p, 0, 2 * sizeof(unsigned long long)));
+  k_bh_far_selftest<<<grid_for(n, 256), 256>>>(n, seed, c.as<unsigned long long>());
+  FS_CK(cudaGetLastError());
+  FS_CK(cudaMemcpy(counts2, c.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return 0;
+}

@@ -142,3 +142,21 @@ def test_fp64_branch_free_div_sqrt_bitwise_equal_intrinsics():
         div_ok, div_bad, sqrt_ok, sqrt_bad = list(counts)
         assert div_bad == 0 and sqrt_bad == 0, list(counts)
         assert div_ok > (1 << 23) and sqrt_ok > (1 << 23)  # the fast path is the common case
+
+
+def test_fp64_bh_acceptance_shortcut_equals_reference_test():
+    """k_bh<F64> decides _ffr(q, node) >= beta (_core.py:44-52, 117) from d2 against
+    (beta dm)^2 (1 +- 2^-46) and runs the reference's sqrt / division only inside
+    that band: the decision must equal the reference's on queries placed within a
+    few ulps of the acceptance sphere, within 1e-9 of it, and anywhere, including
+    sub-floor diameters and betas from 2^-600 to 2^600."""
+    import ctypes as C
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_02219_b200 import _lib
+    counts = (C.c_ulonglong * 2)()
+    for seed in (1, 2, 3):
+        _lib.check(_lib.lib().fsb_selftest_bh_far(1 << 24, seed, counts))
+        assert counts[0] == 1 << 24 and counts[1] == 0, list(counts)
+
