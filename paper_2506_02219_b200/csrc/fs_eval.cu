@@ -35,13 +35,35 @@ __device__ __forceinline__ void load_query(const double* __restrict__ q, int64_t
   z = q[3 * qi + 2];
 }
 
+#ifndef FSB_F64_TERM_FAST
+#define FSB_F64_TERM_FAST 1  // FP64 terms through the branch-free fast paths (same bits)
+#endif
+// FP64 term through the branch-free IEEE fast paths (bit-identical whenever
+// they apply, else the intrinsic sequence)
+template <int KID>
+__device__ __forceinline__ double term_parity(double m0, double m1, double m2, double px,
+                                              double py, double pz, double qx, double qy,
+                                              double qz, const KParams& kp) {
+  if constexpr (KID == KID_SMOOTH) {
+    return contrib_parity<KID>(m0, m1, m2, px, py, pz, qx, qy, qz, kp);
+  } else {
+    bool ok;
+    const double v = contrib_parity_fast<KID, true>(m0, m1, m2, px, py, pz, qx, qy, qz, kp, ok);
+    return ok ? v : contrib_parity<KID>(m0, m1, m2, px, py, pz, qx, qy, qz, kp);
+  }
+}
+
 // term of one aggregate / point (contribution_rows)
 template <int KID, bool F64>
 __device__ __forceinline__ double term(const typename Prec<F64>::V4& g,
                                        const typename Prec<F64>::V4& mm, double qx, double qy,
                                        double qz, const KParams& kp) {
   if constexpr (F64) {
+#if FSB_F64_TERM_FAST
+    return term_parity<KID>(mm.x, mm.y, mm.z, g.x, g.y, g.z, qx, qy, qz, kp);
+#else
     return contrib_parity<KID>(mm.x, mm.y, mm.z, g.x, g.y, g.z, qx, qy, qz, kp);
+#endif
   } else {
     return (double)contrib_fast<KID>(mm.x, mm.y, mm.z, g.x, g.y, g.z, (float)qx, (float)qy,
                                      (float)qz, kp);
@@ -106,21 +128,6 @@ __device__ __forceinline__ bool far_parity(double cx, double cy, double cz, doub
   return __ddiv_rn(__dsqrt_rn(d2), dm) >= beta;
 }
 
-// FP64 term through the branch-free IEEE fast paths (bit-identical whenever
-// they apply, else the intrinsic sequence)
-template <int KID>
-__device__ __forceinline__ double term_parity(double m0, double m1, double m2, double px,
-                                              double py, double pz, double qx, double qy,
-                                              double qz, const KParams& kp) {
-  if constexpr (KID == KID_SMOOTH) {
-    return contrib_parity<KID>(m0, m1, m2, px, py, pz, qx, qy, qz, kp);
-  } else {
-    bool ok;
-    const double v = contrib_parity_fast<KID, true>(m0, m1, m2, px, py, pz, qx, qy, qz, kp, ok);
-    return ok ? v : contrib_parity<KID>(m0, m1, m2, px, py, pz, qx, qy, qz, kp);
-  }
-}
-
 // ====================================================================== BH
 // barnes_hut_batch (_core.py:101-129).  The reference pops an explicit stack
 // with children pushed in reverse, i.e. it walks the accepted frontier in DFS
@@ -133,9 +140,6 @@ __device__ __forceinline__ double term_parity(double m0, double m1, double m2, d
 #endif
 #ifndef FSB_BH_FAR_FAST
 #define FSB_BH_FAR_FAST 1  // FP64 acceptance test without sqrt / division (exact)
-#endif
-#ifndef FSB_BH_TERM_FAST
-#define FSB_BH_TERM_FAST 1  // FP64 terms through the branch-free fast paths
 #endif
 template <int KID, bool F64, bool VOTE>
 __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64>::V4* __restrict__ rec,
@@ -213,8 +217,6 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
               e = __float_as_int(mm.y);
             }
             v = leaf_points_sum<KID, F64>(pa, pb, b, e, qx, qy, qz, kp);
-          } else if constexpr (F64 && FSB_BH_TERM_FAST) {
-            v = term_parity<KID>(mm.x, mm.y, mm.z, g.x, g.y, g.z, qx, qy, qz, kp);
           } else {
             v = term<KID, F64>(g, mm, qx, qy, qz, kp);
           }
