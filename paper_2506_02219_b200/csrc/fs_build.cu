@@ -110,15 +110,15 @@ __device__ __forceinline__ int digit_step(const double p[3], double cmin[3], dou
   return (int)((r[0] * d + r[1]) * d + r[2]);
 }
 
-__global__ void k_keys(const double* __restrict__ pos, int64_t m, const double* __restrict__ csz,
-                       Geo g, uint64_t* __restrict__ keys) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= m) return;
+// the digit key words of point i over levels [0, levels) (word w at keys[w m + i])
+__device__ __forceinline__ void point_key(const double* __restrict__ pos, int64_t m, int64_t i,
+                                          const double* __restrict__ csz, const Geo& g,
+                                          int levels, uint64_t* __restrict__ keys) {
   double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
   double cmin[3] = {g.rmin[0], g.rmin[1], g.rmin[2]};
   uint64_t word = 0;
   int w = 0, t = 0;
-  for (int l = 0; l < g.D; ++l) {
+  for (int l = 0; l < levels; ++l) {
     uint64_t dig = (uint64_t)digit_step(p, cmin, csz[l], g.d);
     word |= dig << (64 - (t + 1) * g.bpl);
     if (++t == g.dpw) {
@@ -129,6 +129,27 @@ __global__ void k_keys(const double* __restrict__ pos, int64_t m, const double* 
     }
   }
   if (t > 0) keys[w * m + i] = word;
+}
+
+// every point's key over the first `levels` levels (the first word, or all D)
+__global__ void k_keys(const double* __restrict__ pos, int64_t m, const double* __restrict__ csz,
+                       Geo g, int levels, uint64_t* __restrict__ keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) point_key(pos, m, i, csz, g, levels, keys);
+}
+
+// the full key (all D levels) of the points whose first word ties with a
+// neighbour's in the first-word order: the only keys whose deeper words the
+// tie refinement, the LCPs and the node ends ever compare
+__global__ void k_keys_tied(const double* __restrict__ pos, int64_t m,
+                            const double* __restrict__ csz, Geo g,
+                            const uint64_t* __restrict__ w0s, const int32_t* __restrict__ perm,
+                            uint64_t* __restrict__ keys) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint64_t k = w0s[i];
+  const bool tied = (i > 0 && w0s[i - 1] == k) || (i + 1 < m && w0s[i + 1] == k);
+  if (tied) point_key(pos, m, perm[i], csz, g, g.D, keys);
 }
 
 __global__ void k_gather_key(const uint64_t* __restrict__ kw, const int32_t* __restrict__ perm,
@@ -620,11 +641,14 @@ int build_tree(FsTree** out, const double* pos, const double* masses, const doub
   k_iota<<<grid_for(m, B), B, 0, s>>>(perm, m);
   if (D > 0) {
     FS_CK(cudaMemsetAsync(keys.p, 0, sizeof(uint64_t) * W * m, s));
-    k_keys<<<grid_for(m, 128), 128, 0, s>>>(pos, m, dcsz.as<double>(), g, keys.as<uint64_t>());
     // stable sort by the first word (the top levels), then the short runs of equal
     // first words refined by the remaining words; the full stable LSD sort over
-    // every word (one radix pass group per word) only when some run is long
+    // every word (one radix pass group per word) only when some run is long.
+    // Only the tied points need their deeper words (k_keys_tied).
     bool full = W > 1 && FSB_BUILD_FULL_SORT;
+    const int lv0 = full ? D : std::min(g.dpw, D);
+    k_keys<<<grid_for(m, 128), 128, 0, s>>>(pos, m, dcsz.as<double>(), g, lv0,
+                                            keys.as<uint64_t>());
     if (!full) {
       const int used0 = std::min(g.dpw, D) * g.bpl;
       FS_TRY(sort_pairs_u64(keys.as<uint64_t>(), kw_s.as<uint64_t>(), perm, perm2, m, 64 - used0,
@@ -634,14 +658,19 @@ int build_tree(FsTree** out, const double* pos, const double* masses, const doub
         Scratch ovf;
         FS_TRY(ovf.alloc(sizeof(int), s));
         FS_CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), s));
+        k_keys_tied<<<grid_for(m, 128), 128, 0, s>>>(pos, m, dcsz.as<double>(), g,
+                                                     kw_s.as<uint64_t>(), perm,
+                                                     keys.as<uint64_t>());
         k_refine_ties<<<grid_for(m, B), B, 0, s>>>(kw_s.as<uint64_t>(), keys.as<uint64_t>(), W, m,
                                                    perm, ovf.as<int>());
         int over = 0;
         FS_CK(cudaMemcpyAsync(&over, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         FS_CK(cudaStreamSynchronize(s));
-        if (over) {
+        if (over) {  // every point's full key, then the multi-word LSD sort
           full = true;
           k_iota<<<grid_for(m, B), B, 0, s>>>(perm, m);
+          k_keys<<<grid_for(m, 128), 128, 0, s>>>(pos, m, dcsz.as<double>(), g, D,
+                                                  keys.as<uint64_t>());
         }
       }
     }
