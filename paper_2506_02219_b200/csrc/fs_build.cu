@@ -406,15 +406,21 @@ __global__ void k_aggregate(int64_t r0, int64_t r1, const int32_t* __restrict__ 
                             const int64_t* __restrict__ cc, const int32_t* __restrict__ fc,
                             const double* __restrict__ pts, const double* __restrict__ msp,
                             const double* __restrict__ wp, int c, double* __restrict__ am,
-                            double* __restrict__ aw, double* __restrict__ com) {
+                            double* __restrict__ aw, double* __restrict__ com,
+                            double* __restrict__ lam, double* __restrict__ law,
+                            double* __restrict__ lcom) {
+  // (am, aw, com: preorder, the tree's arrays; lam, law, lcom: the same values in
+  // level order, where a node's children are contiguous, so the children's
+  // aggregates are read sequentially rather than gathered through lo2pre)
   int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= r1) return;
   int64_t id = lo2pre[r];
   int64_t b = begin[id], e = end[id], k_n = cc[id];
   if (e - b == 1) {  // verbatim copy, octree.py:161-168
-    for (int k = 0; k < c; ++k) am[(int64_t)c * id + k] = msp[(int64_t)c * b + k];
-    aw[id] = wp[b];
-    for (int k = 0; k < 3; ++k) com[3 * id + k] = pts[3 * b + k];
+    for (int k = 0; k < c; ++k)
+      am[(int64_t)c * id + k] = lam[(int64_t)c * r + k] = msp[(int64_t)c * b + k];
+    aw[id] = law[r] = wp[b];
+    for (int k = 0; k < 3; ++k) com[3 * id + k] = lcom[3 * r + k] = pts[3 * b + k];
     return;
   }
   if (k_n == 0) {  // depth-capped / zero-side multi-point leaf, octree.py:169-176
@@ -428,29 +434,29 @@ __global__ void k_aggregate(int64_t r0, int64_t r1, const int32_t* __restrict__ 
         acc = 0.0;
         for (int64_t i = b; i < e; ++i) acc = __dadd_rn(acc, msp[(int64_t)c * i + k]);
       }
-      am[(int64_t)c * id + k] = acc;
+      am[(int64_t)c * id + k] = lam[(int64_t)c * r + k] = acc;
     }
-    aw[id] = wsum;
+    aw[id] = law[r] = wsum;
     for (int k = 0; k < 3; ++k) {
       double acc = 0.0;
       for (int64_t i = b; i < e; ++i) acc = __dadd_rn(acc, __dmul_rn(wp[i], pts[3 * i + k]));
-      com[3 * id + k] = __ddiv_rn(acc, wsum);
+      com[3 * id + k] = lcom[3 * r + k] = __ddiv_rn(acc, wsum);
     }
     return;
   }
   double w = 0.0, wc[3] = {0.0, 0.0, 0.0}, ms[kMaxChannels];
   for (int k = 0; k < c; ++k) ms[k] = 0.0;
-  int32_t f = fc[id];
+  const int64_t f = fc[id];  // first child, level order
   for (int64_t t = 0; t < k_n; ++t) {
-    int64_t k2 = lo2pre[f + t];
-    double wk = aw[k2];
+    const int64_t k2 = f + t;
+    double wk = law[k2];
     w = __dadd_rn(w, wk);
-    for (int k = 0; k < c; ++k) ms[k] = __dadd_rn(ms[k], am[(int64_t)c * k2 + k]);
-    for (int k = 0; k < 3; ++k) wc[k] = __dadd_rn(wc[k], __dmul_rn(wk, com[3 * k2 + k]));
+    for (int k = 0; k < c; ++k) ms[k] = __dadd_rn(ms[k], lam[(int64_t)c * k2 + k]);
+    for (int k = 0; k < 3; ++k) wc[k] = __dadd_rn(wc[k], __dmul_rn(wk, lcom[3 * k2 + k]));
   }
-  for (int k = 0; k < c; ++k) am[(int64_t)c * id + k] = ms[k];
-  aw[id] = w;
-  for (int k = 0; k < 3; ++k) com[3 * id + k] = __ddiv_rn(wc[k], w);
+  for (int k = 0; k < c; ++k) am[(int64_t)c * id + k] = lam[(int64_t)c * r + k] = ms[k];
+  aw[id] = law[r] = w;
+  for (int k = 0; k < 3; ++k) com[3 * id + k] = lcom[3 * r + k] = __ddiv_rn(wc[k], w);
 }
 
 // ------------------------------------------------------------ host helpers
@@ -743,13 +749,18 @@ int build_tree(FsTree** out, const double* pos, const double* masses, const doub
                                                dsides.as<double>(), g, n, off.as<int32_t>(), m,
                                                t->bbox_min, t->bbox_max, t->diameter, t->begin,
                                                t->end, t->depth, t->skip);
-  // -------- 8. aggregates, deepest level first
+  // -------- 8. aggregates, deepest level first (level-order copies as scratch)
+  Scratch lam, law, lcom;
+  FS_TRY(lam.alloc(sizeof(double) * (size_t)c * n, s));
+  FS_TRY(law.alloc(sizeof(double) * (size_t)n, s));
+  FS_TRY(lcom.alloc(sizeof(double) * 3 * (size_t)n, s));
   for (int l = t->num_levels - 1; l >= 0; --l) {
     int64_t r0 = t->level_off[l], r1 = t->level_off[l + 1];
     if (r1 <= r0) continue;
     k_aggregate<<<grid_for(r1 - r0, 128), 128, 0, s>>>(
         r0, r1, t->lo2pre, t->begin, t->end, t->child_count, t->fc_lo, t->points, t->masses,
-        t->weights, c, t->agg_mass, t->agg_weight, t->com);
+        t->weights, c, t->agg_mass, t->agg_weight, t->com, lam.as<double>(), law.as<double>(),
+        lcom.as<double>());
   }
   FS_CK(cudaGetLastError());
   int64_t rk = 0;
