@@ -5,7 +5,8 @@ equally spaced, and the host pipeline then moves a slab's columns in one 2-D
 copy.  A C-ABI caller may pass any separately allocated (pageable) arrays, or
 leave optional columns null; the pipeline then copies column by column.  Both
 layouts must give the same bytes, for every method (brute force, BH,
-telescoping, stochastic) and slab count.  Reference contract:
+telescoping, stochastic) and slab count; so must pinned and pageable query
+arrays (the latter staged by the library's worker threads).  Reference contract:
 estimators.py:260-323 (host in, host out; outputs caller-allocated,
 estimators.py:273-276).
 """
@@ -101,3 +102,26 @@ def test_separate_columns_equal_the_pinned_block(fs, method, kw):
             np.testing.assert_array_equal(out["path_steps"], ref.path_steps)
             np.testing.assert_array_equal(out["path_count"], ref.path_count)
         del keep
+
+
+@pytest.mark.parametrize("method,kw", [("stochastic", dict(seed=3, precision="f32")),
+                                       ("stochastic", dict(seed=3)),
+                                       ("barnes_hut", dict(beta=1.5))],
+                         ids=["sto-f32", "sto-f64", "bh-f64"])
+def test_pageable_and_pinned_queries_give_the_same_bytes(fs, method, kw):
+    """Pinned queries are copied to the device directly; pageable ones are first
+    staged into page-locked memory slab by slab by the library's worker threads.
+    Both must give identical results for any slab count."""
+    import torch
+    s = scenes.build_sources(dict(kind="mesh_torus", m=30000, seed=3))
+    kern = fs.KernelSpec("coulomb")
+    q = np.ascontiguousarray(np.random.default_rng(9).uniform(-0.6, 0.6, (400_003, 3)))
+    pinned = torch.empty(q.shape, dtype=torch.float64, pin_memory=True)
+    pinned.numpy()[:] = q
+    cfg = fs.EstimatorConfig(method, **kw)
+    tree = fs.build_tree(s, cfg.resolved_branching)
+    for chunks in (1, 5):
+        a = fs.evaluate_field(cfg, s, kern, fs.QuerySet(q), tree=tree, chunks=chunks)
+        b = fs.evaluate_field(cfg, s, kern, fs.QuerySet(pinned.numpy()), tree=tree, chunks=chunks)
+        for f in ("values", "raw", "flagged", "visited_nodes", "path_steps", "path_count"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f"{f} {chunks}")
