@@ -1024,13 +1024,14 @@ def _e2e(args, fs, src, kern, qs, tree, cfg, world, rank):
     off = rank * n
 
     def timed(qset):
-        """median of three trials of K steps (the host side of the step -- page
-        faults, PCIe, numpy allocation -- varies between trials by up to ~30 %)"""
+        """median of five trials of K steps after ten warm-up calls (the host side
+        of the step -- worker threads, page-locked blocks, PCIe -- keeps warming up
+        over the first tens of calls: trials of 1.27 / 1.07 / 0.91 ms after five)"""
         r = None
-        for _ in range(max(2, args.warmup)):  # like the timed loop: the previous result stays alive
+        for _ in range(max(10, args.warmup)):  # like the timed loop: the previous result stays alive
             r = fs.evaluate_field(cfg, src, kern, qset, tree=tree, query_offset=off)
         trials = []
-        for _ in range(3):
+        for _ in range(5):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
