@@ -507,6 +507,9 @@ __global__ void __launch_bounds__(128) k_telescoping(LoTree<KID, F64> T,
 // sources streamed through shared memory in the reference's order with the
 // same Kahan recurrence.
 constexpr int kBruteTile64 = 512;
+#ifndef FSB_BRUTE64_GROUPS
+#define FSB_BRUTE64_GROUPS 1  // few queries: several lanes per query (same bits)
+#endif
 template <int KID>
 __global__ void __launch_bounds__(256) k_brute64(const double* __restrict__ pts,
                                                  const double* __restrict__ ms, int64_t m, int c,
@@ -545,6 +548,55 @@ __global__ void __launch_bounds__(256) k_brute64(const double* __restrict__ pts,
     }
   }
   if (live) out[qi] = acc;
+}
+
+// Few queries: G lanes per query (G a power of two, chosen so the launch has
+// enough warps).  The group's lanes evaluate consecutive sources' terms in
+// parallel; then every lane of the group applies the reference's Kahan
+// recurrence to the G terms in source order (width-G shuffles), so each lane
+// holds the same (acc, comp) as the one-thread-per-query kernel, bit for bit.
+template <int KID, int G>
+__global__ void __launch_bounds__(256) k_brute64g(const double* __restrict__ pts,
+                                                  const double* __restrict__ ms, int64_t m, int c,
+                                                  const double* __restrict__ q, int64_t n,
+                                                  KParams kp, double* __restrict__ out) {
+  __shared__ double4 sa[kBruteTile64];
+  __shared__ double2 sb[KID == KID_WINDING ? kBruteTile64 : 1];
+  const int sub = threadIdx.x & (G - 1);
+  const int64_t qi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const bool live = qi < n;
+  double qx = 0, qy = 0, qz = 0;
+  if (live) load_query(q, qi, qx, qy, qz);
+  double acc = 0.0, comp = 0.0;
+  for (int64_t base = 0; base < m; base += kBruteTile64) {
+    const int cnt = (int)(m - base < kBruteTile64 ? m - base : kBruteTile64);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+      const int64_t j = base + k;
+      sa[k] = make_double4(pts[3 * j], pts[3 * j + 1], pts[3 * j + 2], ms[(int64_t)c * j]);
+      if (KID == KID_WINDING) sb[k] = make_double2(ms[(int64_t)c * j + 1], ms[(int64_t)c * j + 2]);
+    }
+    __syncthreads();
+    for (int k0 = 0; k0 < cnt; k0 += G) {  // (uniform across the block)
+      const int k = k0 + sub;
+      double v = 0.0;
+      if (live && k < cnt) {
+        const double4 sv = sa[k];
+        const double m1 = KID == KID_WINDING ? sb[k].x : 0.0;
+        const double m2 = KID == KID_WINDING ? sb[k].y : 0.0;
+        v = term_parity<KID>(sv.w, m1, m2, sv.x, sv.y, sv.z, qx, qy, qz, kp);
+      }
+      const int take = min(G, cnt - k0);
+      for (int t = 0; t < take; ++t) {
+        const double vt = __shfl_sync(0xffffffffu, v, t, G);
+        const double y = __dsub_rn(vt, comp);
+        const double tt = __dadd_rn(acc, y);
+        comp = __dsub_rn(__dsub_rn(tt, acc), y);
+        acc = tt;
+      }
+    }
+  }
+  if (live && sub == 0) out[qi] = acc;
 }
 
 // Fast flavour: FP32 terms, each thread owns QPT queries (register tiling over
@@ -829,9 +881,21 @@ int brute_force(int kid, double alpha, double dfloor, bool f64, const double* pt
   if (n <= 0) return 0;
   KParams kp = make_kp(alpha, dfloor);
   if (f64) {
+    // lanes per query: enough warps for 148 SMs x 16 (one query per thread from
+    // ~38 K queries up)
+    int G = 1;
+    while (G < 32 && (int64_t)n * G < (int64_t)148 * 16 * 32) G *= 2;
     return with_kid(kid, true, [&](auto K, auto) {
-      k_brute64<decltype(K)::value><<<grid_for(n, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp,
-                                                                     (double*)out);
+      constexpr int KD = decltype(K)::value;
+      const int64_t threads = n * G;
+      switch (FSB_BRUTE64_GROUPS ? G : 1) {
+        case 1: k_brute64<KD><<<grid_for(n, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
+        case 2: k_brute64g<KD, 2><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
+        case 4: k_brute64g<KD, 4><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
+        case 8: k_brute64g<KD, 8><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
+        case 16: k_brute64g<KD, 16><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
+        default: k_brute64g<KD, 32><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
+      }
     });
   }
   Scratch sa, sb;
