@@ -502,11 +502,67 @@ __global__ void __launch_bounds__(128) k_telescoping(LoTree<KID, F64> T,
   if (visited) visited[qi] = seen;
 }
 
+// Few queries: G lanes per query.  The group's lanes evaluate consecutive
+// preorder nodes' deltas (children sum - node term, each in its one lane, in
+// the reference's order) in parallel; every lane then adds the internal nodes'
+// deltas to the accumulator in preorder (width-G shuffles): the same additions
+// in the same order as the one-thread-per-query kernel, so the same bits.
+template <int KID, bool F64, int G>
+__global__ void __launch_bounds__(128) k_telescoping_g(LoTree<KID, F64> T,
+                                                       const int32_t* __restrict__ pre2lo,
+                                                       int64_t nn, const double* __restrict__ q,
+                                                       int64_t n, KParams kp,
+                                                       typename Prec<F64>::Out* __restrict__ out,
+                                                       int64_t* __restrict__ visited) {
+  const int sub = threadIdx.x & (G - 1);
+  const int64_t qi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const bool live = qi < n;
+  double qx = 0, qy = 0, qz = 0;
+  if (live) load_query(q, qi, qx, qy, qz);
+  double acc = live ? T.node_term(0, qx, qy, qz, kp) : 0.0;
+  int64_t seen = 0;  // this lane's share of the visited count
+  for (int64_t a0 = 0; a0 < nn; a0 += G) {  // (uniform across the block)
+    const int64_t a = a0 + sub;
+    double delta = 0.0;
+    bool internal = false;
+    if (live && a < nn) {
+      const int r = pre2lo[a];
+      const int4 tp = T.topo[r];
+      if (tp.y > 0) {
+        const double kids = T.children_sum(tp, qx, qy, qz, kp);
+        const double parent = T.agg_term(r, qx, qy, qz, kp);
+        delta = F64 ? __dsub_rn(kids, parent) : (kids - parent);
+        internal = true;
+        seen += 1 + tp.y;
+      }
+    }
+    const unsigned im = __ballot_sync(0xffffffffu, internal);
+    const int take = nn - a0 < G ? (int)(nn - a0) : G;
+    const unsigned gm = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (threadIdx.x & 31 & ~(G - 1));
+    const unsigned mine = im & gm;  // this group's internal nodes
+    for (int t = 0; t < take; ++t) {
+      const double dt = __shfl_sync(0xffffffffu, delta, t, G);
+      if (mine >> ((threadIdx.x & 31 & ~(G - 1)) + t) & 1u)
+        acc = F64 ? __dadd_rn(acc, dt) : acc + dt;
+    }
+  }
+  // visited: 1 (root) + the group's counts
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) seen += __shfl_xor_sync(0xffffffffu, seen, o, G);
+  if (live && sub == 0) {
+    out[qi] = (typename Prec<F64>::Out)acc;
+    if (visited) visited[qi] = 1 + seen;
+  }
+}
+
 // ============================================================== brute force
 // brute_force_batch (_core.py:80-98).  Parity flavour: one query per thread,
 // sources streamed through shared memory in the reference's order with the
 // same Kahan recurrence.
 constexpr int kBruteTile64 = 512;
+#ifndef FSB_TELESCOPING_GROUPS
+#define FSB_TELESCOPING_GROUPS 1  // few queries: several lanes per query (same bits)
+#endif
 #ifndef FSB_BRUTE64_GROUPS
 #define FSB_BRUTE64_GROUPS 1  // few queries: several lanes per query (same bits)
 #endif
@@ -1079,11 +1135,24 @@ int telescoping(FsTree* t, int kid, double alpha, double dfloor, bool f64, const
   if (n <= 0) return 0;
   FS_TRY(ensure_lo(t, f64, s));
   KParams kp = make_kp(alpha, dfloor);
+  // lanes per query: enough warps for 148 SMs x 16 (one query per thread from
+  // ~38 K queries up)
+  int G = 1;
+  while (FSB_TELESCOPING_GROUPS && G < 32 && (int64_t)n * G < (int64_t)148 * 16 * 32) G *= 2;
   return with_kid(kid, f64, [&](auto K, auto P) {
     constexpr int KID = decltype(K)::value;
     constexpr bool F64 = decltype(P)::value;
-    k_telescoping<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(
-        lo_view<KID, F64>(t), t->pre2lo, t->n, q, n, kp, (typename Prec<F64>::Out*)out, visited);
+    using O = typename Prec<F64>::Out;
+    const auto V = lo_view<KID, F64>(t);
+    const int64_t th = n * G;
+    switch (G) {
+      case 1: k_telescoping<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
+      case 2: k_telescoping_g<KID, F64, 2><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
+      case 4: k_telescoping_g<KID, F64, 4><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
+      case 8: k_telescoping_g<KID, F64, 8><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
+      case 16: k_telescoping_g<KID, F64, 16><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
+      default: k_telescoping_g<KID, F64, 32><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
+    }
   });
 }
 
