@@ -474,6 +474,75 @@ __global__ void __launch_bounds__(128) k_moments(LoTree<KID, F64> T, int root_ki
   var_out[qi] = v > 0.0 ? v : 0.0;
 }
 
+// Few queries: G lanes per query.  Lane 0 of the group stages the query's
+// deltas; the group's lanes then evaluate consecutive repetitions' estimates in
+// parallel (each one exactly as above) and every lane adds them to (acc, acc2)
+// in repetition order through width-G shuffles: the same bits.
+template <int KID, bool F64, int G>
+__global__ void __launch_bounds__(128) k_moments_g(LoTree<KID, F64> T, int root_kids,
+                                                   const double* __restrict__ q, int64_t n,
+                                                   int64_t n_reps, int rr_mode, uint64_t seed,
+                                                   KParams kp, double* __restrict__ work,
+                                                   double* __restrict__ mean_out,
+                                                   double* __restrict__ var_out) {
+  const int sub = threadIdx.x & (G - 1);
+  const int64_t qi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const bool live = qi < n;
+  double qx = 0, qy = 0, qz = 0;
+  if (live) load_query(q, qi, qx, qy, qz);
+  double* delta = work + (live ? qi : 0) * (int64_t)root_kids;
+  double base = 0.0;
+  if (live && sub == 0 && root_kids > 0) {
+    for (int a_ord = 0; a_ord < root_kids; ++a_ord)
+      if (T.topo[1 + a_ord].y == 0) base = dadd<F64>(base, T.node_term(1 + a_ord, qx, qy, qz, kp));
+    for (int a_ord = 0; a_ord < root_kids; ++a_ord) {
+      const int a = 1 + a_ord;
+      const int4 tpa = T.topo[a];
+      if (tpa.y == 0) continue;
+      const double cv = T.agg_term(a, qx, qy, qz, kp);
+      base = dadd<F64>(base, cv);
+      const double ks = T.children_sum(tpa, qx, qy, qz, kp);
+      delta[a_ord] = F64 ? __dsub_rn(ks, cv) : ks - cv;
+    }
+  }
+  __syncwarp();  // the group's deltas are staged
+  const uint64_t hq = key_fold(mix64(seed + kGamma), (uint64_t)qi);
+  double acc = 0.0, acc2 = 0.0;
+  int64_t st = 0, se = 0;
+  const int64_t reps = root_kids > 0 ? n_reps : 0;
+  for (int64_t r0 = 0; r0 < reps; r0 += G) {  // (uniform across the block)
+    const int64_t r = r0 + sub;
+    double tsum = 0.0;
+    if (live && r < reps) {
+      for (int a_ord = 0; a_ord < root_kids; ++a_ord) {
+        const int a = 1 + a_ord;
+        const int4 tpa = T.topo[a];
+        if (tpa.y == 0) continue;
+        const uint64_t hs = key_fold(key_fold(hq, (uint64_t)a_ord), (uint64_t)r);
+        tsum = __dadd_rn(tsum, sample_residual<KID, F64>(T, a, tpa, delta[a_ord], key_fold(hs, 0),
+                                                         key_fold(hs, 1), rr_mode, qx, qy, qz, kp,
+                                                         st, se));
+      }
+    }
+    const int take = reps - r0 < G ? (int)(reps - r0) : G;
+    for (int t = 0; t < take; ++t) {
+      const double ts = __shfl_sync(0xffffffffu, tsum, t, G);
+      acc = __dadd_rn(acc, ts);
+      acc2 = __dadd_rn(acc2, __dmul_rn(ts, ts));
+    }
+  }
+  if (!live || sub != 0) return;
+  if (root_kids == 0) {
+    mean_out[qi] = T.node_term(0, qx, qy, qz, kp);
+    var_out[qi] = 0.0;
+    return;
+  }
+  const double mr = __ddiv_rn(acc, (double)n_reps);
+  mean_out[qi] = __dadd_rn(base, mr);
+  const double v = __dsub_rn(__ddiv_rn(acc2, (double)n_reps), __dmul_rn(mr, mr));
+  var_out[qi] = v > 0.0 ? v : 0.0;
+}
+
 // telescoping_batch, _core.py:132-156 (preorder sweep over every internal node)
 template <int KID, bool F64>
 __global__ void __launch_bounds__(128) k_telescoping(LoTree<KID, F64> T,
@@ -560,6 +629,9 @@ __global__ void __launch_bounds__(128) k_telescoping_g(LoTree<KID, F64> T,
 // sources streamed through shared memory in the reference's order with the
 // same Kahan recurrence.
 constexpr int kBruteTile64 = 512;
+#ifndef FSB_MOMENTS_GROUPS
+#define FSB_MOMENTS_GROUPS 1  // few queries: repetitions on several lanes per query (same bits)
+#endif
 #ifndef FSB_TELESCOPING_GROUPS
 #define FSB_TELESCOPING_GROUPS 1  // few queries: several lanes per query (same bits)
 #endif
@@ -1122,11 +1194,23 @@ int stochastic_moments(FsTree* t, int kid, double alpha, double dfloor, const do
   KParams kp = make_kp(alpha, dfloor);
   Scratch work;
   FS_TRY(work.alloc(sizeof(double) * n * std::max(1, t->root_kids), s));
+  // lanes per query (repetitions in parallel) when the queries alone cannot fill
+  // 148 SMs x 16 warps
+  int G = 1;
+  while (FSB_MOMENTS_GROUPS && G < 32 && n * G < (int64_t)148 * 16 * 32 && n_reps >= 2 * G) G *= 2;
   return with_kid(kid, true, [&](auto K, auto) {
     constexpr int KID = decltype(K)::value;
-    k_moments<KID, true><<<grid_for(n, 128), 128, 0, s>>>(lo_view<KID, true>(t), t->root_kids, q,
-                                                          n, n_reps, rr_mode, seed, kp,
-                                                          work.as<double>(), mean_out, var_out);
+    const auto V = lo_view<KID, true>(t);
+    double* w = work.as<double>();
+    const int64_t th = n * G;
+    switch (G) {
+      case 1: k_moments<KID, true><<<grid_for(n, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
+      case 2: k_moments_g<KID, true, 2><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
+      case 4: k_moments_g<KID, true, 4><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
+      case 8: k_moments_g<KID, true, 8><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
+      case 16: k_moments_g<KID, true, 16><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
+      default: k_moments_g<KID, true, 32><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
+    }
   });
 }
 
