@@ -35,4 +35,13 @@ for src, kind in ((s, "coulomb"), (sw, "winding_dipole"), (s, "smooth_exp")):
         fs.evaluate_field(fs.EstimatorConfig("brute_force", precision=prec), src, kern, q)
         fs.evaluate_field(fs.EstimatorConfig("telescoping_exhaustive", precision=prec), src,
                           kern, q, tree=t4)
+    # moments (lane groups of 32 at 64 queries, one thread per query at 40,000) and
+    # the few-query lane groups of brute force / telescoping (G = 32 at 3,000 queries)
+    from paper_2506_02219_b200 import _core
+    for nq in (64, 40000):
+        qm = np.random.default_rng(3).uniform(-0.8, 0.8, (nq, 3))
+        mean, var = np.zeros(nq), np.zeros(nq)
+        _core.stochastic_moments_batch(*t4.core_arrays(), fs.estimators.kernel_id(kern),
+                                       kern.alpha, kern.distance_floor, qm, 40, 0, np.uint64(3),
+                                       mean, var)
 print("sanitize run done")
