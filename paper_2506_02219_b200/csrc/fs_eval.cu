@@ -4,6 +4,8 @@
 // winding); F32 = FP32 inputs/terms with FP64 accumulation (the reference's
 // precision="f32" contract, estimators.py:270-298), MUFU fast math for terms.
 #include <algorithm>
+#include <cstdio>
+#include <vector>
 #include <cstdlib>
 #include <type_traits>
 
@@ -138,6 +140,12 @@ __device__ __forceinline__ bool far_parity(double cx, double cy, double cz, doub
 #ifndef FSB_BH_MINB
 #define FSB_BH_MINB 1
 #endif
+#ifdef FSB_BH_CHUNK_PROF
+__device__ long long* g_bh_chunk_cycles;
+#endif
+#ifndef FSB_BH_PIPELINE
+#define FSB_BH_PIPELINE 1  // next union node's records fetched during this node's term
+#endif
 #ifndef FSB_BH_FAR_FAST
 #define FSB_BH_FAR_FAST 1  // FP64 acceptance test without sqrt / division (exact)
 #endif
@@ -161,6 +169,9 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
     chunk = __shfl_sync(0xffffffffu, chunk, 0);
     const int64_t t = (int64_t)chunk * 32 + lane;
     if ((int64_t)chunk * 32 >= n) break;
+#ifdef FSB_BH_CHUNK_PROF
+    const long long c_t0 = clock64();
+#endif
     const bool live = t < n;
     const int64_t qi = live ? (qperm ? (int64_t)qperm[t] : t) : 0;
     double qx = 0, qy = 0, qz = 0;
@@ -168,9 +179,84 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
     uint32_t i = live ? 0u : nn;
     double acc = 0.0;
     int64_t seen = 0;
+#ifdef FSB_BH_CHUNK_PROF
+    long long iters = 0;
+#endif
+#if FSB_BH_PIPELINE
+    // software-pipelined union walk: the next union node is known once this
+    // node's accept / open decisions are made, so its records are fetched before
+    // this node's term is evaluated (the load overlaps the FP64 term chain);
+    // every lane still adds its accepted terms in its own preorder
+    uint32_t cur = warp_min_u32(i);
+    V4 g_n, mm_n;
+    if (cur < nn) {
+      g_n = rec[2 * (int64_t)cur];
+      mm_n = rec[2 * (int64_t)cur + 1];
+    }
+    while (cur < nn) {
+#ifdef FSB_BH_CHUNK_PROF
+      ++iters;
+#endif
+      const bool mine = i == cur;
+      const V4 g = g_n, mm = mm_n;
+      uint32_t skip = 0;
+      bool accept = false;
+      if (mine) {
+        ++seen;
+        if constexpr (F64)
+          skip = (uint32_t)__double_as_longlong(mm.w);
+        else
+          skip = (uint32_t)__float_as_int(mm.w);
+        const bool leaf = skip == cur + 1;
+        bool far;
+        if constexpr (F64) {
+#if FSB_BH_FAR_FAST
+          far = far_parity(g.x, g.y, g.z, g.w, qx, qy, qz, beta);  // exact _ffr >= beta
+#else
+          far = ffr<F64>(g, qx, qy, qz) >= beta;  // exact _ffr (_core.py:44-52)
+#endif
+        } else {
+          float dx = (float)qx - g.x, dy = (float)qy - g.y, dz = (float)qz - g.z;
+          float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+          float thr = beta_f * fmaxf(g.w, 1e-12f);
+          far = d2 >= thr * thr;
+        }
+        accept = leaf || far;
+      }
+      if (VOTE) accept = __all_sync(0xffffffffu, !mine || accept);
+      const uint32_t i_next = mine ? (accept ? skip : cur + 1) : i;
+      const uint32_t cur_next = warp_min_u32(i_next);
+      if (cur_next < nn) {  // the next node's records, in flight during this term
+        g_n = rec[2 * (int64_t)cur_next];
+        mm_n = rec[2 * (int64_t)cur_next + 1];
+      }
+      if (mine && accept) {
+        double v;
+        if (g.w < 0) {  // multi-point leaf: exact per-point sum
+          int64_t b, e;
+          if constexpr (F64) {
+            b = __double_as_longlong(mm.x);
+            e = __double_as_longlong(mm.y);
+          } else {
+            b = __float_as_int(mm.x);
+            e = __float_as_int(mm.y);
+          }
+          v = leaf_points_sum<KID, F64>(pa, pb, b, e, qx, qy, qz, kp);
+        } else {
+          v = term<KID, F64>(g, mm, qx, qy, qz, kp);
+        }
+        acc = dadd<F64>(acc, v);
+      }
+      i = i_next;
+      cur = cur_next;
+    }
+#else
     while (true) {
       uint32_t cur = warp_min_u32(i);
       if (cur >= nn) break;
+#ifdef FSB_BH_CHUNK_PROF
+      ++iters;
+#endif
       const bool mine = i == cur;
       V4 g, mm;
       uint32_t skip = 0;
@@ -227,10 +313,21 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
         }
       }
     }
+#endif
     if (live) {
       out[qi] = (typename Prec<F64>::Out)acc;
       if (visited) visited[qi] = seen;
     }
+#ifdef FSB_BH_CHUNK_PROF
+    {  // cycles, union iterations, longest lane sequence (seen)
+      const long long mx = __reduce_max_sync(0xffffffffu, (unsigned)(live ? seen : 0));
+      if (lane == 0 && g_bh_chunk_cycles) {
+        g_bh_chunk_cycles[3 * chunk] = clock64() - c_t0;
+        g_bh_chunk_cycles[3 * chunk + 1] = iters;
+        g_bh_chunk_cycles[3 * chunk + 2] = mx;
+      }
+    }
+#endif
   }
 }
 
@@ -1119,10 +1216,36 @@ int barnes_hut(FsTree* t, int kid, double alpha, double dfloor, bool f64, const 
                                           (typename Prec<F64>::Out*)out, visited,
                                           work.as<unsigned int>());
     };
+#ifdef FSB_BH_CHUNK_PROF
+    const int64_t nch = (n + 31) / 32;
+    long long* prof = nullptr;
+    cudaMalloc(&prof, 3 * sizeof(long long) * nch);
+    cudaMemset(prof, 0, 3 * sizeof(long long) * nch);
+    cudaMemcpyToSymbol(g_bh_chunk_cycles, &prof, sizeof(prof));
+#endif
     if (vote)
       launch(k_bh<KID, F64, true>);
     else
       launch(k_bh<KID, F64, false>);
+#ifdef FSB_BH_CHUNK_PROF
+    std::vector<long long> h(3 * nch);
+    cudaMemcpy(h.data(), prof, 3 * sizeof(long long) * nch, cudaMemcpyDeviceToHost);
+    std::vector<int64_t> idx(nch);
+    for (int64_t k = 0; k < nch; ++k) idx[k] = k;
+    std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return h[3 * a] > h[3 * b]; });
+    long long sum = 0;
+    for (int64_t k = 0; k < nch; ++k) sum += h[3 * k];
+    fprintf(stderr, "bh chunks %lld: sum %.3e cycles; top chunks (cycles / union iters / max lane seen):",
+            (long long)nch, (double)sum);
+    for (int k = 0; k < 8 && k < nch; ++k)
+      fprintf(stderr, " [%lld: %lld/%lld/%lld]", (long long)idx[k], h[3 * idx[k]], h[3 * idx[k] + 1],
+              h[3 * idx[k] + 2]);
+    const int64_t med = idx[nch / 2];
+    fprintf(stderr, " median chunk %lld/%lld/%lld\n", h[3 * med], h[3 * med + 1], h[3 * med + 2]);
+    cudaFree(prof);
+    long long* z = nullptr;
+    cudaMemcpyToSymbol(g_bh_chunk_cycles, &z, sizeof(z));
+#endif
   });
 }
 
