@@ -941,6 +941,18 @@ def run_ours(args):
             "nominal_peak": nominal * 10 / 1e12, "frac_of_nominal": ach / nominal,
             "nominal_source": (f"FP32 128/clk/SM over 8 ops, MUFU 16/clk/SM over 1 op, {sms} SMs "
                                f"x {f_mhz:.0f} MHz"),
+            "survey_8d": {
+                "flops_per_query": 10.0 * (n1 + n2) + 20.0 * S * n_int + 10.0 * walk_inter,
+                "formula": ("SURVEY 8(d): (N1 + N2) F_k + S N_sub (2 x 10 flops for the two "
+                            "far-field ratios) + sum over deeper levels (kids + 1) F_k, F_k = 10"),
+                "achieved": (10.0 * (n1 + n2) + 20.0 * S * n_int + 10.0 * walk_inter) * n
+                            / (kern_ms * 1e-3) / 1e12,
+                "frac": (10.0 * (n1 + n2) + 20.0 * S * n_int + 10.0 * walk_inter) * n
+                        / (kern_ms * 1e-3) / (limit * 10),
+                "note": ("the survey's algorithmic count includes the N1 control-variate terms, "
+                         "which the kernel's dense part cancels (never evaluated), and the "
+                         "ratio arithmetic of every sample; `frac` above counts only the node "
+                         "terms the kernel evaluates")},
             "pipe_floor_ms": floor_ms, "frac_of_pipe_floor": floor_ms / kern_ms,
             "pipe_floor_note": (f"FMA/ALU/MUFU pipe floor incl. {samples_q} samples/query x 6 "
                                 f"splitmix64 mixes; cycles/query fma {fma_cyc:.1f} alu "
