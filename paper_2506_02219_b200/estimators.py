@@ -274,11 +274,18 @@ def _pinned_block(nbytes: int):
         return entry[0].data_ptr(), entry[1]
 
 
-def _pipeline_chunks(n: int) -> int:
+def _pipeline_chunks(n: int, config=None) -> int:
     """Slabs for the host pipeline: enough to overlap PCIe with compute, each
     slab still several waves of 148 SMs x 4 blocks x 256 queries (C4, 10^6
-    queries: 6 slabs 0.89 ms, 8 slabs 0.92, 4 slabs 1.00; tools/e2e_chunks.py)."""
-    return int(max(1, min(6, n // 160_000)))
+    queries: 6 slabs 0.89 ms, 8 slabs 0.92, 4 slabs 1.00; tools/e2e_chunks.py).
+    Barnes-Hut takes fewer (tools/e2e_f64.py, C4): the load-balanced FP32 kernel
+    synchronises with the host between its work-splitting rounds, so slabs
+    serialise (beta 6.4: 4.7 ms in one slab, 20.7 in six), and each FP64 slab pays
+    its own longest-chunk tail (beta 2: 2.58 ms in three slabs, 2.75 in six)."""
+    cap = 6
+    if config is not None and config.method == "barnes_hut":
+        cap = 1 if config.precision == "f32" else 3
+    return int(max(1, min(cap, n // 160_000)))
 
 
 def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSpec,
@@ -337,7 +344,7 @@ def evaluate_field(config: EstimatorConfig, sources: SourceSet, kernel: KernelSp
         h, C.byref(args), q.ctypes.data_as(C.c_void_p), n,
         C.c_void_p(ptrs[0]), C.c_void_p(ptrs[3]), C.c_void_p(ptrs[5]), C.c_void_p(ptrs[1]),
         C.c_void_p(ptrs[2]), C.c_void_p(ptrs[4]),
-        int(chunks if chunks is not None else _pipeline_chunks(n)), _sp()))
+        int(chunks if chunks is not None else _pipeline_chunks(n, config)), _sp()))
     cols = [mem[8 * n * k: 8 * n * (k + 1)] for k in range(5)]
     return FieldResult(values=cols[0].view(np.float64), raw=cols[3].view(np.float64),
                        flagged=mem[40 * n: 41 * n].view(bool),
