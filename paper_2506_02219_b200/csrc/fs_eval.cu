@@ -726,6 +726,12 @@ __global__ void __launch_bounds__(128) k_telescoping_g(LoTree<KID, F64> T,
 // sources streamed through shared memory in the reference's order with the
 // same Kahan recurrence.
 constexpr int kBruteTile64 = 512;
+// lanes per query for the few-query kernels: 1 when the queries alone give
+// 148 SMs x 16 warps, else 8, or 32 below ~9.5 K queries (two instantiations)
+static inline int lane_groups(int64_t n) {
+  const int64_t want = (int64_t)148 * 16 * 32;
+  return n >= want ? 1 : (n * 8 >= want ? 8 : 32);
+}
 #ifndef FSB_MOMENTS_GROUPS
 #define FSB_MOMENTS_GROUPS 1  // few queries: repetitions on several lanes per query (same bits)
 #endif
@@ -1106,21 +1112,17 @@ int brute_force(int kid, double alpha, double dfloor, bool f64, const double* pt
   if (n <= 0) return 0;
   KParams kp = make_kp(alpha, dfloor);
   if (f64) {
-    // lanes per query: enough warps for 148 SMs x 16 (one query per thread from
-    // ~38 K queries up)
-    int G = 1;
-    while (G < 32 && (int64_t)n * G < (int64_t)148 * 16 * 32) G *= 2;
+    // lanes per query (lane_groups): several when the queries alone cannot fill the GPU
+    const int G = FSB_BRUTE64_GROUPS ? lane_groups(n) : 1;
     return with_kid(kid, true, [&](auto K, auto) {
       constexpr int KD = decltype(K)::value;
       const int64_t threads = n * G;
-      switch (FSB_BRUTE64_GROUPS ? G : 1) {
-        case 1: k_brute64<KD><<<grid_for(n, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
-        case 2: k_brute64g<KD, 2><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
-        case 4: k_brute64g<KD, 4><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
-        case 8: k_brute64g<KD, 8><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
-        case 16: k_brute64g<KD, 16><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
-        default: k_brute64g<KD, 32><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out); break;
-      }
+      if (G == 1)
+        k_brute64<KD><<<grid_for(n, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out);
+      else if (G == 8)
+        k_brute64g<KD, 8><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out);
+      else
+        k_brute64g<KD, 32><<<grid_for(threads, 256), 256, 0, s>>>(pts, ms, m, c, q, n, kp, (double*)out);
     });
   }
   Scratch sa, sb;
@@ -1319,21 +1321,19 @@ int stochastic_moments(FsTree* t, int kid, double alpha, double dfloor, const do
   FS_TRY(work.alloc(sizeof(double) * n * std::max(1, t->root_kids), s));
   // lanes per query (repetitions in parallel) when the queries alone cannot fill
   // 148 SMs x 16 warps
-  int G = 1;
-  while (FSB_MOMENTS_GROUPS && G < 32 && n * G < (int64_t)148 * 16 * 32 && n_reps >= 2 * G) G *= 2;
+  int G = FSB_MOMENTS_GROUPS ? lane_groups(n) : 1;
+  if (n_reps < 2 * G) G = 1;
   return with_kid(kid, true, [&](auto K, auto) {
     constexpr int KID = decltype(K)::value;
     const auto V = lo_view<KID, true>(t);
     double* w = work.as<double>();
     const int64_t th = n * G;
-    switch (G) {
-      case 1: k_moments<KID, true><<<grid_for(n, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
-      case 2: k_moments_g<KID, true, 2><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
-      case 4: k_moments_g<KID, true, 4><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
-      case 8: k_moments_g<KID, true, 8><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
-      case 16: k_moments_g<KID, true, 16><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
-      default: k_moments_g<KID, true, 32><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out); break;
-    }
+    if (G == 1)
+      k_moments<KID, true><<<grid_for(n, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out);
+    else if (G == 8)
+      k_moments_g<KID, true, 8><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out);
+    else
+      k_moments_g<KID, true, 32><<<grid_for(th, 128), 128, 0, s>>>(V, t->root_kids, q, n, n_reps, rr_mode, seed, kp, w, mean_out, var_out);
   });
 }
 
@@ -1342,24 +1342,20 @@ int telescoping(FsTree* t, int kid, double alpha, double dfloor, bool f64, const
   if (n <= 0) return 0;
   FS_TRY(ensure_lo(t, f64, s));
   KParams kp = make_kp(alpha, dfloor);
-  // lanes per query: enough warps for 148 SMs x 16 (one query per thread from
-  // ~38 K queries up)
-  int G = 1;
-  while (FSB_TELESCOPING_GROUPS && G < 32 && (int64_t)n * G < (int64_t)148 * 16 * 32) G *= 2;
+  // lanes per query (lane_groups): several when the queries alone cannot fill the GPU
+  const int G = FSB_TELESCOPING_GROUPS ? lane_groups(n) : 1;
   return with_kid(kid, f64, [&](auto K, auto P) {
     constexpr int KID = decltype(K)::value;
     constexpr bool F64 = decltype(P)::value;
     using O = typename Prec<F64>::Out;
     const auto V = lo_view<KID, F64>(t);
     const int64_t th = n * G;
-    switch (G) {
-      case 1: k_telescoping<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
-      case 2: k_telescoping_g<KID, F64, 2><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
-      case 4: k_telescoping_g<KID, F64, 4><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
-      case 8: k_telescoping_g<KID, F64, 8><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
-      case 16: k_telescoping_g<KID, F64, 16><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
-      default: k_telescoping_g<KID, F64, 32><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited); break;
-    }
+    if (G == 1)
+      k_telescoping<KID, F64><<<grid_for(n, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited);
+    else if (G == 8)
+      k_telescoping_g<KID, F64, 8><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited);
+    else
+      k_telescoping_g<KID, F64, 32><<<grid_for(th, 128), 128, 0, s>>>(V, t->pre2lo, t->n, q, n, kp, (O*)out, visited);
   });
 }
 
