@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(kBlock, FSB_STO_MINB)
 //    committing once its roulette fails; the walk ends when no lane is alive.
 //    No queue, no sort, no result slots: residuals accumulate in (a, s) order.
 #ifndef FSB_WARP_BLOCK
-#define FSB_WARP_BLOCK 256  // (512: 0.643 vs 0.483 ms on C4 since the per-warp child staging)
+#define FSB_WARP_BLOCK 512  // with 2 blocks/SM: 0.476 vs 0.482 ms at 256 x 4 (same bits)
 #endif
 constexpr int kWarpBlock = FSB_WARP_BLOCK;
 #ifdef FSB_WARP_STATS
@@ -834,7 +834,7 @@ __device__ unsigned long long g_warp_stats[8];
 #define WSTAT(i, v)
 #endif
 #ifndef FSB_WARP_MINB
-#define FSB_WARP_MINB 4
+#define FSB_WARP_MINB (1024 / FSB_WARP_BLOCK)  // 1024 threads/SM: 64 registers
 #endif
 
 #ifndef FSB_WARP_STAGE_KIDS
