@@ -23,9 +23,15 @@ kern = fs.KernelSpec("coulomb")
 cases = [("C1", c1, q1)] + [(f"C4[{n}]", src4, dev.to_device(qs4.positions[:n].copy())) for n in (1000, 16384)]
 for name, src, q in cases:
     t4, t2 = fs.build_tree(src, 4), fs.build_tree(src, 2)
-    for label, cfg, t in (("sto f64", fs.EstimatorConfig("stochastic", seed=1), t4),
-                          ("sto f32", fs.EstimatorConfig("stochastic", seed=1, precision="f32"), t4),
-                          ("bh f64", fs.EstimatorConfig("barnes_hut", beta=2.0), t2)):
+    cases_k = (("sto f64", fs.EstimatorConfig("stochastic", seed=1), t4),
+               ("sto f32", fs.EstimatorConfig("stochastic", seed=1, precision="f32"), t4),
+               ("sto f32 warp", fs.EstimatorConfig("stochastic", seed=1, precision="f32",
+                                                   rng_sharing="warp"), t4),
+               ("bh f64", fs.EstimatorConfig("barnes_hut", beta=2.0), t2))
+    only = os.environ.get("ONLY")
+    for label, cfg, t in cases_k:
+        if only and label != only:
+            continue
         for _ in range(3):
             evaluate_field_device(cfg, src, kern, q, t)
         torch.cuda.synchronize()
@@ -35,4 +41,5 @@ for name, src, q in cases:
             evaluate_field_device(cfg, src, kern, q, t)
         b.record()
         torch.cuda.synchronize()
-        print(f"{name:>10} {label}: {a.elapsed_time(b) / 10:.3f} ms", flush=True)
+        print(f"{os.path.basename(os.environ.get('FSB_LIB', 'default')):>10} {name:>10} {label}: "
+              f"{a.elapsed_time(b) / 10:.3f} ms", flush=True)
