@@ -157,6 +157,17 @@ __global__ void k_gather_key(const uint64_t* __restrict__ kw, const int32_t* __r
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b < m) out[b] = kw[perm[b]];
 }
+// the same for the sorted positions whose first word ties with a neighbour's
+// (the others are never read: 0)
+__global__ void k_gather_key_tied(const uint64_t* __restrict__ kw, const int32_t* __restrict__ perm,
+                                  const uint64_t* __restrict__ w0s, int64_t m,
+                                  uint64_t* __restrict__ out) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= m) return;
+  const uint64_t k = w0s[b];
+  const bool tied = (b > 0 && w0s[b - 1] == k) || (b + 1 < m && w0s[b + 1] == k);
+  out[b] = tied ? kw[perm[b]] : 0ull;
+}
 
 // Runs of equal first key words after the stable sort by word 0: each run's
 // permutation is insertion-sorted (stable) by the remaining words, which gives
@@ -697,9 +708,20 @@ int build_tree(FsTree** out, const double* pos, const double* masses, const doub
         std::swap(perm, perm2);
       }
     }
-    for (int w = 0; w < W; ++w)
-      k_gather_key<<<grid_for(m, B), B, 0, s>>>(keys.as<uint64_t>() + (int64_t)w * m, perm, m,
-                                                skeys.as<uint64_t>() + (int64_t)w * m);
+    if (full) {
+      for (int w = 0; w < W; ++w)
+        k_gather_key<<<grid_for(m, B), B, 0, s>>>(keys.as<uint64_t>() + (int64_t)w * m, perm, m,
+                                                  skeys.as<uint64_t>() + (int64_t)w * m);
+    } else {
+      // the sorted first words are kw_s (the refinement only permutes within runs
+      // of equal first words); the deeper words are gathered for tied points only,
+      // the only ones whose deeper words are ever compared
+      FS_CK(cudaMemcpyAsync(skeys.p, kw_s.p, sizeof(uint64_t) * m, cudaMemcpyDeviceToDevice, s));
+      for (int w = 1; w < W; ++w)
+        k_gather_key_tied<<<grid_for(m, B), B, 0, s>>>(keys.as<uint64_t>() + (int64_t)w * m, perm,
+                                                       kw_s.as<uint64_t>(), m,
+                                                       skeys.as<uint64_t>() + (int64_t)w * m);
+    }
   } else {
     FS_CK(cudaMemsetAsync(skeys.p, 0, sizeof(uint64_t) * W * m, s));
   }
