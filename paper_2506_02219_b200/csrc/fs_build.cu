@@ -174,6 +174,9 @@ __global__ void k_gather_key_tied(const uint64_t* __restrict__ kw, const int32_t
 // the full multi-word stable order.  A run longer than kMaxTieRun (duplicate-
 // heavy inputs) sets *overflow and the caller runs the full LSD sort instead.
 constexpr int kMaxTieRun = 64;
+#ifndef FSB_GEOM_FROM_KEYS
+#define FSB_GEOM_FROM_KEYS 1  // node cell mins from the sorted keys' digits (no divisions)
+#endif
 #ifndef FSB_LEVEL_SORT_FULL
 #define FSB_LEVEL_SORT_FULL 0  // 1: the level-order sort over (depth, begin) bits
 #endif
@@ -367,6 +370,7 @@ __global__ void k_permute(const double* __restrict__ pos, const double* __restri
 
 __global__ void k_node_geom(const int32_t* __restrict__ nb, const int32_t* __restrict__ nd,
                             const int64_t* __restrict__ nend, const double* __restrict__ pts,
+                            const uint64_t* __restrict__ sk,
                             const double* __restrict__ csz, const double* __restrict__ sides,
                             Geo g, int64_t n, const int32_t* __restrict__ off, int64_t m,
                             double* __restrict__ bmin, double* __restrict__ bmax,
@@ -377,9 +381,28 @@ __global__ void k_node_geom(const int32_t* __restrict__ nb, const int32_t* __res
   if (id >= n) return;
   int64_t b = nb[id], e = nend[id];
   int l = nd[id];
-  double p[3] = {pts[3 * b], pts[3 * b + 1], pts[3 * b + 2]};
   double cmin[3] = {g.rmin[0], g.rmin[1], g.rmin[2]};
+#if FSB_GEOM_FROM_KEYS
+  // the cell-min recurrence (octree.py:193) from the node's first point's key
+  // digits, which k_keys computed with the same recurrence: the same additions,
+  // without re-deriving each digit by division.  (A node deeper than the first
+  // key word has >= 2 points sharing that word, so its first point's deeper
+  // words were computed: k_keys_tied.)
+  (void)pts;
+  const uint64_t mask = (1ull << g.bpl) - 1ull;
+  for (int k = 0; k < l; ++k) {
+    const int w = k / g.dpw, tt = k - w * g.dpw;
+    const int dig = (int)((sk[(int64_t)w * m + b] >> (64 - (tt + 1) * g.bpl)) & mask);
+    const int r[3] = {dig / (g.d * g.d), (dig / g.d) % g.d, dig % g.d};
+    const double cs = csz[k];
+#pragma unroll
+    for (int kk = 0; kk < 3; ++kk) cmin[kk] = __dadd_rn(cmin[kk], __dmul_rn((double)r[kk], cs));
+  }
+#else
+  (void)sk;
+  double p[3] = {pts[3 * b], pts[3 * b + 1], pts[3 * b + 2]};
   for (int k = 0; k < l; ++k) digit_step(p, cmin, csz[k], g.d);
+#endif
   double side = sides[l];
   for (int k = 0; k < 3; ++k) {
     bmin[3 * id + k] = cmin[k];
@@ -773,7 +796,8 @@ int build_tree(FsTree** out, const double* pos, const double* masses, const doub
   k_permute<<<grid_for(m, B), B, 0, s>>>(pos, masses, weights, perm, m, c, t->points, t->masses,
                                          t->weights, t->perm);
   // -------- geometry, skip links
-  k_node_geom<<<grid_for(n, 128), 128, 0, s>>>(nb, nd, t->end, t->points, dcsz.as<double>(),
+  k_node_geom<<<grid_for(n, 128), 128, 0, s>>>(nb, nd, t->end, t->points, skeys.as<uint64_t>(),
+                                               dcsz.as<double>(),
                                                dsides.as<double>(), g, n, off.as<int32_t>(), m,
                                                t->bbox_min, t->bbox_max, t->diameter, t->begin,
                                                t->end, t->depth, t->skip);
