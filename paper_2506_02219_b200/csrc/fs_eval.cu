@@ -143,9 +143,6 @@ __device__ __forceinline__ bool far_parity(double cx, double cy, double cz, doub
 #ifdef FSB_BH_CHUNK_PROF
 __device__ long long* g_bh_chunk_cycles;
 #endif
-#ifndef FSB_BH_PIPELINE
-#define FSB_BH_PIPELINE 1  // next union node's records fetched during this node's term
-#endif
 #ifndef FSB_BH_FAR_FAST
 #define FSB_BH_FAR_FAST 1  // FP64 acceptance test without sqrt / division (exact)
 #endif
@@ -182,7 +179,7 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
 #ifdef FSB_BH_CHUNK_PROF
     long long iters = 0;
 #endif
-#if FSB_BH_PIPELINE
+    if constexpr (F64) {  // pipelined: the load overlaps the FP64 term
     // software-pipelined union walk: the next union node is known once this
     // node's accept / open decisions are made, so its records are fetched before
     // this node's term is evaluated (the load overlaps the FP64 term chain);
@@ -250,7 +247,7 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
       i = i_next;
       cur = cur_next;
     }
-#else
+    } else {  // FP32: the plain union walk (the pipelined one measured slower: the term is cheap)
     while (true) {
       uint32_t cur = warp_min_u32(i);
       if (cur >= nn) break;
@@ -313,7 +310,7 @@ __global__ void __launch_bounds__(128, FSB_BH_MINB) k_bh(const typename Prec<F64
         }
       }
     }
-#endif
+    }
     if (live) {
       out[qi] = (typename Prec<F64>::Out)acc;
       if (visited) visited[qi] = seen;
