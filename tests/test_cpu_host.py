@@ -226,3 +226,19 @@ def test_source_set_owns_its_arrays():
     pos[:] = 0.0
     assert not np.all(s.positions == 0.0)
     assert not s.positions.flags.writeable and not s.masses.flags.writeable
+
+
+def test_pipeline_slab_counts():
+    """evaluate_field's default slab count: up to 6 slabs of >= 160 K queries;
+    Barnes-Hut fewer (FP32: one -- its work-splitting rounds synchronise with the
+    host; FP64: up to three)."""
+    import paper_2506_02219_b200 as fs
+    from paper_2506_02219_b200.estimators import _pipeline_chunks
+    sto = fs.EstimatorConfig("stochastic")
+    assert _pipeline_chunks(10, sto) == 1
+    assert _pipeline_chunks(10 ** 6, sto) == 6
+    assert _pipeline_chunks(10 ** 7, sto) == 6
+    assert _pipeline_chunks(10 ** 6, fs.EstimatorConfig("barnes_hut", precision="f32")) == 1
+    assert _pipeline_chunks(10 ** 6, fs.EstimatorConfig("barnes_hut")) == 3
+    assert _pipeline_chunks(320_000, fs.EstimatorConfig("brute_force")) == 2
+    assert _pipeline_chunks(10 ** 6) == 6
